@@ -1,0 +1,418 @@
+/*
+ * asd_oracle.c -- CPU ORACLE for the active-stereo depth path of arXiv 2201.11924.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2201_11924_b200/, libasd.so) never links, imports or executes it and
+ * shares no code, header, table or constant generator with it.
+ *
+ * Plain, slow, single-threaded, scalar C99.  Build: gcc -O2 -ffp-contract=off
+ * (no -ffast-math): every float operation below is one IEEE-754 operation.
+ *
+ * What it computes ("Depth Generation by Stereo Matching";
+ * SPEC.md S:288-356 [OP] census .. disp_to_depth; readings c1-c14 of
+ * SURVEY.md §8(c), restated in DESIGN.md §3):
+ *
+ *   O1 census      CSCT bit i = I(p + o_i) > I(p - o_i)
+ *   O2 cost        C = popcount(cl(x,y) XOR cr(x-delta,y)) or nb
+ *   O3 SGM         L_r(p,d) = C + min(L_r(p-r,d), L_r(p-r,d+-1)+P1,
+ *                                     min_k L_r(p-r,k)+P2) - min_k L_r(p-r,k)
+ *                  S = sum_r L_r
+ *   O4 WTA         smallest argmin + uniqueness test
+ *   O5 sub-pixel   parabola through (d*-1, d*, d*+1)
+ *   O6 right view  same WTA/sub-pixel on S_R(x,d) = S(x+delta,d)  (reading c10)
+ *   O7 LR check    |dl - dr(x - round(dl))| <= lr
+ *   O8 depth       z = f*b/d
+ *
+ * Every function follows the definition in that order, with no blocking,
+ * fusion or reordering.  SGM is organised exactly as its definition reads:
+ * each path r decomposes the image into independent 1-D lines (rows, columns,
+ * diagonals) and the recursion runs along each line (oracle_chain).
+ *
+ * Precision: integers are exact (uint32/int64).  The sub-pixel offset is one
+ * fp32 division because its value decides an integer (the LR rounding,
+ * reading c11/c13) and the kernel decides it in fp32; the depth is fp64.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+typedef struct {
+    int32_t width, height;     /* W, H */
+    int32_t min_disp, num_disp;/* delta(d) = min_disp + d, d in [0, D) */
+    int32_t census_w, census_h;/* odd window */
+    int32_t p1, p2;            /* SGM penalties */
+    int32_t paths;             /* 4 or 8 */
+    int32_t uniqueness;        /* percent; < 0 disables */
+    float   lr_max_diff;       /* px; < 0 disables */
+    int32_t subpixel;          /* 0/1 */
+    float   focal_px, baseline_m;
+} oracle_params;
+
+/* mask bits */
+#define OM_BORDER 1u   /* census window leaves the image (c4), or no defined d (right view) */
+#define OM_UNIQUE 2u   /* uniqueness test failed (O4) */
+#define OM_LR     4u   /* left-right check failed (O7) */
+#define OM_NONPOS 8u   /* dl <= 0 (O8) */
+
+static int nbits(const oracle_params* p) { return (p->census_w * p->census_h) / 2; }
+
+static int valid_c(const oracle_params* p, int x, int y) {
+    int R = p->census_w / 2, Q = p->census_h / 2;
+    return x >= R && x < p->width - R && y >= Q && y < p->height - Q;
+}
+
+/* ---------------------------------------------------------------- O1 census
+ * CSCT: for each of the floor(w*h/2) point-symmetric pairs
+ * (p_a, p_b) around the centre, bit = I(p_a) > I(p_b), with p_a running over
+ * the window in row-major order up to (excluding) the centre.  Pair i -> bit i
+ * (LSB first, reading c1).  Pixels whose window leaves the image get 0.
+ */
+void oracle_census(const oracle_params* p, const uint8_t* img, uint64_t* out)
+{
+    int W = p->width, H = p->height, cw = p->census_w;
+    int R = p->census_w / 2, Q = p->census_h / 2, nb = nbits(p);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            uint64_t sig = 0;
+            if (valid_c(p, x, y)) {
+                for (int i = 0; i < nb; ++i) {
+                    int dy = i / cw - Q;          /* p_a = p + (dx, dy), i-th window pixel */
+                    int dx = i % cw - R;
+                    uint8_t a = img[(y + dy) * W + (x + dx)];
+                    uint8_t b = img[(y - dy) * W + (x - dx)];   /* p_b = p - (dx, dy) */
+                    if (a > b) sig |= (uint64_t)1 << i;
+                }
+            }
+            out[y * W + x] = sig;
+        }
+}
+
+static int popcount64(uint64_t v) { int n = 0; while (v) { n += (int)(v & 1u); v >>= 1; } return n; }
+
+/* ------------------------------------------------------------------ O2 cost
+ * C(x,y,d) = hamming(cl[x,y], cr[x-delta,y]) ("hamming distance as the
+ * cost function").  Out of range or census border -> nb (reading c3).
+ * Layout [H][W][D], d fastest.
+ */
+void oracle_cost(const oracle_params* p, const uint64_t* cl, const uint64_t* cr, uint8_t* C)
+{
+    int W = p->width, H = p->height, D = p->num_disp, nb = nbits(p);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int d = 0; d < D; ++d) {
+                int xr = x - (p->min_disp + d);
+                int c = nb;
+                if (valid_c(p, x, y) && xr >= 0 && valid_c(p, xr, y))
+                    c = popcount64(cl[y * W + x] ^ cr[y * W + xr]);
+                C[((size_t)y * W + x) * D + d] = (uint8_t)c;
+            }
+}
+
+/* ------------------------------------------------------------- O3 one line
+ * The SGM recursion along one line of n pixels ("four-path semi-global
+ * matching (SGM) [Hirschmuller]"):
+ *   L(0,d) = C(0,d)
+ *   L(i,d) = C(i,d) + min( L(i-1,d), L(i-1,d-1)+P1, L(i-1,d+1)+P1, M+P2 ) - M,
+ *   M = min_k L(i-1,k); the d-1 / d+1 terms are omitted at the range ends.
+ * Cin and Lout are [n][D].
+ */
+void oracle_chain(int n, int D, int P1, int P2, const uint32_t* Cin, uint32_t* Lout)
+{
+    for (int i = 0; i < n; ++i) {
+        const uint32_t* c = Cin + (size_t)i * D;
+        uint32_t* l = Lout + (size_t)i * D;
+        if (i == 0) {
+            for (int d = 0; d < D; ++d) l[d] = c[d];
+            continue;
+        }
+        const uint32_t* prev = Lout + (size_t)(i - 1) * D;
+        uint32_t M = prev[0];
+        for (int k = 1; k < D; ++k) if (prev[k] < M) M = prev[k];
+        for (int d = 0; d < D; ++d) {
+            uint32_t best = prev[d];
+            if (d >= 1     && prev[d - 1] + (uint32_t)P1 < best) best = prev[d - 1] + (uint32_t)P1;
+            if (d <= D - 2 && prev[d + 1] + (uint32_t)P1 < best) best = prev[d + 1] + (uint32_t)P1;
+            if (M + (uint32_t)P2 < best) best = M + (uint32_t)P2;
+            l[d] = c[d] + best - M;
+        }
+    }
+}
+
+/* Path directions r (the traversal step; the predecessor of p is p - r).
+ * 4-path = the two horizontal and two vertical directions ("four-path";
+ * S:309); 8-path adds the four diagonals (reading c6). */
+static const int DIRS[8][2] = {
+    {+1, 0}, {-1, 0}, {0, +1}, {0, -1},     /* 4-path */
+    {+1, +1}, {-1, -1}, {+1, -1}, {-1, +1}  /* + diagonals */
+};
+
+int oracle_num_dirs(void) { return 8; }
+void oracle_dir(int i, int* rx, int* ry) { *rx = DIRS[i][0]; *ry = DIRS[i][1]; }
+
+static int inside(const oracle_params* p, int x, int y) {
+    return x >= 0 && x < p->width && y >= 0 && y < p->height;
+}
+
+/* L_r for one direction over the whole image: every line of direction r starts
+ * at a pixel whose predecessor p - r is outside the image ("first pixel of each
+ * path: L_r = C") and is walked forward with oracle_chain. */
+void oracle_sgm_path(const oracle_params* p, const uint8_t* C, int rx, int ry, uint32_t* L)
+{
+    int W = p->width, H = p->height, D = p->num_disp;
+    int nmax = W > H ? W : H;
+    uint32_t* cbuf = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nmax * D);
+    uint32_t* lbuf = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nmax * D);
+    int* xs = (int*)malloc(sizeof(int) * nmax);
+    int* ys = (int*)malloc(sizeof(int) * nmax);
+    for (int y0 = 0; y0 < H; ++y0)
+        for (int x0 = 0; x0 < W; ++x0) {
+            if (inside(p, x0 - rx, y0 - ry)) continue;   /* not the start of a line */
+            int n = 0, x = x0, y = y0;
+            while (inside(p, x, y)) {
+                xs[n] = x; ys[n] = y;
+                for (int d = 0; d < D; ++d)
+                    cbuf[(size_t)n * D + d] = C[((size_t)y * W + x) * D + d];
+                ++n; x += rx; y += ry;
+            }
+            oracle_chain(n, D, p->p1, p->p2, cbuf, lbuf);
+            for (int i = 0; i < n; ++i)
+                for (int d = 0; d < D; ++d)
+                    L[((size_t)ys[i] * W + xs[i]) * D + d] = lbuf[(size_t)i * D + d];
+        }
+    free(cbuf); free(lbuf); free(xs); free(ys);
+}
+
+/* S = sum_r L_r over the configured path set. */
+void oracle_sgm(const oracle_params* p, const uint8_t* C, uint32_t* S)
+{
+    size_t n = (size_t)p->width * p->height * p->num_disp;
+    uint32_t* L = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    memset(S, 0, sizeof(uint32_t) * n);
+    for (int r = 0; r < p->paths; ++r) {
+        oracle_sgm_path(p, C, DIRS[r][0], DIRS[r][1], L);
+        for (size_t i = 0; i < n; ++i) S[i] += L[i];
+    }
+    free(L);
+}
+
+/* S(x,y,.) for ONE pixel, computed from the raw cost volume by walking, for
+ * each path r, the line through (x,y) from its image-border start to (x,y).
+ * Same recursion (oracle_chain); used to check sampled pixels at full size. */
+void oracle_sgm_pixel_from_census(const oracle_params* p, const uint64_t* cl, const uint64_t* cr,
+                                  int x, int y, uint32_t* Sout)
+{
+    int W = p->width, H = p->height, D = p->num_disp, nb = nbits(p);
+    int nmax = W > H ? W : H;
+    uint32_t* cbuf = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nmax * D);
+    uint32_t* lbuf = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nmax * D);
+    for (int d = 0; d < D; ++d) Sout[d] = 0;
+    for (int r = 0; r < p->paths; ++r) {
+        int rx = DIRS[r][0], ry = DIRS[r][1];
+        int sx = x, sy = y, n = 1;                 /* back up to the start of the line */
+        while (inside(p, sx - rx, sy - ry)) { sx -= rx; sy -= ry; ++n; }
+        for (int i = 0; i < n; ++i) {
+            int px = sx + i * rx, py = sy + i * ry;
+            for (int d = 0; d < D; ++d) {          /* O2 restated for this pixel */
+                int xr = px - (p->min_disp + d);
+                int c = nb;
+                if (valid_c(p, px, py) && xr >= 0 && valid_c(p, xr, py))
+                    c = popcount64(cl[py * W + px] ^ cr[py * W + xr]);
+                cbuf[(size_t)i * D + d] = (uint32_t)c;
+            }
+        }
+        oracle_chain(n, D, p->p1, p->p2, cbuf, lbuf);
+        for (int d = 0; d < D; ++d) Sout[d] += lbuf[(size_t)(n - 1) * D + d];
+    }
+    free(cbuf); free(lbuf);
+}
+
+/* ------------------------------------------------- O4 + O5 on one vector
+ * WTA: d* = smallest d minimising s over the defined entries.
+ * Uniqueness ("filter out disparities that are not better than the
+ * second best match by a threshold", reading c8): invalid iff
+ *   T = {d defined : |d - d*| >= 2} is non-empty and s(d*)*(100+u) >= min_T s * 100.
+ * Sub-pixel ("quadratic curve fitting", reading c13): if on and
+ * d*-1, d*+1 are both defined, den = c- - 2c0 + c+; off = den > 0 ?
+ * (float)(c- - c+) / (float)(2 den) : 0, clamped to [-0.5, 0.5];
+ * disparity = (float)(min_disp + d*) + off.
+ * defined[d] == 0 removes d from the search (right view, O6).
+ * Returns d* (or -1 if nothing is defined); sets *unique_fail, *disp.
+ */
+static int wta_subpix(const oracle_params* p, const uint32_t* s, const uint8_t* defined,
+                      int* unique_fail, float* disp)
+{
+    int D = p->num_disp, best = -1;
+    for (int d = 0; d < D; ++d)
+        if (defined[d] && (best < 0 || s[d] < s[best])) best = d;
+    *unique_fail = 0;
+    if (best < 0) { *disp = 0.0f; return -1; }
+    if (p->uniqueness >= 0) {
+        int have = 0; uint32_t second = 0;
+        for (int d = 0; d < D; ++d) {
+            if (!defined[d] || abs(d - best) < 2) continue;
+            if (!have || s[d] < second) { second = s[d]; have = 1; }
+        }
+        if (have && (int64_t)s[best] * (100 + (int64_t)p->uniqueness) >= (int64_t)second * 100)
+            *unique_fail = 1;
+    }
+    float off = 0.0f;
+    if (p->subpixel && best >= 1 && best <= D - 2 && defined[best - 1] && defined[best + 1]) {
+        int64_t cm = s[best - 1], c0 = s[best], cp = s[best + 1];
+        int64_t den = cm - 2 * c0 + cp;
+        if (den > 0) {
+            off = (float)(cm - cp) / (float)(2 * den);
+            if (off < -0.5f) off = -0.5f;
+            if (off > 0.5f) off = 0.5f;
+        }
+    }
+    *disp = (float)(p->min_disp + best) + off;
+    return best;
+}
+
+/* O4 + O5, left view, every pixel.  mask gets OM_BORDER (reading c4) and OM_UNIQUE. */
+void oracle_wta_left(const oracle_params* p, const uint32_t* S,
+                     int16_t* dstar, uint8_t* mask, float* dl)
+{
+    int W = p->width, H = p->height, D = p->num_disp;
+    uint8_t* defined = (uint8_t*)malloc((size_t)D);
+    for (int d = 0; d < D; ++d) defined[d] = 1;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            int uf; float disp;
+            int b = wta_subpix(p, S + ((size_t)y * W + x) * D, defined, &uf, &disp);
+            uint8_t m = 0;
+            if (!valid_c(p, x, y)) m |= OM_BORDER;
+            if (uf) m |= OM_UNIQUE;
+            dstar[y * W + x] = (int16_t)b;
+            mask[y * W + x] = m;
+            dl[y * W + x] = disp;
+        }
+    free(defined);
+}
+
+/* O6 right view (reading c10 = R1, "reuses the same cost volume by
+ * re-indexing"): S_R(xr,y,d) = S(xr + delta(d), y, d), defined iff
+ * xr + delta(d) < W; then O4 + O5 over the defined d.  mask_r gets OM_BORDER
+ * when the right pixel's census window leaves the image or no d is defined. */
+void oracle_wta_right(const oracle_params* p, const uint32_t* S,
+                      int16_t* dstar_r, uint8_t* mask_r, float* dr)
+{
+    int W = p->width, H = p->height, D = p->num_disp;
+    uint32_t* sr = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)D);
+    uint8_t* defined = (uint8_t*)malloc((size_t)D);
+    for (int y = 0; y < H; ++y)
+        for (int xr = 0; xr < W; ++xr) {
+            for (int d = 0; d < D; ++d) {
+                int x = xr + p->min_disp + d;
+                defined[d] = (uint8_t)(x < W);
+                sr[d] = x < W ? S[((size_t)y * W + x) * D + d] : 0;
+            }
+            int uf; float disp;
+            int b = wta_subpix(p, sr, defined, &uf, &disp);
+            uint8_t m = 0;
+            if (!valid_c(p, xr, y) || b < 0) m |= OM_BORDER;
+            if (uf) m |= OM_UNIQUE;
+            dstar_r[y * W + xr] = (int16_t)b;
+            mask_r[y * W + xr] = m;
+            dr[y * W + xr] = disp;
+        }
+    free(sr); free(defined);
+}
+
+/* O7 + O8.  LR ("left-right consistency check", readings c11,
+ * c12): evaluated iff lr >= 0 and (mask & 3) == 0; xr = x - (int)floorf(dl +
+ * 0.5f); invalid if xr outside [0,W), mask_r(xr) != 0 or |dl - dr(xr)| > lr.
+ * Depth (reading c14): OM_NONPOS iff dl <= 0 (always evaluated);
+ * if mask == 0: disp = dl, depth = f*b/dl in fp64; else both NaN. */
+void oracle_lr_depth(const oracle_params* p, const float* dl, const float* dr,
+                     const uint8_t* mask_r, uint8_t* mask, float* disp, double* depth)
+{
+    int W = p->width, H = p->height;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t i = (size_t)y * W + x;
+            uint8_t m = mask[i];
+            float d = dl[i];
+            if (p->lr_max_diff >= 0.0f && (m & 3u) == 0) {
+                int xr = x - (int)floorf(d + 0.5f);
+                if (xr < 0 || xr >= W) m |= OM_LR;
+                else {
+                    size_t j = (size_t)y * W + xr;
+                    if (mask_r[j] != 0 || fabsf(d - dr[j]) > p->lr_max_diff) m |= OM_LR;
+                }
+            }
+            if (d <= 0.0f) m |= OM_NONPOS;
+            mask[i] = m;
+            if (m == 0) {
+                disp[i] = d;
+                depth[i] = (double)p->focal_px * (double)p->baseline_m / (double)d;
+            } else {
+                disp[i] = NAN;
+                depth[i] = NAN;
+            }
+        }
+}
+
+/* murmur3 fmix32 -- per-frame checksum of the bit-exact outputs. */
+static uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16; h *= 0x85ebca6bu; h ^= h >> 13; h *= 0xc2b2ae35u; h ^= h >> 16; return h;
+}
+uint32_t oracle_checksum(int n, const int16_t* dstar, const uint8_t* mask)
+{
+    uint32_t h = 0;
+    for (int i = 0; i < n; ++i)
+        h += fmix32(((uint32_t)i * 0x9E3779B1u) ^ ((uint32_t)(dstar[i] + 1) << 8) ^ (uint32_t)mask[i]);
+    return h;
+}
+
+/* The whole path, O1..O8 in the order of P:289 (S:366-368 compute_depth with
+ * rectification = identity for a born-rectified rig and median off).  Any of the
+ * debug outputs may be NULL.  Returns 0, or -1 on allocation failure. */
+int oracle_compute(const oracle_params* p, const uint8_t* left, const uint8_t* right,
+                   float* out_disp, double* out_depth,
+                   uint64_t* census_l, uint64_t* census_r, uint8_t* cost, uint32_t* agg,
+                   int16_t* dstar_l, int16_t* dstar_r, float* dl_out, float* dr_out,
+                   uint8_t* mask_out, uint8_t* mask_r_out)
+{
+    size_t npx = (size_t)p->width * p->height, ncell = npx * p->num_disp;
+    uint64_t* cl = (uint64_t*)malloc(sizeof(uint64_t) * npx);
+    uint64_t* cr = (uint64_t*)malloc(sizeof(uint64_t) * npx);
+    uint8_t* C = (uint8_t*)malloc(ncell);
+    uint32_t* S = (uint32_t*)malloc(sizeof(uint32_t) * ncell);
+    int16_t* dsl = (int16_t*)malloc(sizeof(int16_t) * npx);
+    int16_t* dsr = (int16_t*)malloc(sizeof(int16_t) * npx);
+    uint8_t* ml = (uint8_t*)malloc(npx);
+    uint8_t* mr = (uint8_t*)malloc(npx);
+    float* dl = (float*)malloc(sizeof(float) * npx);
+    float* dr = (float*)malloc(sizeof(float) * npx);
+    float* disp = (float*)malloc(sizeof(float) * npx);
+    double* z = (double*)malloc(sizeof(double) * npx);
+    int rc = -1;
+    if (!cl || !cr || !C || !S || !dsl || !dsr || !ml || !mr || !dl || !dr || !disp || !z) goto done;
+    oracle_census(p, left, cl);                 /* O1 */
+    oracle_census(p, right, cr);
+    oracle_cost(p, cl, cr, C);                  /* O2 */
+    oracle_sgm(p, C, S);                        /* O3 */
+    oracle_wta_left(p, S, dsl, ml, dl);         /* O4, O5 */
+    oracle_wta_right(p, S, dsr, mr, dr);        /* O6 */
+    oracle_lr_depth(p, dl, dr, mr, ml, disp, z);/* O7, O8 */
+    if (out_disp) memcpy(out_disp, disp, sizeof(float) * npx);
+    if (out_depth) memcpy(out_depth, z, sizeof(double) * npx);
+    if (census_l) memcpy(census_l, cl, sizeof(uint64_t) * npx);
+    if (census_r) memcpy(census_r, cr, sizeof(uint64_t) * npx);
+    if (cost) memcpy(cost, C, ncell);
+    if (agg) memcpy(agg, S, sizeof(uint32_t) * ncell);
+    if (dstar_l) memcpy(dstar_l, dsl, sizeof(int16_t) * npx);
+    if (dstar_r) memcpy(dstar_r, dsr, sizeof(int16_t) * npx);
+    if (dl_out) memcpy(dl_out, dl, sizeof(float) * npx);
+    if (dr_out) memcpy(dr_out, dr, sizeof(float) * npx);
+    if (mask_out) memcpy(mask_out, ml, npx);
+    if (mask_r_out) memcpy(mask_r_out, mr, npx);
+    rc = 0;
+done:
+    free(cl); free(cr); free(C); free(S); free(dsl); free(dsr); free(ml); free(mr);
+    free(dl); free(dr); free(disp); free(z);
+    return rc;
+}
