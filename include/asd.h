@@ -1,0 +1,195 @@
+/*
+ * asd.h -- C ABI of the B200-native active-stereo depth engine (libasd.so).
+ *
+ * The library implements the depth-generation stage of arXiv 2201.11924
+ * ("SimSense"): from a rectified left/right 8-bit IR pair
+ * it computes
+ *   census (CSCT)  ->  Hamming matching cost
+ *   -> semi-global path aggregation, P1/P2, 4 or 8 paths
+ *   -> winner-take-all + uniqueness test  -> quadratic sub-pixel
+ *   -> left-right consistency check       -> depth = f*b/d
+ * with the exact semantics listed in DESIGN.md §3 (readings c1-c18 of
+ * SURVEY.md §8(c); SPEC.md S:288-356 gives the operation interfaces).
+ * Rectification is the identity (born-rectified rig) and the median
+ * filter is off (reading c15).
+ *
+ * Conventions shared by every entry point
+ *   - Images are row-major [H][W] (batches [n][H][W], frames contiguous), no
+ *     row padding.  Disparity delta(d) = min_disp + d, d in [0, num_disp),
+ *     d = x_left - x_right >= 0 (reading c5).
+ *   - Outputs are float32; INVALID = quiet NaN.
+ *   - Device pointers are CUDA device (or managed) memory on the context's
+ *     device; "host" entry points take host memory (pinned memory is fastest).
+ *   - The caller owns every input/output buffer.  The context owns its scratch
+ *     (census images, aggregated-cost volume, per-view disparity temporaries),
+ *     allocated once in asd_create; no entry point allocates device memory.
+ *   - Device entry points are asynchronous on the caller's stream
+ *     (`cuda_stream` is a cudaStream_t; NULL = legacy default stream) and do
+ *     not synchronise the host.  A context must be used by one host thread and
+ *     one stream at a time; distinct contexts may run concurrently.
+ *   - Return value: ASD_OK (0) or a negative ASD_E_* code.  Argument errors are
+ *     detected synchronously before anything is enqueued.  Nothing throws
+ *     across the ABI.  asd_last_error() gives a message for the last failure.
+ */
+#ifndef ASD_H_
+#define ASD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASD_VERSION 1
+
+#define ASD_OK              0
+#define ASD_E_INVALID_ARG  (-1)  /* bad parameter, NULL required pointer, n out of range */
+#define ASD_E_UNSUPPORTED  (-2)  /* valid per SPEC but outside this engine's bounds (see asd_params) */
+#define ASD_E_CUDA         (-3)  /* CUDA launch / runtime failure; see asd_last_error */
+#define ASD_E_OOM          (-4)  /* scratch allocation failed in asd_create */
+
+/* Validity mask bits (debug output `mask`, `mask_r`). */
+#define ASD_MASK_BORDER  1u  /* census window leaves the image (reading c4); right view: no defined d */
+#define ASD_MASK_UNIQUE  2u  /* uniqueness test failed (reading c8) */
+#define ASD_MASK_LR      4u  /* left-right check failed (readings c10-c12) */
+#define ASD_MASK_NONPOS  8u  /* disparity <= 0, no depth (reading c14) */
+
+/* Stereo configuration (SPEC S:257-260 StereoConfig).  Bounds enforced by
+ * asd_create / asd_scratch_bytes:
+ *   width  >= census_w, height >= census_h, width*height <= 2^26
+ *   census_w, census_h odd, 1..15; nb = floor(census_w*census_h/2) in [1, 64]
+ *       (SPEC allows up to 112 bits; nb > 64 -> ASD_E_UNSUPPORTED)
+ *   min_disp >= 0; num_disp % 16 == 0 and 16 <= num_disp <= 256
+ *   0 <= p1 <= p2 and nb + p2 <= 255  (each path's L_r <= C + P2 fits 8 bits;
+ *       else ASD_E_UNSUPPORTED)
+ *   paths in {4, 8} (4 = horizontal + vertical, 8 adds the diagonals, reading c6)
+ *   uniqueness: percent, < 0 disables the test; <= 100000
+ *   lr_max_diff: px, < 0 disables the LR check; not NaN
+ *   subpixel: 0 or 1
+ *   focal_px, baseline_m: finite, > 0; depth = fb / disparity with
+ *       fb = (float)((double)focal_px * (double)baseline_m) */
+typedef struct asd_params {
+    int32_t width, height;
+    int32_t min_disp, num_disp;
+    int32_t census_w, census_h;
+    int32_t p1, p2;
+    int32_t paths;
+    int32_t uniqueness;
+    float   lr_max_diff;
+    int32_t subpixel;
+    float   focal_px, baseline_m;
+} asd_params;
+
+/* Per-frame statistics; exact integers except depth_sum.
+ *   checksum  = sum over pixels p (row-major index) of
+ *               fmix32((p * 0x9E3779B1) ^ ((uint32)(dstar_l(p) + 1) << 8) ^ mask(p))  mod 2^32
+ *               (fmix32 = murmur3 finaliser; dstar_l = raw left argmin index d*)
+ *   valid     = number of pixels with mask == 0
+ *   depth_sum = sum of valid depths (float32 atomics: order-dependent low bits) */
+typedef struct asd_frame_stats {
+    uint32_t checksum;
+    uint32_t valid;
+    float    depth_sum;
+    uint32_t reserved;
+} asd_frame_stats;
+
+/* Stage outputs for parity testing (asd_depth_debug).  Every pointer is a
+ * device pointer and may be NULL (not produced).
+ *   census_l/r : [H][W] uint32 if nb <= 32 else uint64; 0 at census borders
+ *   cost       : [H][W][D] uint8, C(x,y,d) (materialised only here)
+ *   agg        : [H][W][D] uint16, S = sum_r L_r
+ *   dstar_l/r  : [H][W] int16, raw argmin d (right view: -1 if no d defined)
+ *   disp_l/r   : [H][W] float, dl / dr after sub-pixel, before masking
+ *   mask       : [H][W] uint8, final left mask (ASD_MASK_* bits)
+ *   mask_r     : [H][W] uint8, right-view mask (BORDER | UNIQUE)           */
+typedef struct asd_debug_out {
+    void*     census_l;
+    void*     census_r;
+    uint8_t*  cost;
+    uint16_t* agg;
+    int16_t*  dstar_l;
+    int16_t*  dstar_r;
+    float*    disp_l;
+    float*    disp_r;
+    uint8_t*  mask;
+    uint8_t*  mask_r;
+} asd_debug_out;
+
+typedef struct asd_ctx asd_ctx;
+
+/* Library version (ASD_VERSION). */
+int asd_version(void);
+
+/* Device scratch asd_create(p, ., max_batch, .) will allocate, in bytes;
+ * 0 if the parameters are rejected. */
+size_t asd_scratch_bytes(const asd_params* p, int max_batch);
+
+/* Validate p, bind `device`, allocate scratch for up to `max_batch` frames in
+ * flight (1..1024; asd_depth_batch processes larger n in chunks of max_batch).
+ * On success *out owns the scratch; release it with asd_destroy. */
+int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out);
+
+/* Free the context and its scratch (synchronises the device first).  NULL ok. */
+void asd_destroy(asd_ctx* ctx);
+
+/* One frame: left/right u8 [H][W] -> out_disp, out_depth f32 [H][W].
+ * Either output may be NULL (not written). */
+int asd_depth(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
+              float* out_disp, float* out_depth, void* cuda_stream);
+
+/* n frames (n >= 0), [n][H][W] each; stats ([n] asd_frame_stats) may be NULL. */
+int asd_depth_batch(asd_ctx* ctx, int n, const uint8_t* left, const uint8_t* right,
+                    float* out_disp, float* out_depth, asd_frame_stats* stats,
+                    void* cuda_stream);
+
+/* End-to-end variant over HOST buffers: copies each chunk host->device,
+ * computes, copies results device->host, overlapping the copies of one chunk
+ * with the compute of the next.  Synchronous: returns after all results are in
+ * host memory.  Outputs/stats may be NULL. */
+int asd_depth_batch_host(asd_ctx* ctx, int n, const uint8_t* left_host, const uint8_t* right_host,
+                         float* out_disp_host, float* out_depth_host,
+                         asd_frame_stats* stats_host, void* cuda_stream);
+
+/* One frame with stage outputs (see asd_debug_out); out_disp/out_depth via
+ * asd_depth semantics may additionally be requested. */
+int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                    const asd_debug_out* outs, float* out_disp, float* out_depth,
+                    void* cuda_stream);
+
+/* Number of kernel launches one asd_depth_batch call of n frames enqueues. */
+int asd_launches_per_batch(const asd_ctx* ctx, int n);
+
+/* ---- live stage timing (CUDA events on the caller's stream) ----
+ * asd_profile_begin(ctx, max_launches) pre-creates events for up to
+ * max_launches kernel launches; from then on every launch the context enqueues
+ * is bracketed by an event pair on the launching stream (no host sync).
+ * asd_profile_end synchronises on those events and fills `out` with, per
+ * stage, the summed device time, the number of launches, and the ALGORITHMIC
+ * bytes those launches must move at minimum (DESIGN.md §6 per-unit figures x
+ * units processed), then stops profiling.  Launches beyond max_launches are
+ * counted in `dropped` and not timed. */
+#define ASD_STAGE_CENSUS 0   /* K1 */
+#define ASD_STAGE_AGG    1   /* SGM path aggregation kernels */
+#define ASD_STAGE_WTA    2   /* K4 */
+#define ASD_STAGE_LR     3   /* K5 */
+#define ASD_STAGE_COUNT  4
+typedef struct asd_stage_times {
+    double ms[ASD_STAGE_COUNT];
+    double alg_bytes[ASD_STAGE_COUNT];
+    int32_t launches[ASD_STAGE_COUNT];
+    int32_t dropped;
+    int32_t reserved;
+} asd_stage_times;
+
+int asd_profile_begin(asd_ctx* ctx, int max_launches);
+int asd_profile_end(asd_ctx* ctx, asd_stage_times* out);
+
+/* Static strings; never NULL. */
+const char* asd_strerror(int code);
+const char* asd_last_error(const asd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASD_H_ */

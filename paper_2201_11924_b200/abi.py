@@ -1,0 +1,202 @@
+"""Thin ctypes binding of libasd.so (include/asd.h).  Argument marshalling only:
+every step of the depth path runs in the library's sm_100a kernels.
+
+Names mirror the C ABI: ``asd_create`` / ``asd_depth`` / ``asd_depth_batch`` /
+``asd_depth_batch_host`` / ``asd_depth_debug`` / ``asd_destroy`` are wrapped by
+:class:`Stereo`.  Tensors are passed as raw pointers (``tensor.data_ptr()``)
+together with torch's current CUDA stream; this module never computes anything
+itself, and it raises if the library is missing (there is no fallback path).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libasd.so")
+
+ASD_OK, ASD_E_INVALID_ARG, ASD_E_UNSUPPORTED, ASD_E_CUDA, ASD_E_OOM = 0, -1, -2, -3, -4
+MASK_BORDER, MASK_UNIQUE, MASK_LR, MASK_NONPOS = 1, 2, 4, 8
+
+
+class AsdError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"asd error {code}: {msg}")
+        self.code = code
+
+
+class asd_params(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("min_disp", ctypes.c_int32), ("num_disp", ctypes.c_int32),
+                ("census_w", ctypes.c_int32), ("census_h", ctypes.c_int32),
+                ("p1", ctypes.c_int32), ("p2", ctypes.c_int32),
+                ("paths", ctypes.c_int32), ("uniqueness", ctypes.c_int32),
+                ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
+                ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float)]
+
+
+class asd_frame_stats(ctypes.Structure):
+    _fields_ = [("checksum", ctypes.c_uint32), ("valid", ctypes.c_uint32),
+                ("depth_sum", ctypes.c_float), ("reserved", ctypes.c_uint32)]
+
+
+class asd_debug_out(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("census_l", "census_r", "cost", "agg", "dstar_l", "dstar_r",
+                 "disp_l", "disp_r", "mask", "mask_r")]
+
+
+STAGES = ("census", "agg", "wta", "lr")
+
+
+class asd_stage_times(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 4), ("alg_bytes", ctypes.c_double * 4),
+                ("launches", ctypes.c_int32 * 4), ("dropped", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+# (name, restype, argtypes) of every exported symbol declared in include/asd.h
+_VP, _I, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+SYMBOLS = [
+    ("asd_version", _I, []),
+    ("asd_scratch_bytes", _SZ, [ctypes.POINTER(asd_params), _I]),
+    ("asd_create", _I, [ctypes.POINTER(asd_params), _I, _I, ctypes.POINTER(_VP)]),
+    ("asd_destroy", None, [_VP]),
+    ("asd_depth", _I, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    ("asd_depth_batch", _I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
+    ("asd_depth_batch_host", _I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
+    ("asd_depth_debug", _I, [_VP, _VP, _VP, ctypes.POINTER(asd_debug_out), _VP, _VP, _VP]),
+    ("asd_launches_per_batch", _I, [_VP, _I]),
+    ("asd_profile_begin", _I, [_VP, _I]),
+    ("asd_profile_end", _I, [_VP, ctypes.POINTER(asd_stage_times)]),
+    ("asd_strerror", ctypes.c_char_p, [_I]),
+    ("asd_last_error", ctypes.c_char_p, [_VP]),
+]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libasd.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not found: build it with "
+                              "`python -m paper_2201_11924_b200.build` (no CPU fallback exists)")
+        lib = ctypes.CDLL(path)
+        for name, res, args in SYMBOLS:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+@dataclass
+class Params:
+    """asd_params (include/asd.h; SPEC S:257-260 StereoConfig, defaults)."""
+    width: int
+    height: int
+    num_disp: int = 64
+    min_disp: int = 0
+    census_w: int = 9
+    census_h: int = 7
+    p1: int = 8
+    p2: int = 32
+    paths: int = 8
+    uniqueness: int = 10
+    lr_max_diff: float = 1.0
+    subpixel: int = 1
+    focal_px: float = 430.0
+    baseline_m: float = 0.055
+
+    def c(self) -> asd_params:
+        return asd_params(self.width, self.height, self.min_disp, self.num_disp, self.census_w,
+                          self.census_h, self.p1, self.p2, self.paths, self.uniqueness,
+                          self.lr_max_diff, self.subpixel, self.focal_px, self.baseline_m)
+
+    @property
+    def nbits(self) -> int:
+        return (self.census_w * self.census_h) // 2
+
+
+def _check(rc: int, ctx=None):
+    if rc != ASD_OK:
+        lib = load()
+        msg = lib.asd_last_error(ctx).decode() if ctx is not None else lib.asd_last_error(None).decode()
+        raise AsdError(rc, f"{lib.asd_strerror(rc).decode()}: {msg}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def scratch_bytes(params: Params, max_batch: int = 1) -> int:
+    return int(load().asd_scratch_bytes(ctypes.byref(params.c()), max_batch))
+
+
+class Stereo:
+    """One libasd context (asd_create ... asd_destroy) bound to a CUDA device."""
+
+    def __init__(self, params: Params, device: int = 0, max_batch: int = 1):
+        self.params = params
+        self.device = device
+        self.max_batch = max_batch
+        self._lib = load()
+        ctx = ctypes.c_void_p()
+        _check(self._lib.asd_create(ctypes.byref(params.c()), device, max_batch, ctypes.byref(ctx)))
+        self._ctx = ctx
+
+    def close(self):
+        if getattr(self, "_ctx", None) is not None and self._ctx.value:
+            self._lib.asd_destroy(self._ctx)
+        self._ctx = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- device entry points (torch CUDA tensors) ----
+    def asd_depth(self, left, right, out_disp=None, out_depth=None, stream=None):
+        _check(self._lib.asd_depth(self._ctx, _ptr(left), _ptr(right), _ptr(out_disp),
+                                   _ptr(out_depth), _stream(stream)), self._ctx)
+
+    def asd_depth_batch(self, left, right, out_disp=None, out_depth=None, stats=None, stream=None):
+        n = left.shape[0]
+        _check(self._lib.asd_depth_batch(self._ctx, n, _ptr(left), _ptr(right), _ptr(out_disp),
+                                         _ptr(out_depth), _ptr(stats), _stream(stream)), self._ctx)
+
+    def asd_depth_debug(self, left, right, outs: dict, out_disp=None, out_depth=None, stream=None):
+        d = asd_debug_out(**{k: (v.data_ptr() if v is not None else None) for k, v in outs.items()})
+        _check(self._lib.asd_depth_debug(self._ctx, _ptr(left), _ptr(right), ctypes.byref(d),
+                                         _ptr(out_disp), _ptr(out_depth), _stream(stream)), self._ctx)
+
+    # ---- host entry point (CPU tensors, ideally pinned) ----
+    def asd_depth_batch_host(self, left, right, out_disp=None, out_depth=None, stats=None, stream=None):
+        n = left.shape[0]
+        _check(self._lib.asd_depth_batch_host(self._ctx, n, _ptr(left), _ptr(right), _ptr(out_disp),
+                                              _ptr(out_depth), _ptr(stats), _stream(stream)), self._ctx)
+
+    def profile_begin(self, max_launches: int = 65536):
+        _check(self._lib.asd_profile_begin(self._ctx, max_launches), self._ctx)
+
+    def profile_end(self) -> dict:
+        t = asd_stage_times()
+        _check(self._lib.asd_profile_end(self._ctx, ctypes.byref(t)), self._ctx)
+        return {name: {"ms": t.ms[i], "alg_bytes": t.alg_bytes[i], "launches": t.launches[i]}
+                for i, name in enumerate(STAGES)} | {"dropped": t.dropped}
+
+    def launches_per_batch(self, n: int) -> int:
+        return int(self._lib.asd_launches_per_batch(self._ctx, n))

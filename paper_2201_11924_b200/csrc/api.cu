@@ -1,0 +1,527 @@
+// api.cu -- the C ABI of libasd (include/asd.h): parameter validation, scratch
+// ownership, launch sequencing of the sm_100a kernels, host<->device pipeline.
+//
+// Stage order per chunk of frames (PAPER.md P:289 stage list; rectification is
+// the identity for a born-rectified rig and the median filter is off,
+// DESIGN.md §3 readings c15/c16):
+//   K1 census(L), census(R)                               census.cu
+//   SGM aggregation, one launch per path direction         sgm_dir.cu   (design D1)
+//   K4 WTA + uniqueness + sub-pixel, left and right view   post.cu
+//   K5 LR check + depth (+ per-frame stats)                post.cu
+// Every step runs in these kernels; the host only validates and enqueues.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "asd.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace asd;
+
+struct asd_ctx {
+    asd_params prm;
+    DevParams dp;
+    int device = 0;
+    int max_batch = 1;
+    size_t sig_bytes = 4;
+    // scratch (max_batch frame slots)
+    void* census_l = nullptr;
+    void* census_r = nullptr;
+    uint16_t* S = nullptr;
+    float* dl = nullptr;
+    float* dr = nullptr;
+    int16_t* dstar_l = nullptr;
+    int16_t* dstar_r = nullptr;
+    uint8_t* mask_l = nullptr;
+    uint8_t* mask_r = nullptr;
+    // host-path staging: two chunk buffers (inputs u8, outputs f32) + stats
+    uint8_t* stage_in[2] = {nullptr, nullptr};     // [max_batch][2][H][W]
+    float* stage_out[2] = {nullptr, nullptr};      // [max_batch][2][H][W]
+    asd_frame_stats* stage_stats[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};
+    cudaEvent_t ev_comp[2] = {nullptr, nullptr};
+    // live stage timing (asd_profile_begin/end)
+    struct Mark { int stage; double bytes; };
+    bool prof = false;
+    std::vector<cudaEvent_t> prof_ev;   // 2 per launch
+    std::vector<Mark> prof_marks;
+    int prof_dropped = 0;
+    char err[512] = {0};
+};
+
+static thread_local char g_err[512];
+
+static void set_err(asd_ctx* c, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) snprintf(c->err, sizeof c->err, "%s", buf);
+    snprintf(g_err, sizeof g_err, "%s", buf);
+}
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+int validate(const asd_params* p, char* why, size_t n)
+{
+    if (!p) { snprintf(why, n, "params is NULL"); return ASD_E_INVALID_ARG; }
+    if (p->census_w < 1 || p->census_h < 1 || !(p->census_w & 1) || !(p->census_h & 1)) {
+        snprintf(why, n, "census_w/census_h must be odd and >= 1 (got %d x %d)", p->census_w, p->census_h);
+        return ASD_E_INVALID_ARG;
+    }
+    if (p->census_w > 15 || p->census_h > 15) {
+        snprintf(why, n, "census window %dx%d exceeds 15x15", p->census_w, p->census_h);
+        return ASD_E_UNSUPPORTED;
+    }
+    const int nb = (p->census_w * p->census_h) / 2;
+    if (nb < 1) { snprintf(why, n, "census window must have >= 1 pair"); return ASD_E_INVALID_ARG; }
+    if (nb > 64) { snprintf(why, n, "census bits nb=%d > 64", nb); return ASD_E_UNSUPPORTED; }
+    if (p->width < p->census_w || p->height < p->census_h) {
+        snprintf(why, n, "image %dx%d smaller than census window", p->width, p->height);
+        return ASD_E_INVALID_ARG;
+    }
+    if ((long long)p->width * p->height > (1ll << 26)) {
+        snprintf(why, n, "image %dx%d too large", p->width, p->height);
+        return ASD_E_UNSUPPORTED;
+    }
+    if (p->min_disp < 0) { snprintf(why, n, "min_disp must be >= 0"); return ASD_E_INVALID_ARG; }
+    if (p->num_disp < 1) { snprintf(why, n, "num_disp must be >= 1"); return ASD_E_INVALID_ARG; }
+    if (p->num_disp % 16 != 0 || p->num_disp < 16 || p->num_disp > 256) {
+        snprintf(why, n, "num_disp=%d: need a multiple of 16 in [16, 256]", p->num_disp);
+        return ASD_E_UNSUPPORTED;
+    }
+    if (p->min_disp > (1 << 20)) { snprintf(why, n, "min_disp too large"); return ASD_E_INVALID_ARG; }
+    if (p->p1 < 0 || p->p2 < p->p1) {
+        snprintf(why, n, "need 0 <= p1 <= p2 (got p1=%d p2=%d)", p->p1, p->p2);
+        return ASD_E_INVALID_ARG;
+    }
+    if (nb + p->p2 > 255) {
+        snprintf(why, n, "nb + p2 = %d > 255 (per-path cost must fit 8 bits)", nb + p->p2);
+        return ASD_E_UNSUPPORTED;
+    }
+    if (p->paths != 4 && p->paths != 8) {
+        snprintf(why, n, "paths must be 4 or 8 (got %d)", p->paths);
+        return ASD_E_INVALID_ARG;
+    }
+    if (p->uniqueness > 100000) { snprintf(why, n, "uniqueness > 100000"); return ASD_E_INVALID_ARG; }
+    if (std::isnan(p->lr_max_diff)) { snprintf(why, n, "lr_max_diff is NaN"); return ASD_E_INVALID_ARG; }
+    if (p->subpixel != 0 && p->subpixel != 1) { snprintf(why, n, "subpixel must be 0/1"); return ASD_E_INVALID_ARG; }
+    if (!(std::isfinite(p->focal_px) && p->focal_px > 0.0f) ||
+        !(std::isfinite(p->baseline_m) && p->baseline_m > 0.0f)) {
+        snprintf(why, n, "focal_px and baseline_m must be finite and > 0");
+        return ASD_E_INVALID_ARG;
+    }
+    return ASD_OK;
+}
+
+DevParams make_dev(const asd_params* p)
+{
+    DevParams d{};
+    d.W = p->width; d.H = p->height;
+    d.min_disp = p->min_disp; d.D = p->num_disp;
+    d.cw = p->census_w; d.ch = p->census_h;
+    d.R = p->census_w / 2; d.Q = p->census_h / 2;
+    d.nb = (p->census_w * p->census_h) / 2;
+    d.p1 = p->p1; d.p2 = p->p2;
+    d.paths = p->paths;
+    d.uniq = p->uniqueness;
+    d.lr = p->lr_max_diff;
+    d.subpix = p->subpixel;
+    d.fb = (float)((double)p->focal_px * (double)p->baseline_m);
+    d.npx = (long long)p->width * p->height;
+    d.ncell = d.npx * p->num_disp;
+    return d;
+}
+
+struct Layout {
+    size_t sig, s, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
+};
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+Layout layout(const DevParams& d, int max_batch)
+{
+    Layout L{};
+    const size_t B = (size_t)max_batch;
+    L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
+    L.s = align_up(B * d.ncell * 2);
+    L.px_f32 = align_up(B * d.npx * 4);
+    L.px_i16 = align_up(B * d.npx * 2);
+    L.px_u8 = align_up(B * d.npx);
+    L.stage_in = align_up(B * d.npx * 2);
+    L.stage_out = align_up(B * d.npx * 2 * 4);
+    L.stats = align_up(B * sizeof(asd_frame_stats));
+    L.total = 2 * L.sig + L.s + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
+              2 * (L.stage_in + L.stage_out + L.stats);
+    return L;
+}
+
+// Direction table r = (rx, ry): the traversal step; 4-path = horizontal and
+// vertical, 8-path adds the diagonals ("four-path"; reading c6).
+const int kDirs[8][2] = {{+1, 0}, {-1, 0}, {0, +1}, {0, -1}, {+1, +1}, {-1, -1}, {+1, -1}, {-1, +1}};
+
+FrameScratch frame_scratch(asd_ctx* c)
+{
+    FrameScratch fs;
+    fs.census_l = c->census_l; fs.census_r = c->census_r; fs.S = c->S;
+    fs.dl = c->dl; fs.dr = c->dr; fs.dstar_l = c->dstar_l; fs.dstar_r = c->dstar_r;
+    fs.mask_l = c->mask_l; fs.mask_r = c->mask_r;
+    return fs;
+}
+
+// Bracket one kernel launch with an event pair when profiling is on.
+struct ProfScope {
+    asd_ctx* c; cudaStream_t s; int idx = -1;
+    ProfScope(asd_ctx* c_, cudaStream_t s_, int stage, double bytes) : c(c_), s(s_) {
+        if (!c->prof) return;
+        const size_t k = c->prof_marks.size();
+        if (2 * k + 1 >= c->prof_ev.size()) { ++c->prof_dropped; return; }
+        idx = (int)k;
+        c->prof_marks.push_back({stage, bytes});
+        cudaEventRecord(c->prof_ev[2 * k], s);
+    }
+    ~ProfScope() { if (idx >= 0) cudaEventRecord(c->prof_ev[2 * idx + 1], s); }
+};
+
+// Algorithmic bytes: the minimum HBM traffic each kernel's job
+// implies, per frame.  Census: read 1 B/px, write sig B/px (two views).
+// Aggregation (design D1, one direction per launch): read+write the u16 S
+// volume (4 B/cell), the first direction only writes it (2 B/cell); census
+// reads are L2-resident and excluded.  WTA: read S once (2 B/cell) and write
+// dl, dr (f32), d* (i16) and masks (u8) for both views.  LR: read those per-
+// pixel maps once, write disp and depth (f32).
+static double alg_bytes_census(const DevParams& p, size_t sig) { return 2.0 * p.npx * (1 + sig); }
+static double alg_bytes_dir(const DevParams& p, bool first) { return (first ? 2.0 : 4.0) * p.ncell; }
+static double alg_bytes_wta(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * (4 + 2 + 1); }
+static double alg_bytes_lr(const DevParams& p) { return p.npx * (2 * (4 + 1) + 2 + 2 * 4.0); }
+
+// Enqueue the whole path for n <= max_batch frames resident on the device.
+int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
+              float* out_disp, float* out_depth, asd_frame_stats* stats,
+              uint8_t* mask_out, cudaStream_t s)
+{
+    const DevParams& p = c->dp;
+    if (n <= 0) return ASD_OK;
+    const long long npx = p.npx;
+    {
+        ProfScope ps(c, s, ASD_STAGE_CENSUS, n * alg_bytes_census(p, c->sig_bytes));
+        launch_census(p, n, left, right, npx, c->census_l, c->census_r, npx, s);
+    }
+    for (int r = 0; r < p.paths; ++r) {
+        ProfScope ps(c, s, ASD_STAGE_AGG, n * alg_bytes_dir(p, r == 0));
+        if (!launch_sgm_dir(p, n, kDirs[r][0], kDirs[r][1], r == 0, c->census_l, c->census_r, npx,
+                            c->S, p.ncell, s)) {
+            set_err(c, "no SGM kernel instance for num_disp=%d", p.D);
+            return ASD_E_UNSUPPORTED;
+        }
+    }
+    FrameScratch fs = frame_scratch(c);
+    {
+        ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta(p));
+        if (!launch_wta(p, n, c->S, p.ncell, fs, npx, s)) {
+            set_err(c, "no WTA kernel instance for num_disp=%d", p.D);
+            return ASD_E_UNSUPPORTED;
+        }
+    }
+    if (stats) cudaMemsetAsync(stats, 0, sizeof(asd_frame_stats) * n, s);
+    {
+        ProfScope ps(c, s, ASD_STAGE_LR, n * alg_bytes_lr(p));
+        launch_lr_depth(p, n, fs, npx, out_disp, out_depth, npx, mask_out, stats, s);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_err(c, "CUDA launch failed: %s", cudaGetErrorString(e));
+        return ASD_E_CUDA;
+    }
+    return ASD_OK;
+}
+
+void free_ctx(asd_ctx* c)
+{
+    if (!c) return;
+    void* ptrs[] = {c->census_l, c->census_r, c->S, c->dl, c->dr, c->dstar_l, c->dstar_r,
+                    c->mask_l, c->mask_r, c->stage_in[0], c->stage_in[1], c->stage_out[0],
+                    c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
+    for (void* q : ptrs) if (q) cudaFree(q);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+        if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+    delete c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int asd_version(void) { return ASD_VERSION; }
+
+const char* asd_strerror(int code)
+{
+    switch (code) {
+        case ASD_OK: return "ok";
+        case ASD_E_INVALID_ARG: return "invalid argument";
+        case ASD_E_UNSUPPORTED: return "unsupported configuration";
+        case ASD_E_CUDA: return "CUDA error";
+        case ASD_E_OOM: return "out of device memory";
+        default: return "unknown error";
+    }
+}
+
+const char* asd_last_error(const asd_ctx* ctx) { return ctx ? ctx->err : g_err; }
+
+size_t asd_scratch_bytes(const asd_params* p, int max_batch)
+{
+    char why[256];
+    if (validate(p, why, sizeof why) != ASD_OK || max_batch < 1 || max_batch > 1024) return 0;
+    return layout(make_dev(p), max_batch).total;
+}
+
+int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
+{
+    char why[256];
+    if (!out) { set_err(nullptr, "out is NULL"); return ASD_E_INVALID_ARG; }
+    *out = nullptr;
+    int rc = validate(p, why, sizeof why);
+    if (rc != ASD_OK) { set_err(nullptr, "%s", why); return rc; }
+    if (max_batch < 1 || max_batch > 1024) { set_err(nullptr, "max_batch must be in [1, 1024]"); return ASD_E_INVALID_ARG; }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        set_err(nullptr, "device %d not available (%d CUDA devices)", device, ndev);
+        return ASD_E_CUDA;
+    }
+    DeviceGuard g(device);
+    asd_ctx* c = new (std::nothrow) asd_ctx();
+    if (!c) return ASD_E_OOM;
+    c->prm = *p;
+    c->dp = make_dev(p);
+    c->device = device;
+    c->max_batch = max_batch;
+    c->sig_bytes = c->dp.nb <= 32 ? 4 : 8;
+    const Layout L = layout(c->dp, max_batch);
+    bool ok = true;
+    auto alloc = [&](void** q, size_t bytes) {
+        if (ok && cudaMalloc(q, bytes) != cudaSuccess) ok = false;
+    };
+    alloc(&c->census_l, L.sig); alloc(&c->census_r, L.sig);
+    alloc((void**)&c->S, L.s);
+    alloc((void**)&c->dl, L.px_f32); alloc((void**)&c->dr, L.px_f32);
+    alloc((void**)&c->dstar_l, L.px_i16); alloc((void**)&c->dstar_r, L.px_i16);
+    alloc((void**)&c->mask_l, L.px_u8); alloc((void**)&c->mask_r, L.px_u8);
+    for (int i = 0; i < 2; ++i) {
+        alloc((void**)&c->stage_in[i], L.stage_in);
+        alloc((void**)&c->stage_out[i], L.stage_out);
+        alloc((void**)&c->stage_stats[i], L.stats);
+    }
+    if (!ok) {
+        cudaGetLastError();
+        set_err(nullptr, "cudaMalloc of %zu scratch bytes failed", L.total);
+        free_ctx(c);
+        return ASD_E_OOM;
+    }
+    if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) ok = false;
+    for (int i = 0; i < 2 && ok; ++i)
+        if (cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming) != cudaSuccess) ok = false;
+    if (!ok) {
+        set_err(nullptr, "stream/event creation failed: %s", cudaGetErrorString(cudaGetLastError()));
+        free_ctx(c);
+        return ASD_E_CUDA;
+    }
+    *out = c;
+    return ASD_OK;
+}
+
+void asd_destroy(asd_ctx* ctx)
+{
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    free_ctx(ctx);
+}
+
+int asd_launches_per_batch(const asd_ctx* ctx, int n)
+{
+    if (!ctx || n <= 0) return 0;
+    const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
+    return chunks * (3 + ctx->dp.paths);
+}
+
+int asd_depth_batch(asd_ctx* ctx, int n, const uint8_t* left, const uint8_t* right,
+                    float* out_disp, float* out_depth, asd_frame_stats* stats, void* cuda_stream)
+{
+    if (!ctx) { set_err(nullptr, "ctx is NULL"); return ASD_E_INVALID_ARG; }
+    if (n < 0) { set_err(ctx, "n < 0"); return ASD_E_INVALID_ARG; }
+    if (n == 0) return ASD_OK;
+    if (!left || !right) { set_err(ctx, "left/right is NULL"); return ASD_E_INVALID_ARG; }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const long long npx = ctx->dp.npx;
+    for (int f0 = 0; f0 < n; f0 += ctx->max_batch) {
+        const int m = (n - f0) < ctx->max_batch ? (n - f0) : ctx->max_batch;
+        int rc = run_chunk(ctx, m, left + f0 * npx, right + f0 * npx,
+                           out_disp ? out_disp + f0 * npx : nullptr,
+                           out_depth ? out_depth + f0 * npx : nullptr,
+                           stats ? stats + f0 : nullptr, nullptr, s);
+        if (rc != ASD_OK) return rc;
+    }
+    return ASD_OK;
+}
+
+int asd_depth(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
+              float* out_disp, float* out_depth, void* cuda_stream)
+{
+    return asd_depth_batch(ctx, 1, left, right, out_disp, out_depth, nullptr, cuda_stream);
+}
+
+int asd_depth_batch_host(asd_ctx* ctx, int n, const uint8_t* left_host, const uint8_t* right_host,
+                         float* out_disp_host, float* out_depth_host, asd_frame_stats* stats_host,
+                         void* cuda_stream)
+{
+    if (!ctx) { set_err(nullptr, "ctx is NULL"); return ASD_E_INVALID_ARG; }
+    if (n < 0) { set_err(ctx, "n < 0"); return ASD_E_INVALID_ARG; }
+    if (n == 0) return ASD_OK;
+    if (!left_host || !right_host) { set_err(ctx, "left/right is NULL"); return ASD_E_INVALID_ARG; }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    cudaStream_t cs = ctx->copy_stream;
+    const size_t npx = (size_t)ctx->dp.npx;
+    const int B = ctx->max_batch;
+    const int nchunks = (n + B - 1) / B;
+    // Pipeline: H2D(k+1) on the copy stream overlaps compute(k) on s; D2H(k) on
+    // the copy stream waits for compute(k) and overlaps compute(k+1).
+    auto chunk_n = [&](int k) { return (k + 1) * B <= n ? B : n - k * B; };
+    auto h2d = [&](int k) {
+        const int b = k & 1, m = chunk_n(k);
+        uint8_t* in = ctx->stage_in[b];
+        cudaStreamWaitEvent(cs, ctx->ev_done[b], 0);          // slot free (its D2H finished)
+        cudaMemcpyAsync(in, left_host + (size_t)k * B * npx, m * npx, cudaMemcpyHostToDevice, cs);
+        cudaMemcpyAsync(in + (size_t)B * npx, right_host + (size_t)k * B * npx, m * npx,
+                        cudaMemcpyHostToDevice, cs);
+        cudaEventRecord(ctx->ev_in[b], cs);
+    };
+    for (int i = 0; i < 2; ++i) cudaEventRecord(ctx->ev_done[i], cs);
+    h2d(0);
+    for (int k = 0; k < nchunks; ++k) {
+        const int b = k & 1, m = chunk_n(k);
+        uint8_t* in = ctx->stage_in[b];
+        float* od = ctx->stage_out[b];
+        float* oz = od + (size_t)B * npx;
+        cudaStreamWaitEvent(s, ctx->ev_in[b], 0);
+        int rc = run_chunk(ctx, m, in, in + (size_t)B * npx, out_disp_host ? od : nullptr,
+                           out_depth_host ? oz : nullptr, stats_host ? ctx->stage_stats[b] : nullptr,
+                           nullptr, s);
+        if (rc != ASD_OK) { cudaStreamSynchronize(s); cudaStreamSynchronize(cs); return rc; }
+        cudaEvent_t computed = ctx->ev_comp[b];
+        cudaEventRecord(computed, s);
+        if (k + 1 < nchunks) h2d(k + 1);
+        cudaStreamWaitEvent(cs, computed, 0);
+        if (out_disp_host)
+            cudaMemcpyAsync(out_disp_host + (size_t)k * B * npx, od, m * npx * 4, cudaMemcpyDeviceToHost, cs);
+        if (out_depth_host)
+            cudaMemcpyAsync(out_depth_host + (size_t)k * B * npx, oz, m * npx * 4, cudaMemcpyDeviceToHost, cs);
+        if (stats_host)
+            cudaMemcpyAsync(stats_host + (size_t)k * B, ctx->stage_stats[b], m * sizeof(asd_frame_stats),
+                            cudaMemcpyDeviceToHost, cs);
+        cudaEventRecord(ctx->ev_done[b], cs);
+    }
+    cudaError_t e = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { set_err(ctx, "host pipeline failed: %s", cudaGetErrorString(e)); return ASD_E_CUDA; }
+    return ASD_OK;
+}
+
+int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                    const asd_debug_out* outs, float* out_disp, float* out_depth, void* cuda_stream)
+{
+    if (!ctx) { set_err(nullptr, "ctx is NULL"); return ASD_E_INVALID_ARG; }
+    if (!left || !right) { set_err(ctx, "left/right is NULL"); return ASD_E_INVALID_ARG; }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    asd_debug_out o{};
+    if (outs) o = *outs;
+    const DevParams& p = ctx->dp;
+    int rc = run_chunk(ctx, 1, left, right, out_disp, out_depth, nullptr, o.mask, s);
+    if (rc != ASD_OK) return rc;
+    const size_t npx = (size_t)p.npx;
+    if (o.census_l) cudaMemcpyAsync(o.census_l, ctx->census_l, npx * ctx->sig_bytes, cudaMemcpyDeviceToDevice, s);
+    if (o.census_r) cudaMemcpyAsync(o.census_r, ctx->census_r, npx * ctx->sig_bytes, cudaMemcpyDeviceToDevice, s);
+    if (o.cost) launch_cost_volume(p, ctx->census_l, ctx->census_r, o.cost, s);
+    if (o.agg) cudaMemcpyAsync(o.agg, ctx->S, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, s);
+    if (o.dstar_l) cudaMemcpyAsync(o.dstar_l, ctx->dstar_l, npx * 2, cudaMemcpyDeviceToDevice, s);
+    if (o.dstar_r) cudaMemcpyAsync(o.dstar_r, ctx->dstar_r, npx * 2, cudaMemcpyDeviceToDevice, s);
+    if (o.disp_l) cudaMemcpyAsync(o.disp_l, ctx->dl, npx * 4, cudaMemcpyDeviceToDevice, s);
+    if (o.disp_r) cudaMemcpyAsync(o.disp_r, ctx->dr, npx * 4, cudaMemcpyDeviceToDevice, s);
+    if (o.mask_r) cudaMemcpyAsync(o.mask_r, ctx->mask_r, npx, cudaMemcpyDeviceToDevice, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_err(ctx, "debug extraction failed: %s", cudaGetErrorString(e)); return ASD_E_CUDA; }
+    return ASD_OK;
+}
+
+int asd_profile_begin(asd_ctx* ctx, int max_launches)
+{
+    if (!ctx || max_launches < 1 || max_launches > (1 << 20)) {
+        set_err(ctx, "asd_profile_begin: bad arguments");
+        return ASD_E_INVALID_ARG;
+    }
+    DeviceGuard g(ctx->device);
+    for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
+    ctx->prof_ev.assign(2 * (size_t)max_launches, nullptr);
+    for (auto& e : ctx->prof_ev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            set_err(ctx, "cudaEventCreate failed");
+            return ASD_E_CUDA;
+        }
+    ctx->prof_marks.clear();
+    ctx->prof_marks.reserve(max_launches);
+    ctx->prof_dropped = 0;
+    ctx->prof = true;
+    return ASD_OK;
+}
+
+int asd_profile_end(asd_ctx* ctx, asd_stage_times* out)
+{
+    if (!ctx || !out) { set_err(ctx, "asd_profile_end: NULL argument"); return ASD_E_INVALID_ARG; }
+    DeviceGuard g(ctx->device);
+    std::memset(out, 0, sizeof *out);
+    ctx->prof = false;
+    for (size_t k = 0; k < ctx->prof_marks.size(); ++k) {
+        float ms = 0.0f;
+        if (cudaEventSynchronize(ctx->prof_ev[2 * k + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, ctx->prof_ev[2 * k], ctx->prof_ev[2 * k + 1]) != cudaSuccess) {
+            set_err(ctx, "event timing failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return ASD_E_CUDA;
+        }
+        const int st = ctx->prof_marks[k].stage;
+        out->ms[st] += ms;
+        out->alg_bytes[st] += ctx->prof_marks[k].bytes;
+        out->launches[st] += 1;
+    }
+    out->dropped = ctx->prof_dropped;
+    ctx->prof_marks.clear();
+    return ASD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (internal to libasd).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "asd.h"
+#include "common.cuh"
+
+namespace asd {
+
+// K1 census, both views of nframes frames.
+void launch_census(const DevParams& p, int nframes, const uint8_t* left, const uint8_t* right,
+                   long long img_stride, void* out_l, void* out_r, long long sig_stride,
+                   cudaStream_t s);
+
+// K2/K3 one SGM direction (design D1); first = write S instead of accumulate.
+int num_chains(const DevParams& p, int rx, int ry);
+bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
+                    const void* cl, const void* cr, long long sig_stride,
+                    uint16_t* S, long long s_stride, cudaStream_t s);
+
+// K4 WTA/uniqueness/sub-pixel, left + right view.
+bool launch_wta(const DevParams& p, int nframes, const uint16_t* S, long long s_stride,
+                const FrameScratch& fs, long long px_stride, cudaStream_t s);
+
+// K5 LR check + depth + per-frame stats.
+void launch_lr_depth(const DevParams& p, int nframes, const FrameScratch& fs, long long px_stride,
+                     float* out_disp, float* out_depth, long long out_stride, uint8_t* mask_out,
+                     asd_frame_stats* stats, cudaStream_t s);
+
+// Debug: materialise the raw cost volume C [H][W][D] u8 from the census images.
+void launch_cost_volume(const DevParams& p, const void* cl, const void* cr, uint8_t* cost,
+                        cudaStream_t s);
+
+}  // namespace asd

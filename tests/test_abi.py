@@ -1,0 +1,85 @@
+"""The C-ABI library loads and exports every symbol include/asd.h declares;
+host-side validation works without a GPU (no compute calls here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2201_11924_b200 as asd
+from paper_2201_11924_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2201_11924_b200 import build
+    build.build()
+    return asd.load()
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "asd.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(asd_[a-z_]+)\s*\(", hdr)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_symbols()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(n for n, _, _ in abi.SYMBOLS) == names
+    out = os.popen(f"nm -D --defined-only {abi.LIB_PATH}").read()
+    for n in names:
+        assert re.search(rf"\bT {n}\b", out), n
+
+
+def test_version_and_strerror(lib):
+    assert lib.asd_version() == 1
+    assert lib.asd_strerror(0) == b"ok"
+    assert lib.asd_strerror(-2) == b"unsupported configuration"
+
+
+def test_sm100a_only_cubin():
+    out = os.popen(f"cuobjdump --list-elf {abi.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(num_disp=100), asd.ASD_E_UNSUPPORTED),
+    (dict(num_disp=512), asd.ASD_E_UNSUPPORTED),
+    (dict(census_w=8), asd.ASD_E_INVALID_ARG),
+    (dict(census_w=13, census_h=11), asd.ASD_E_UNSUPPORTED),      # nb = 71 > 64
+    (dict(p1=10, p2=5), asd.ASD_E_INVALID_ARG),
+    (dict(p2=250), asd.ASD_E_UNSUPPORTED),                       # nb + p2 > 255
+    (dict(paths=6), asd.ASD_E_INVALID_ARG),
+    (dict(min_disp=-1), asd.ASD_E_INVALID_ARG),
+    (dict(focal_px=0.0), asd.ASD_E_INVALID_ARG),
+    (dict(lr_max_diff=float("nan")), asd.ASD_E_INVALID_ARG),
+    (dict(width=3), asd.ASD_E_INVALID_ARG),
+])
+def test_validation(lib, kw, code):
+    d = dict(width=64, height=48, num_disp=16, census_w=5, census_h=5)
+    d.update(kw)
+    p = asd.Params(**d)
+    ctx = ctypes.c_void_p()
+    assert lib.asd_create(ctypes.byref(p.c()), 0, 1, ctypes.byref(ctx)) == code
+    assert not ctx.value
+    assert lib.asd_last_error(None)
+    assert lib.asd_scratch_bytes(ctypes.byref(p.c()), 1) == 0
+
+
+def test_scratch_bytes(lib):
+    p = asd.Params(1280, 720, 128)
+    one = lib.asd_scratch_bytes(ctypes.byref(p.c()), 1)
+    assert one >= 1280 * 720 * 128 * 2
+    assert lib.asd_scratch_bytes(ctypes.byref(p.c()), 4) >= 4 * 1280 * 720 * 128 * 2
+    assert lib.asd_scratch_bytes(ctypes.byref(p.c()), 0) == 0
+
+
+def test_null_ctx_rejected(lib):
+    assert lib.asd_depth(None, None, None, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert lib.asd_depth_batch(None, 1, None, None, None, None, None, None) == asd.ASD_E_INVALID_ARG

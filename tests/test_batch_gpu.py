@@ -1,0 +1,97 @@
+"""The batched entry points in the launch configuration bench.py uses
+(asd_depth_batch over chunks of max_batch frames, asd_depth_batch_host with
+host buffers): per-frame outputs and checksums vs the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2201_11924_b200 as asd
+import synth
+from tests.gpu_util import assert_bits_equal, assert_depth_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_frame(d, L, R):
+    o = oracle.compute(oracle.Params(**d), L, R)
+    return o, oracle.checksum(o["dstar_l"], o["mask"])
+
+
+@pytest.mark.parametrize("name,n,max_batch", [("A", 7, 3), ("B", 5, 2)])
+def test_batch_matches_oracle(name, n, max_batch):
+    import torch
+    cfg = synth.CONFIGS[name]
+    d = cfg.params_dict()
+    Ls, Rs = synth.frame_pool(cfg, n)
+    L = torch.from_numpy(Ls).cuda()
+    R = torch.from_numpy(Rs).cuda()
+    disp = torch.empty(n, cfg.height, cfg.width, device="cuda")
+    depth = torch.empty_like(disp)
+    stats = torch.zeros(n, 4, dtype=torch.int32, device="cuda")
+    with asd.Stereo(asd.Params(**d), 0, max_batch) as st:
+        st.asd_depth_batch(L, R, disp, depth, stats)
+        torch.cuda.synchronize()
+    disp, depth, stats = disp.cpu().numpy(), depth.cpu().numpy(), stats.cpu().numpy()
+    for i in range(n):
+        o, h = _oracle_frame(d, Ls[i], Rs[i])
+        assert_bits_equal(disp[i], o["disp"], f"disp frame {i}")
+        assert_depth_close(depth[i], o["depth"])
+        assert int(stats[i, 0]) & 0xFFFFFFFF == h, f"checksum frame {i}"
+        assert stats[i, 1] == int((o["mask"] == 0).sum())
+
+
+def test_host_path_matches_device_path():
+    import torch
+    cfg = synth.CONFIGS["B"]
+    d = cfg.params_dict()
+    n = 5
+    Ls, Rs = synth.frame_pool(cfg, n)
+    Lh = torch.from_numpy(Ls).pin_memory()
+    Rh = torch.from_numpy(Rs).pin_memory()
+    dh = torch.empty(n, cfg.height, cfg.width).pin_memory()
+    zh = torch.empty_like(dh).pin_memory()
+    sh = torch.zeros(n, 4, dtype=torch.int32).pin_memory()
+    with asd.Stereo(asd.Params(**d), 0, 2) as st:
+        st.asd_depth_batch_host(Lh, Rh, dh, zh, sh)
+        Ld, Rd = Lh.cuda(), Rh.cuda()
+        dd = torch.empty(n, cfg.height, cfg.width, device="cuda")
+        zd = torch.empty_like(dd)
+        sd = torch.zeros(n, 4, dtype=torch.int32, device="cuda")
+        st.asd_depth_batch(Ld, Rd, dd, zd, sd)
+        torch.cuda.synchronize()
+    assert_bits_equal(dh.numpy(), dd.cpu().numpy(), "host disp")
+    assert_bits_equal(zh.numpy(), zd.cpu().numpy(), "host depth")
+    assert (sh.numpy()[:, :2] == sd.cpu().numpy()[:, :2]).all()
+    o, h = _oracle_frame(d, Ls[4], Rs[4])
+    assert int(sh.numpy()[4, 0]) & 0xFFFFFFFF == h
+
+
+def test_config_C_batch_launch_config():
+    """Config C in bench.py's launch configuration (chunks of max_batch); the first
+    and last frames are checked against the full oracle."""
+    import torch
+    cfg = synth.CONFIGS["C"]
+    d = cfg.params_dict()
+    n, mb = 6, 4
+    Ls, Rs = synth.frame_pool(cfg, n)
+    L, R = torch.from_numpy(Ls).cuda(), torch.from_numpy(Rs).cuda()
+    disp = torch.empty(n, cfg.height, cfg.width, device="cuda")
+    depth = torch.empty_like(disp)
+    stats = torch.zeros(n, 4, dtype=torch.int32, device="cuda")
+    with asd.Stereo(asd.Params(**d), 0, mb) as st:
+        st.asd_depth_batch(L, R, disp, depth, stats)
+        torch.cuda.synchronize()
+    for i in (0, n - 1):
+        o, h = _oracle_frame(d, Ls[i], Rs[i])
+        assert_bits_equal(disp[i].cpu().numpy(), o["disp"], f"disp frame {i}")
+        assert_depth_close(depth[i].cpu().numpy(), o["depth"])
+        assert int(stats[i, 0].item()) & 0xFFFFFFFF == h
+
+
+def test_empty_batch_is_noop():
+    import torch
+    cfg = synth.CONFIGS["A"]
+    with asd.Stereo(asd.Params(**cfg.params_dict()), 0, 2) as st:
+        e = torch.empty(0, cfg.height, cfg.width, dtype=torch.uint8, device="cuda")
+        st.asd_depth_batch(e, e)
+        torch.cuda.synchronize()
