@@ -34,7 +34,14 @@ METRIC = "frames/s and Gcell/s (W·H·D) at 1280×720×D128 8-path; HBM GB/s vs 
 CONFIG = "C"
 FRAMES_PER_STEP = 128          # inputs 128 x 2 x 0.92 MB = 236 MB per step > 126 MB L2
 POOL = 8                       # distinct synthetic frames (kernels are data-oblivious)
-MAX_BATCH = 8                  # frames in flight per asd_depth_batch chunk
+MAX_BATCH = 32                 # frames in flight per asd_depth_batch chunk
+
+
+KERNEL_NAMES = {"census": "census_kernel (K1)", "dir": "sgm_dir_kernel (D1, one path direction)",
+                "wta": "wta_kernel (D1 K4)", "lr": "lr_depth_kernel (K5)",
+                "down": "vsweep_kernel<down> (D3, 3 downward paths)",
+                "up": "vsweep_kernel<up> (D3, 3 upward paths)",
+                "row": "row_kernel (D3, horizontal paths + WTA)"}
 
 
 def peaks():
@@ -294,7 +301,8 @@ def main():
     if rank == 0:
         pk = peaks()
         hbm_peak = pk["hbm_gbs"] if pk else 6650.0
-        agg = prof["agg"]
+        top = max(asd.abi.STAGES, key=lambda k: prof[k]["ms"])
+        agg = prof[top]
         avg_ms = agg["ms"] / max(1, agg["launches"])
         alg_per_launch = agg["alg_bytes"] / max(1, agg["launches"])
         achieved = alg_per_launch / (avg_ms / 1000.0) / 1e9
@@ -323,10 +331,11 @@ def main():
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
                        "l2": "inputs larger than L2 (236 MB/step/GPU; plus 236 MB S scratch per frame)",
-                       "design": "D1: one SGM kernel per path direction"},
+                       "engine": {1: "D1: one SGM kernel per path direction",
+                                  3: "D3: grouped sweeps (cluster down/up kernels + fused row/WTA kernel)"}[st.engine]},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                         "kernel": "sgm_dir_kernel (aggregation, one direction per launch)",
+                         "kernel": KERNEL_NAMES[top],
                          "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": round(avg_ms, 4),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md"},
             "stage_ms": {k: round(prof[k]["ms"], 3) for k in asd.abi.STAGES},

@@ -68,7 +68,23 @@ extern "C" {
  *   lr_max_diff: px, < 0 disables the LR check; not NaN
  *   subpixel: 0 or 1
  *   focal_px, baseline_m: finite, > 0; depth = fb / disparity with
- *       fb = (float)((double)focal_px * (double)baseline_m) */
+ *       fb = (float)((double)focal_px * (double)baseline_m)
+ *   engine: ASD_ENGINE_AUTO / _D1 / _D3; D3 outside its envelope ->
+ *       ASD_E_UNSUPPORTED.  Results are bit-identical across engines. */
+/* Aggregation designs:
+ *   ASD_ENGINE_D1  one warp-per-line kernel per path direction, u16 S volume
+ *                  read-modify-written in HBM (any configuration above)
+ *   ASD_ENGINE_D3  grouped sweeps: cluster kernels for the 3 downward and 3
+ *                  upward paths, a warp-per-row kernel for the 2 horizontal
+ *                  paths fused with WTA/uniqueness/sub-pixel; the cost volume
+ *                  and S are never materialised.  Envelope: nb <= 32,
+ *                  num_disp in {16,32,64,128}, 3*(nb+p2) <= 255 (8-path),
+ *                  paths*(nb+p2)*2^ceil(log2 num_disp) < 65535.
+ *   ASD_ENGINE_AUTO D3 inside its envelope, else D1.                      */
+#define ASD_ENGINE_AUTO 0
+#define ASD_ENGINE_D1   1
+#define ASD_ENGINE_D3   3
+
 typedef struct asd_params {
     int32_t width, height;
     int32_t min_disp, num_disp;
@@ -79,6 +95,7 @@ typedef struct asd_params {
     float   lr_max_diff;
     int32_t subpixel;
     float   focal_px, baseline_m;
+    int32_t engine;      /* ASD_ENGINE_* (0 = auto) */
 } asd_params;
 
 /* Per-frame statistics; exact integers except depth_sum.
@@ -160,6 +177,9 @@ int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
 /* Number of kernel launches one asd_depth_batch call of n frames enqueues. */
 int asd_launches_per_batch(const asd_ctx* ctx, int n);
 
+/* The engine the context runs (ASD_ENGINE_D1 or ASD_ENGINE_D3). */
+int asd_engine(const asd_ctx* ctx);
+
 /* ---- live stage timing (CUDA events on the caller's stream) ----
  * asd_profile_begin(ctx, max_launches) pre-creates events for up to
  * max_launches kernel launches; from then on every launch the context enqueues
@@ -169,11 +189,14 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n);
  * bytes those launches must move at minimum (DESIGN.md §6 per-unit figures x
  * units processed), then stops profiling.  Launches beyond max_launches are
  * counted in `dropped` and not timed. */
-#define ASD_STAGE_CENSUS 0   /* K1 */
-#define ASD_STAGE_AGG    1   /* SGM path aggregation kernels */
-#define ASD_STAGE_WTA    2   /* K4 */
-#define ASD_STAGE_LR     3   /* K5 */
-#define ASD_STAGE_COUNT  4
+#define ASD_STAGE_CENSUS 0   /* K1 census */
+#define ASD_STAGE_DIR    1   /* D1: one SGM path direction per launch */
+#define ASD_STAGE_WTA    2   /* D1: K4 WTA / uniqueness / sub-pixel, both views */
+#define ASD_STAGE_LR     3   /* K5 LR check + depth (+ stats) */
+#define ASD_STAGE_DOWN   4   /* D3: downward sweep (3 paths, or 1 at 4-path) */
+#define ASD_STAGE_UP     5   /* D3: upward sweep */
+#define ASD_STAGE_ROW    6   /* D3: horizontal paths + WTA, both views */
+#define ASD_STAGE_COUNT  7
 typedef struct asd_stage_times {
     double ms[ASD_STAGE_COUNT];
     double alg_bytes[ASD_STAGE_COUNT];

@@ -33,7 +33,8 @@ class asd_params(ctypes.Structure):
                 ("p1", ctypes.c_int32), ("p2", ctypes.c_int32),
                 ("paths", ctypes.c_int32), ("uniqueness", ctypes.c_int32),
                 ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
-                ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float)]
+                ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
+                ("engine", ctypes.c_int32)]
 
 
 class asd_frame_stats(ctypes.Structure):
@@ -47,12 +48,12 @@ class asd_debug_out(ctypes.Structure):
                  "disp_l", "disp_r", "mask", "mask_r")]
 
 
-STAGES = ("census", "agg", "wta", "lr")
+STAGES = ("census", "dir", "wta", "lr", "down", "up", "row")
 
 
 class asd_stage_times(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 4), ("alg_bytes", ctypes.c_double * 4),
-                ("launches", ctypes.c_int32 * 4), ("dropped", ctypes.c_int32),
+    _fields_ = [("ms", ctypes.c_double * 7), ("alg_bytes", ctypes.c_double * 7),
+                ("launches", ctypes.c_int32 * 7), ("dropped", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
 
@@ -68,6 +69,7 @@ SYMBOLS = [
     ("asd_depth_batch_host", _I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     ("asd_depth_debug", _I, [_VP, _VP, _VP, ctypes.POINTER(asd_debug_out), _VP, _VP, _VP]),
     ("asd_launches_per_batch", _I, [_VP, _I]),
+    ("asd_engine", _I, [_VP]),
     ("asd_profile_begin", _I, [_VP, _I]),
     ("asd_profile_end", _I, [_VP, ctypes.POINTER(asd_stage_times)]),
     ("asd_strerror", ctypes.c_char_p, [_I]),
@@ -110,11 +112,13 @@ class Params:
     subpixel: int = 1
     focal_px: float = 430.0
     baseline_m: float = 0.055
+    engine: int = 0            # ASD_ENGINE_AUTO (0), _D1 (1), _D3 (3)
 
     def c(self) -> asd_params:
         return asd_params(self.width, self.height, self.min_disp, self.num_disp, self.census_w,
                           self.census_h, self.p1, self.p2, self.paths, self.uniqueness,
-                          self.lr_max_diff, self.subpixel, self.focal_px, self.baseline_m)
+                          self.lr_max_diff, self.subpixel, self.focal_px, self.baseline_m,
+                          self.engine)
 
     @property
     def nbits(self) -> int:
@@ -197,6 +201,10 @@ class Stereo:
         _check(self._lib.asd_profile_end(self._ctx, ctypes.byref(t)), self._ctx)
         return {name: {"ms": t.ms[i], "alg_bytes": t.alg_bytes[i], "launches": t.launches[i]}
                 for i, name in enumerate(STAGES)} | {"dropped": t.dropped}
+
+    @property
+    def engine(self) -> int:
+        return int(self._lib.asd_engine(self._ctx))
 
     def launches_per_batch(self, n: int) -> int:
         return int(self._lib.asd_launches_per_batch(self._ctx, n))

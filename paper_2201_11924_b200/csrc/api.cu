@@ -38,6 +38,12 @@ struct asd_ctx {
     int16_t* dstar_r = nullptr;
     uint8_t* mask_l = nullptr;
     uint8_t* mask_r = nullptr;
+    // design D3 scratch
+    int engine = ASD_ENGINE_D1;
+    V2Plan plan{};
+    uint8_t* pa = nullptr;        // [B][H][W][D] u8 partial (down sweep)
+    uint16_t* pab = nullptr;      // [B][H][W][D] u16 partial (down + up)
+    uint8_t* stash = nullptr;     // [B][H][W][D] u8 left->right path
     // host-path staging: two chunk buffers (inputs u8, outputs f32) + stats
     uint8_t* stage_in[2] = {nullptr, nullptr};     // [max_batch][2][H][W]
     float* stage_out[2] = {nullptr, nullptr};      // [max_batch][2][H][W]
@@ -123,6 +129,10 @@ int validate(const asd_params* p, char* why, size_t n)
     if (p->uniqueness > 100000) { snprintf(why, n, "uniqueness > 100000"); return ASD_E_INVALID_ARG; }
     if (std::isnan(p->lr_max_diff)) { snprintf(why, n, "lr_max_diff is NaN"); return ASD_E_INVALID_ARG; }
     if (p->subpixel != 0 && p->subpixel != 1) { snprintf(why, n, "subpixel must be 0/1"); return ASD_E_INVALID_ARG; }
+    if (p->engine != ASD_ENGINE_AUTO && p->engine != ASD_ENGINE_D1 && p->engine != ASD_ENGINE_D3) {
+        snprintf(why, n, "engine must be 0 (auto), 1 (D1) or 3 (D3)");
+        return ASD_E_INVALID_ARG;
+    }
     if (!(std::isfinite(p->focal_px) && p->focal_px > 0.0f) ||
         !(std::isfinite(p->baseline_m) && p->baseline_m > 0.0f)) {
         snprintf(why, n, "focal_px and baseline_m must be finite and > 0");
@@ -151,24 +161,27 @@ DevParams make_dev(const asd_params* p)
 }
 
 struct Layout {
-    size_t sig, s, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
+    size_t sig, s, pa, pab, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
 };
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
-Layout layout(const DevParams& d, int max_batch)
+Layout layout(const DevParams& d, int max_batch, int engine)
 {
     Layout L{};
     const size_t B = (size_t)max_batch;
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
-    L.s = align_up(B * d.ncell * 2);
+    L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
+    L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
+    L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
+    L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
     L.px_f32 = align_up(B * d.npx * 4);
     L.px_i16 = align_up(B * d.npx * 2);
     L.px_u8 = align_up(B * d.npx);
     L.stage_in = align_up(B * d.npx * 2);
     L.stage_out = align_up(B * d.npx * 2 * 4);
     L.stats = align_up(B * sizeof(asd_frame_stats));
-    L.total = 2 * L.sig + L.s + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
+    L.total = 2 * L.sig + L.s + L.pa + L.pab + L.stash + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
               2 * (L.stage_in + L.stage_out + L.stats);
     return L;
 }
@@ -211,11 +224,18 @@ static double alg_bytes_census(const DevParams& p, size_t sig) { return 2.0 * p.
 static double alg_bytes_dir(const DevParams& p, bool first) { return (first ? 2.0 : 4.0) * p.ncell; }
 static double alg_bytes_wta(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * (4 + 2 + 1); }
 static double alg_bytes_lr(const DevParams& p) { return p.npx * (2 * (4 + 1) + 2 + 2 * 4.0); }
+// Design D3: down sweep writes the u8 partial (1 B/cell); up sweep reads it and
+// writes the u16 partial (3 B/cell); the row kernel reads the u16 partial and
+// writes + reads the u8 left->right stash (4 B/cell) and writes the per-pixel
+// maps of both views (2 x (4 + 2 + 1) B/px).  Census reads are L2-resident.
+static double alg_bytes_down(const DevParams& p) { return 1.0 * p.ncell; }
+static double alg_bytes_up(const DevParams& p) { return 3.0 * p.ncell; }
+static double alg_bytes_row(const DevParams& p) { return 4.0 * p.ncell + 2.0 * p.npx * 7; }
 
 // Enqueue the whole path for n <= max_batch frames resident on the device.
 int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
               float* out_disp, float* out_depth, asd_frame_stats* stats,
-              uint8_t* mask_out, cudaStream_t s)
+              uint8_t* mask_out, cudaStream_t s, uint16_t* agg_debug = nullptr)
 {
     const DevParams& p = c->dp;
     if (n <= 0) return ASD_OK;
@@ -224,16 +244,39 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         ProfScope ps(c, s, ASD_STAGE_CENSUS, n * alg_bytes_census(p, c->sig_bytes));
         launch_census(p, n, left, right, npx, c->census_l, c->census_r, npx, s);
     }
-    for (int r = 0; r < p.paths; ++r) {
-        ProfScope ps(c, s, ASD_STAGE_AGG, n * alg_bytes_dir(p, r == 0));
+    FrameScratch fs = frame_scratch(c);
+    if (c->engine == ASD_ENGINE_D3) {
+        {
+            ProfScope ps(c, s, ASD_STAGE_DOWN, n * alg_bytes_down(p));
+            if (launch_v2_stage(0, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
+                                p.ncell, fs, npx, nullptr, s) != 0) {
+                set_err(c, "down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return ASD_E_CUDA;
+            }
+        }
+        {
+            ProfScope ps(c, s, ASD_STAGE_UP, n * alg_bytes_up(p));
+            if (launch_v2_stage(1, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
+                                p.ncell, fs, npx, nullptr, s) != 0) {
+                set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return ASD_E_CUDA;
+            }
+        }
+        {
+            ProfScope ps(c, s, ASD_STAGE_ROW, n * alg_bytes_row(p));
+            launch_v2_stage(2, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
+                            p.ncell, fs, npx, agg_debug, s);
+        }
+    }
+    for (int r = 0; c->engine == ASD_ENGINE_D1 && r < p.paths; ++r) {
+        ProfScope ps(c, s, ASD_STAGE_DIR, n * alg_bytes_dir(p, r == 0));
         if (!launch_sgm_dir(p, n, kDirs[r][0], kDirs[r][1], r == 0, c->census_l, c->census_r, npx,
                             c->S, p.ncell, s)) {
             set_err(c, "no SGM kernel instance for num_disp=%d", p.D);
             return ASD_E_UNSUPPORTED;
         }
     }
-    FrameScratch fs = frame_scratch(c);
-    {
+    if (c->engine == ASD_ENGINE_D1) {
         ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta(p));
         if (!launch_wta(p, n, c->S, p.ncell, fs, npx, s)) {
             set_err(c, "no WTA kernel instance for num_disp=%d", p.D);
@@ -257,7 +300,7 @@ void free_ctx(asd_ctx* c)
 {
     if (!c) return;
     void* ptrs[] = {c->census_l, c->census_r, c->S, c->dl, c->dr, c->dstar_l, c->dstar_r,
-                    c->mask_l, c->mask_r, c->stage_in[0], c->stage_in[1], c->stage_out[0],
+                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (int i = 0; i < 2; ++i) {
@@ -294,7 +337,16 @@ size_t asd_scratch_bytes(const asd_params* p, int max_batch)
 {
     char why[256];
     if (validate(p, why, sizeof why) != ASD_OK || max_batch < 1 || max_batch > 1024) return 0;
-    return layout(make_dev(p), max_batch).total;
+    const DevParams d = make_dev(p);
+    int engine = p->engine == ASD_ENGINE_AUTO ? ASD_ENGINE_D1 : p->engine;
+    if (p->engine != ASD_ENGINE_D1) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        V2Plan pl;
+        if (v2_plan(d, dev, pl)) engine = ASD_ENGINE_D3;
+        cudaGetLastError();
+    }
+    return layout(d, max_batch, engine).total;
 }
 
 int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
@@ -319,13 +371,26 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     c->device = device;
     c->max_batch = max_batch;
     c->sig_bytes = c->dp.nb <= 32 ? 4 : 8;
-    const Layout L = layout(c->dp, max_batch);
+    c->engine = ASD_ENGINE_D1;
+    if (p->engine != ASD_ENGINE_D1) {
+        if (v2_plan(c->dp, device, c->plan)) {
+            c->engine = ASD_ENGINE_D3;
+        } else if (p->engine == ASD_ENGINE_D3) {
+            set_err(nullptr, "engine D3 unsupported for these parameters: %s", c->plan.why);
+            delete c;
+            return ASD_E_UNSUPPORTED;
+        }
+    }
+    const Layout L = layout(c->dp, max_batch, c->engine);
     bool ok = true;
     auto alloc = [&](void** q, size_t bytes) {
         if (ok && cudaMalloc(q, bytes) != cudaSuccess) ok = false;
     };
     alloc(&c->census_l, L.sig); alloc(&c->census_r, L.sig);
-    alloc((void**)&c->S, L.s);
+    if (L.s) alloc((void**)&c->S, L.s);
+    if (L.pa) alloc((void**)&c->pa, L.pa);
+    if (L.pab) alloc((void**)&c->pab, L.pab);
+    if (L.stash) alloc((void**)&c->stash, L.stash);
     alloc((void**)&c->dl, L.px_f32); alloc((void**)&c->dr, L.px_f32);
     alloc((void**)&c->dstar_l, L.px_i16); alloc((void**)&c->dstar_r, L.px_i16);
     alloc((void**)&c->mask_l, L.px_u8); alloc((void**)&c->mask_r, L.px_u8);
@@ -366,8 +431,10 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 {
     if (!ctx || n <= 0) return 0;
     const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
-    return chunks * (3 + ctx->dp.paths);
+    return chunks * (ctx->engine == ASD_ENGINE_D3 ? 5 : 3 + ctx->dp.paths);
 }
+
+int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }
 
 int asd_depth_batch(asd_ctx* ctx, int n, const uint8_t* left, const uint8_t* right,
                     float* out_disp, float* out_depth, asd_frame_stats* stats, void* cuda_stream)
@@ -463,13 +530,15 @@ int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
     asd_debug_out o{};
     if (outs) o = *outs;
     const DevParams& p = ctx->dp;
-    int rc = run_chunk(ctx, 1, left, right, out_disp, out_depth, nullptr, o.mask, s);
+    int rc = run_chunk(ctx, 1, left, right, out_disp, out_depth, nullptr, o.mask, s,
+                       ctx->engine == ASD_ENGINE_D3 ? o.agg : nullptr);
     if (rc != ASD_OK) return rc;
     const size_t npx = (size_t)p.npx;
     if (o.census_l) cudaMemcpyAsync(o.census_l, ctx->census_l, npx * ctx->sig_bytes, cudaMemcpyDeviceToDevice, s);
     if (o.census_r) cudaMemcpyAsync(o.census_r, ctx->census_r, npx * ctx->sig_bytes, cudaMemcpyDeviceToDevice, s);
     if (o.cost) launch_cost_volume(p, ctx->census_l, ctx->census_r, o.cost, s);
-    if (o.agg) cudaMemcpyAsync(o.agg, ctx->S, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, s);
+    if (o.agg && ctx->engine == ASD_ENGINE_D1)
+        cudaMemcpyAsync(o.agg, ctx->S, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, s);
     if (o.dstar_l) cudaMemcpyAsync(o.dstar_l, ctx->dstar_l, npx * 2, cudaMemcpyDeviceToDevice, s);
     if (o.dstar_r) cudaMemcpyAsync(o.dstar_r, ctx->dstar_r, npx * 2, cudaMemcpyDeviceToDevice, s);
     if (o.disp_l) cudaMemcpyAsync(o.disp_l, ctx->dl, npx * 4, cudaMemcpyDeviceToDevice, s);

@@ -27,6 +27,22 @@ void launch_lr_depth(const DevParams& p, int nframes, const FrameScratch& fs, lo
                      float* out_disp, float* out_depth, long long out_stride, uint8_t* mask_out,
                      asd_frame_stats* stats, cudaStream_t s);
 
+// Design D3 (sgm_v2.cu): grouped sweeps.  v2_plan checks the envelope and
+// picks the cluster geometry; launch_v2_stage(0 = down, 1 = up, 2 = row).
+struct V2Plan {
+    bool ok;
+    int DC, T, NP, cs, w, vthreads, active_ctas;
+    size_t vsmem;
+    int DPL, nbuf, bstride;
+    size_t rsmem;
+    char why[128];
+};
+bool v2_plan(const DevParams& p, int device, V2Plan& pl);
+int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes,
+                    const void* cl, const void* cr, long long sig_stride,
+                    uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,
+                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s);
+
 // Debug: materialise the raw cost volume C [H][W][D] u8 from the census images.
 void launch_cost_volume(const DevParams& p, const void* cl, const void* cr, uint8_t* cost,
                         cudaStream_t s);

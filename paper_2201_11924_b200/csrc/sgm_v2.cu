@@ -1,0 +1,908 @@
+// sgm_v2.cu -- design D3: SGM aggregation in three sweeps with the cost
+// volume never materialised and the path state packed two disparities per
+// 32-bit register (u16x2, VIMNMX/VIMNMX3 on sm_100a).
+//
+//   K_down  (cluster kernel)  rows top->bottom, paths  down, down-right, down-left
+//                             -> P_A  = sum of those L_r, u8 per cell
+//   K_up    (cluster kernel)  rows bottom->top, paths  up, up-left, up-right
+//                             -> P_AB = P_A + sum, u16 per cell
+//   K_row   (warp per row)    left->right path (L stashed as u8), then
+//                             right->left path; S = P_AB + L_lr + L_rl, and
+//                             WTA/uniqueness/sub-pixel for the left view and
+//                             the re-indexed right view from a shared-memory
+//                             window of S rows (K4 semantics, post.cu).
+// 4-path: K_down/K_up carry only the vertical path.
+//
+// Recursion ("four-path semi-global matching", SPEC S:309,
+// reading c6), for every path r:
+//   L_r(p,d) = C(p,d) + min(L_r(p-r,d), L_r(p-r,d+-1)+P1, M+P2) - M.
+// A predecessor outside the image is fed as L = 0, M = 0, which makes the
+// formula return C (the line start) without a branch.  Cost (P:289 Hamming,
+// S:300, reading c3) is recomputed from the census rows staged in shared
+// memory: C = popc(cl(x,y) ^ cr(x-delta,y)) or nb.
+//
+// Vertical sweeps: one cluster of CS CTAs per frame, CTA k owns columns
+// [k*w, (k+1)*w); thread = (column, chunk of DC disparities), lane =
+// col*T + chunk.  Register layout per path: reg k holds (d0+k, d0+NR+k),
+// NR = DC/2, so d-1 / d+1 neighbours are the adjacent registers except at the
+// chunk edges (one shuffle + PRMT each).  Diagonal predecessors (x-1 / x+1 of
+// the previous row) come from __shfl_up/down by T lanes; warp-edge columns read
+// them from a double-buffered shared-memory halo that the neighbouring warp
+// (or, at CTA edges, the neighbouring CTA through DSMEM) wrote.  One cluster
+// barrier per row, split arrive/wait around the next row's cost computation.
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace asd {
+namespace v2 {
+
+constexpr uint32_t INF2 = 0x7FFF7FFFu;
+
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_arrive()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait()
+{
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+struct VArgs {
+    DevParams p;
+    int w;                    // columns per CTA (multiple of 32/T)
+    int cs;                   // CTAs per frame (cluster size when NP == 3)
+    const uint32_t* cl;       // census, [frames][H][W]
+    const uint32_t* cr;
+    long long sig_stride;
+    const uint8_t* pin;       // K_up input P_A  [frames][H][W][D] (chunk-interleaved u8)
+    uint8_t* pout8;           // K_down output P_A
+    uint16_t* pout16;         // K_up output P_AB (row-kernel layout)
+    long long cell_stride;    // H*W*D
+};
+
+// ---------------------------------------------------------------- helpers
+template <int NR, int T>
+__device__ __forceinline__ void path_update(const DevParams& p, int chunk, const uint32_t (&P)[NR],
+                                            uint32_t Mp, const uint32_t (&C)[NR], uint32_t (&Ln)[NR],
+                                            uint32_t& mout)
+{
+    const uint32_t P1P1 = (uint32_t)p.p1 * 0x10001u;
+    const uint32_t MP2 = (Mp + (uint32_t)p.p2) * 0x10001u;
+    const uint32_t negMM = 0u - Mp * 0x10001u;
+    uint32_t Q[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) Q[k] = P[k] + P1P1;
+    uint32_t qprev = INF2, qnext = INF2;
+    if (T > 1) {
+        const uint32_t u = __shfl_up_sync(FULL, Q[NR - 1], 1);
+        const uint32_t v = __shfl_down_sync(FULL, Q[0], 1);
+        if (chunk > 0) qprev = u;
+        if (chunk < T - 1) qnext = v;
+    }
+    uint32_t macc = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        const uint32_t dm1 = k > 0 ? Q[k - 1] : __byte_perm(qprev, Q[NR - 1], 0x5432);
+        const uint32_t dp1 = k < NR - 1 ? Q[k + 1] : __byte_perm(Q[0], qnext, 0x5432);
+        uint32_t t = vmin2(vmin2(dm1, dp1), P[k]);
+        t = vmin2(t, MP2);
+        Ln[k] = t + C[k] + negMM;
+        macc = vmin2(macc, Ln[k]);
+    }
+    uint32_t m = min(macc & 0xFFFFu, macc >> 16);
+#pragma unroll
+    for (int o = 1; o < T; o <<= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+    mout = m;
+}
+
+// ---------------------------------------------------------------- K_down / K_up
+// Shared-memory census rows: the left row (w words) and, per chunk k, the
+// slice of the right row its DC disparities read (w + DC - 1 words), placed at
+// a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
+// the same bank.  Three slots (rows i, i+1, i+2 in flight).
+template <int DC, int T>
+struct VGeom {
+    static constexpr int NR = DC / 2;
+    static constexpr int CPW = 32 / T;
+    __host__ __device__ static int cstride(int w) { return ((w + DC - 1 + 31) / 32) * 32 + 32; }
+    __host__ __device__ static int coff(int k) { return (k * (DC + 32 / T)) & 31; }
+    __host__ __device__ static int slot_words(int w) { return w + T * cstride(w); }
+};
+
+template <int DC, int T, int NP, bool UP, int DPL_ROW>
+__global__ void __launch_bounds__(DC == 32 ? 512 : 1024)
+vsweep_kernel(VArgs a)
+{
+    using G = VGeom<DC, T>;
+    constexpr int NR = G::NR;
+    constexpr int CPW = G::CPW;
+    extern __shared__ uint32_t smem[];
+    const DevParams& p = a.p;
+    const int W = p.W, H = p.H, D = p.D;
+    const int nw = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int col = lane / T, chunk = lane % T;
+    const int rank = blockIdx.x;
+    const int frame = blockIdx.y;
+    const int w = a.w;
+    const int x0 = rank * w;
+    const int xl = warp * CPW + col;
+    const int x = x0 + xl;
+    const int cstr = G::cstride(w);
+    const int sw = G::slot_words(w);
+    const bool clustered = NP == 3 && a.cs > 1;
+
+    uint32_t* cens = smem;                   // [3][sw]: left row, then T right-row slices
+    uint32_t* hL = cens + 3 * sw;            // [2][nw][T][NR]   (NP == 3)
+    uint32_t* hR = hL + 2 * nw * T * NR;
+    uint32_t* hLM = hR + 2 * nw * T * NR;    // [2][nw]
+    uint32_t* hRM = hLM + 2 * nw;
+
+    const uint32_t* cl = a.cl + frame * a.sig_stride;
+    const uint32_t* cr = a.cr + frame * a.sig_stride;
+
+    if (NP == 3) {
+        for (int i = threadIdx.x; i < 4 * nw * T * NR + 4 * nw; i += blockDim.x) hL[i] = 0u;
+    }
+    auto row_of = [&](int i) { return UP ? H - 1 - i : i; };
+    auto stage = [&](int yrow, int slot) {
+        uint32_t* sl = cens + slot * sw;
+        const uint32_t* rl = cl + (long long)yrow * W;
+        const uint32_t* rr = cr + (long long)yrow * W;
+        for (int i = threadIdx.x; i < w; i += blockDim.x) {
+            const int gx = x0 + i;
+            sl[i] = gx < W ? __ldg(rl + gx) : 0u;
+        }
+        const int n = w + DC - 1;
+        for (int i = threadIdx.x; i < T * n; i += blockDim.x) {
+            const int k = i / n, ii = i - k * n;
+            const int gx = x0 - p.min_disp - DC * k - (DC - 1) + ii;
+            sl[w + k * cstr + G::coff(k) + ii] = (gx >= 0 && gx < W) ? __ldg(rr + gx) : 0u;
+        }
+    };
+    auto cost = [&](int yrow, int slot, uint32_t (&C)[NR]) {
+        const bool vx = yrow >= p.Q && yrow < H - p.Q && x >= p.R && x < W - p.R;
+        const uint32_t nbnb = (uint32_t)p.nb * 0x10001u;
+        if (!vx) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) C[k] = nbnb;
+            return;
+        }
+        const uint32_t* sl = cens + slot * sw;
+        const uint32_t clv = sl[xl];
+        // element for local disparity j (d = chunk*DC + j) at row[-j]
+        const uint32_t* row = sl + w + chunk * cstr + G::coff(chunk) + xl + (DC - 1);
+        const int lim = x - p.min_disp - p.R - chunk * DC;      // local j valid iff j <= lim
+        if (lim >= DC - 1) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k)
+                C[k] = __byte_perm(__popc(clv ^ row[-k]), __popc(clv ^ row[-(NR + k)]), 0x5410);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const uint32_t lo = k <= lim ? (uint32_t)__popc(clv ^ row[-k]) : (uint32_t)p.nb;
+                const uint32_t hi = NR + k <= lim ? (uint32_t)__popc(clv ^ row[-(NR + k)]) : (uint32_t)p.nb;
+                C[k] = __byte_perm(lo, hi, 0x5410);
+            }
+        }
+    };
+    constexpr int PW = DC / 4;                       // u32 words of the u8 partial per thread
+    const bool xin = x < W;
+    auto load_pin = [&](int yrow, uint32_t (&pw)[PW]) {
+        const uint4* src = reinterpret_cast<const uint4*>(
+            a.pin + frame * a.cell_stride + ((long long)yrow * W + (xin ? x : 0)) * D + chunk * DC);
+#pragma unroll
+        for (int q = 0; q < PW / 4; ++q) {
+            const uint4 v = __ldg(src + q);
+            pw[4 * q] = v.x; pw[4 * q + 1] = v.y; pw[4 * q + 2] = v.z; pw[4 * q + 3] = v.w;
+        }
+    };
+    auto arrive = [&]() { if (clustered) cluster_arrive(); else __syncthreads(); };
+    auto wait = [&]() { if (clustered) cluster_wait(); };
+
+    uint32_t Lv[NR], Ll[NR], Lr[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
+    uint32_t Mv = 0u, Ml = 0u, Mr = 0u;
+    uint32_t C[NR];
+    uint32_t pinw[PW];
+
+    stage(row_of(0), 0);
+    if (H > 1) stage(row_of(1), 1);
+    arrive();
+    wait();
+    cost(row_of(0), 0, C);
+    if (UP) load_pin(row_of(0), pinw);
+
+    for (int i = 0; i < H; ++i) {
+        const int y = row_of(i);
+        if (i > 0) wait();
+        // ---- vertical path: predecessor = own column
+        {
+            uint32_t Ln[NR], mnew;
+            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
+            Mv = mnew;
+        }
+        if (NP == 3) {
+            const int rs = (i + 1) & 1;              // slot written at row i-1
+            uint32_t Pp[NR], Mp;
+            // path "L": predecessor column x-1 (down-right / up-right)
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Pp[k] = __shfl_up_sync(FULL, Ll[k], T);
+            Mp = __shfl_up_sync(FULL, Ml, T);
+            if (col == 0) {
+                const uint32_t* h = hL + ((rs * nw + warp) * T + chunk) * NR;
+#pragma unroll
+                for (int k = 0; k < NR; ++k) Pp[k] = h[k];
+                Mp = hLM[rs * nw + warp];
+            }
+            path_update<NR, T>(p, chunk, Pp, Mp, C, Ll, Ml);
+            // path "R": predecessor column x+1 (down-left / up-left)
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Pp[k] = __shfl_down_sync(FULL, Lr[k], T);
+            Mp = __shfl_down_sync(FULL, Mr, T);
+            if (col == CPW - 1) {
+                const uint32_t* h = hR + ((rs * nw + warp) * T + chunk) * NR;
+#pragma unroll
+                for (int k = 0; k < NR; ++k) Pp[k] = h[k];
+                Mp = hRM[rs * nw + warp];
+            }
+            path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
+        }
+        // columns beyond the image act as "outside" predecessors: zero state
+        if (!xin) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
+            Mv = Ml = Mr = 0u;
+        }
+        // ---- partial sum out
+        if (xin) {
+            uint32_t s[NR];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) s[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
+            const long long cell = ((long long)y * W + x) * D + chunk * DC;
+            if (!UP) {
+                uint32_t o[PW];
+#pragma unroll
+                for (int q = 0; q < PW; ++q) o[q] = __byte_perm(s[2 * q], s[2 * q + 1], 0x6420);
+                uint4* dst = reinterpret_cast<uint4*>(a.pout8 + frame * a.cell_stride + cell);
+#pragma unroll
+                for (int q = 0; q < PW / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NR; ++k)
+                    s[k] += __byte_perm(pinw[k >> 1], 0u, (k & 1) ? 0x4342 : 0x4140);
+                uint32_t o[NR];
+                if (DPL_ROW == 4) {
+#pragma unroll
+                    for (int g = 0; g < DC / 4; ++g) {
+                        const int kk = 4 * g < NR ? 4 * g : 4 * g - NR;
+                        const uint32_t sel = 4 * g < NR ? 0x5410u : 0x7632u;
+                        o[2 * g] = __byte_perm(s[kk], s[kk + 2], sel);
+                        o[2 * g + 1] = __byte_perm(s[kk + 1], s[kk + 3], sel);
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < DC / 2; ++g) {
+                        const int kk = 2 * g < NR ? 2 * g : 2 * g - NR;
+                        const uint32_t sel = 2 * g < NR ? 0x5410u : 0x7632u;
+                        o[g] = __byte_perm(s[kk], s[kk + 1], sel);
+                    }
+                }
+                uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + cell);
+#pragma unroll
+                for (int q = 0; q < NR / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            }
+        }
+        // ---- halos for the next row (slot i & 1)
+        if (NP == 3) {
+            const int ws = i & 1;
+            if (col == CPW - 1) {            // my "L" state feeds column x+1 next row
+                uint32_t* dst = nullptr;
+                uint32_t* dstm = nullptr;
+                if (warp + 1 < nw) {
+                    dst = hL + ((ws * nw + warp + 1) * T + chunk) * NR;
+                    dstm = hLM + ws * nw + warp + 1;
+                } else if (rank + 1 < a.cs) {
+                    cg::cluster_group cl_g = cg::this_cluster();
+                    dst = cl_g.map_shared_rank(hL + ((ws * nw + 0) * T + chunk) * NR, rank + 1);
+                    dstm = cl_g.map_shared_rank(hLM + ws * nw + 0, rank + 1);
+                }
+                if (dst) {
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) dst[k] = Ll[k];
+                    if (chunk == 0) *dstm = Ml;
+                }
+            }
+            if (col == 0) {                  // my "R" state feeds column x-1 next row
+                uint32_t* dst = nullptr;
+                uint32_t* dstm = nullptr;
+                if (warp > 0) {
+                    dst = hR + ((ws * nw + warp - 1) * T + chunk) * NR;
+                    dstm = hRM + ws * nw + warp - 1;
+                } else if (rank > 0) {
+                    cg::cluster_group cl_g = cg::this_cluster();
+                    dst = cl_g.map_shared_rank(hR + ((ws * nw + nw - 1) * T + chunk) * NR, rank - 1);
+                    dstm = cl_g.map_shared_rank(hRM + ws * nw + nw - 1, rank - 1);
+                }
+                if (dst) {
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) dst[k] = Lr[k];
+                    if (chunk == 0) *dstm = Mr;
+                }
+            }
+        }
+        // ---- stage row i+2, publish, then compute row i+1's cost during the barrier
+        if (i + 2 < H) stage(row_of(i + 2), (i + 2) % 3);
+        arrive();
+        if (i + 1 < H) {
+            cost(row_of(i + 1), (i + 1) % 3, C);
+            if (UP) load_pin(row_of(i + 1), pinw);
+        }
+    }
+    wait();                                          // pairs with the last arrive
+}
+
+// ---------------------------------------------------------------- K_row
+struct RArgs {
+    DevParams p;
+    const uint32_t* cl;
+    const uint32_t* cr;
+    long long sig_stride;
+    const uint16_t* pab;      // [frames][H][W][D] row-kernel layout
+    uint8_t* stash;           // [frames][H][W][D] left->right path, u8
+    long long cell_stride;
+    FrameScratch fs;          // outputs for K5
+    long long px_stride;
+    uint16_t* agg;            // debug: S [H][W][D] natural order (frame 0), may be NULL
+    int nbuf;                 // rows of the S window (>= D + 32)
+    int bstride;              // u16 per window row (D + 4)
+};
+
+constexpr uint32_t NONE16 = 0xFFFFu;
+
+// Uniqueness + sub-pixel from (d*, S(d*), s2, S(d*-1), S(d*+1)) -- K4 semantics
+// (post.cu): PAPER.md P:289, readings c8, c13.
+__device__ __forceinline__ void finish_wta(const DevParams& p, int dstar, uint32_t s0, uint32_t s2,
+                                           uint32_t cm, uint32_t cp, bool& unique_fail, float& disp)
+{
+    unique_fail = p.uniq >= 0 && s2 != NONE16 &&
+                  (long long)s0 * (100 + (long long)p.uniq) >= (long long)s2 * 100;
+    float off = 0.0f;
+    if (p.subpix && dstar >= 1 && dstar <= p.D - 2 && cm != NONE16 && cp != NONE16) {
+        const int den = (int)cm - 2 * (int)s0 + (int)cp;
+        if (den > 0) {
+            off = __fdiv_rn((float)((int)cm - (int)cp), (float)(2 * den));
+            off = fminf(fmaxf(off, -0.5f), 0.5f);
+        }
+    }
+    disp = __fadd_rn((float)(p.min_disp + dstar), off);
+}
+
+template <int D> struct RowGeom {
+    static constexpr int DPL = D == 128 ? 4 : 2;     // disparities per lane
+    static constexpr int NRR = DPL / 2;              // u16x2 registers per lane
+    static constexpr int ACT = D / DPL;              // active lanes
+    static constexpr int NB = D + 32;                // rows of the S window
+    static constexpr int BS = D + 4;                 // u16 per window row (8-byte aligned rows)
+    static constexpr int KS = D <= 16 ? 4 : D <= 32 ? 5 : D <= 64 ? 6 : 7;   // key shift = log2(D)
+};
+
+// Left view, one pixel per lane, from its window row r[0..D) (natural order).
+// Pass 1: packed u16 keys (S << KS) | d, u16x2 min.  Pass 2: min of S with
+// d*-1..d*+1 poisoned (the row belongs to this lane alone), then restored.
+template <int D>
+__device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, int& dstar, bool& uf, float& disp)
+{
+    constexpr int KS = RowGeom<D>::KS;
+    uint32_t kmin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 0; q < D; q += 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(r + q);
+        const uint32_t k0 = v.x * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16));
+        const uint32_t k1 = v.y * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16));
+        kmin = vmin2(kmin, vmin2(k0, k1));
+    }
+    const uint32_t kb = min(kmin & 0xFFFFu, kmin >> 16);
+    dstar = (int)(kb & ((1u << KS) - 1u));
+    const uint32_t s0 = kb >> KS;
+    const uint32_t cm = dstar >= 1 ? r[dstar - 1] : NONE16;
+    const uint32_t cp = dstar + 1 < D ? r[dstar + 1] : NONE16;
+    if (dstar >= 1) r[dstar - 1] = (uint16_t)NONE16;
+    r[dstar] = (uint16_t)NONE16;
+    if (dstar + 1 < D) r[dstar + 1] = (uint16_t)NONE16;
+    uint32_t vm = 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 0; q < D; q += 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(r + q);
+        vm = vmin2(vm, vmin2(v.x, v.y));
+    }
+    if (dstar >= 1) r[dstar - 1] = (uint16_t)cm;
+    r[dstar] = (uint16_t)s0;
+    if (dstar + 1 < D) r[dstar + 1] = (uint16_t)cp;
+    finish_wta(p, dstar, s0, min(vm & 0xFFFFu, vm >> 16), cm, cp, uf, disp);
+}
+
+// Right view, one right pixel per lane: S_R(d) = S(xr + delta(d), d) lies on a
+// diagonal of the window (row (r0 + d) mod NB, column d); nd >= 1 defined d.
+template <int D>
+__device__ __forceinline__ void wta_right_lane(const DevParams& p, uint16_t* sb, int r0, int nd,
+                                               int& dstar, bool& uf, float& disp)
+{
+    constexpr int NB = RowGeom<D>::NB, BS = RowGeom<D>::BS, KS = RowGeom<D>::KS;
+    constexpr int STEP = BS + 1;
+    const int dwrap = NB - r0;                       // first d whose row wraps to 0
+    const uint16_t* b0 = sb + r0 * BS;
+    const uint16_t* b1 = b0 - NB * BS;
+    const int n0 = min(nd, dwrap);
+    uint32_t kmin = 0xFFFFFFFFu;
+#pragma unroll 8
+    for (int d = 0; d < n0; ++d) kmin = min(kmin, ((uint32_t)b0[d * STEP] << KS) | (uint32_t)d);
+#pragma unroll 8
+    for (int d = n0; d < nd; ++d) kmin = min(kmin, ((uint32_t)b1[d * STEP] << KS) | (uint32_t)d);
+    dstar = (int)(kmin & ((1u << KS) - 1u));
+    const uint32_t s0 = kmin >> KS;
+    auto at = [&](int d) -> uint16_t* { return const_cast<uint16_t*>((d < dwrap ? b0 : b1) + d * STEP); };
+    const uint32_t cm = dstar >= 1 ? *at(dstar - 1) : NONE16;
+    const uint32_t cp = dstar + 1 < nd ? *at(dstar + 1) : NONE16;
+    if (dstar >= 1) *at(dstar - 1) = (uint16_t)NONE16;
+    *at(dstar) = (uint16_t)NONE16;
+    if (dstar + 1 < nd) *at(dstar + 1) = (uint16_t)NONE16;
+    uint32_t vm = NONE16;
+#pragma unroll 8
+    for (int d = 0; d < n0; ++d) vm = min(vm, (uint32_t)b0[d * STEP]);
+#pragma unroll 8
+    for (int d = n0; d < nd; ++d) vm = min(vm, (uint32_t)b1[d * STEP]);
+    if (dstar >= 1) *at(dstar - 1) = (uint16_t)cm;
+    *at(dstar) = (uint16_t)s0;
+    if (dstar + 1 < nd) *at(dstar + 1) = (uint16_t)cp;
+    finish_wta(p, dstar, s0, vm, cm, cp, uf, disp);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* ptr)
+{
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
+}
+
+// One recursion step of a horizontal path for one warp (lane = DPL disparities).
+// Lp: predecessor state (zero at the line start), M: its min (0 at the start).
+template <int D>
+__device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint32_t clv, bool vx, int lim,
+                                             const uint32_t (&wnd)[RowGeom<D>::DPL],
+                                             const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t M,
+                                             uint32_t (&Ln)[RowGeom<D>::NRR])
+{
+    constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
+    const int d0 = lane * DPL;
+    uint32_t c[DPL];
+    if (vx && lim >= D - 1) {                         // warp-uniform fast path: all d valid
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) c[j] = __popc(clv ^ wnd[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) c[j] = (vx && d0 + j <= lim) ? (uint32_t)__popc(clv ^ wnd[j]) : (uint32_t)p.nb;
+    }
+    const uint32_t P1P1 = (uint32_t)p.p1 * 0x10001u;
+    const uint32_t MP2 = (M + (uint32_t)p.p2) * 0x10001u;
+    const uint32_t negMM = 0u - M * 0x10001u;
+    uint32_t lmin;
+    if constexpr (DPL == 4) {
+        // registers: A = (d0, d0+2), B = (d0+1, d0+3)
+        const uint32_t CA = __byte_perm(c[0], c[2], 0x5410), CB = __byte_perm(c[1], c[3], 0x5410);
+        const uint32_t QA = Lp[0] + P1P1, QB = Lp[NRR - 1] + P1P1;
+        uint32_t prevB = __shfl_up_sync(FULL, QB, 1);
+        uint32_t nextA = __shfl_down_sync(FULL, QA, 1);
+        if (lane == 0) prevB = INF2;
+        if (lane >= ACT - 1) nextA = INF2;
+        const uint32_t dm1A = __byte_perm(prevB, QB, 0x5432);
+        const uint32_t dp1B = __byte_perm(QA, nextA, 0x5432);
+        uint32_t tA = vmin2(vmin2(dm1A, QB), Lp[0]);
+        uint32_t tB = vmin2(vmin2(QA, dp1B), Lp[NRR - 1]);
+        tA = vmin2(tA, MP2);
+        tB = vmin2(tB, MP2);
+        Ln[0] = tA + CA + negMM;
+        Ln[NRR - 1] = tB + CB + negMM;
+        const uint32_t mm = vmin2(Ln[0], Ln[NRR - 1]);
+        lmin = min(mm & 0xFFFFu, mm >> 16);
+    } else {
+        // register: (d0, d0+1)
+        const uint32_t C0 = __byte_perm(c[0], c[1], 0x5410);
+        const uint32_t Q = Lp[0] + P1P1;
+        uint32_t prev = __shfl_up_sync(FULL, Q, 1);
+        uint32_t next = __shfl_down_sync(FULL, Q, 1);
+        if (lane == 0) prev = INF2;
+        if (lane >= ACT - 1) next = INF2;
+        const uint32_t dm1 = __byte_perm(prev, Q, 0x5432);
+        const uint32_t dp1 = __byte_perm(Q, next, 0x5432);
+        uint32_t t = vmin2(vmin2(dm1, dp1), Lp[0]);
+        t = vmin2(t, MP2);
+        Ln[0] = t + C0 + negMM;
+        lmin = min(Ln[0] & 0xFFFFu, Ln[0] >> 16);
+    }
+    if (lane >= ACT) lmin = 0xFFFFFFFFu;
+    return __reduce_min_sync(FULL, lmin);
+}
+
+template <int D>
+__global__ void __launch_bounds__(32)
+row_kernel(RArgs a)
+{
+    using G = RowGeom<D>;
+    constexpr int DPL = G::DPL, NRR = G::NRR, ACT = G::ACT, NB = G::NB, BS = G::BS;
+    constexpr int PF = 4;                             // register prefetch distance (steps)
+    constexpr int PL2 = 24;                           // L2 prefetch distance (steps)
+    extern __shared__ __align__(16) uint16_t sbuf[];  // [NB][BS]
+    const DevParams& p = a.p;
+    const int W = p.W;
+    const int y = blockIdx.x, frame = blockIdx.y;
+    const int lane = threadIdx.x;
+    const bool active = lane < ACT;
+    const int d0 = lane * DPL;
+    const uint32_t* cl = a.cl + frame * a.sig_stride + (long long)y * W;
+    const uint32_t* cr = a.cr + frame * a.sig_stride + (long long)y * W;
+    const long long rowcell = (long long)y * W * D;
+    uint8_t* stash = a.stash + frame * a.cell_stride + rowcell;
+    const uint16_t* pab = a.pab + frame * a.cell_stride + rowcell;
+    const bool vrow = y >= p.Q && y < p.H - p.Q;
+    auto crv = [&](int xr) -> uint32_t { return (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u; };
+    auto clv_at = [&](int x) -> uint32_t { return (x >= 0 && x < W) ? __ldg(cl + x) : 0u; };
+
+    // ------------------------------------------------ left -> right, stash L
+    {
+        uint32_t L[NRR], wnd[DPL];
+#pragma unroll
+        for (int k = 0; k < NRR; ++k) L[k] = 0u;
+        uint32_t M = 0u;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) wnd[j] = crv(0 - p.min_disp - d0 - j);
+        // prefetch ring: census words for steps x+1..x+PF (cl uniform, window edge for lane 0)
+        uint32_t pcl[PF], pin[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) { pcl[k] = clv_at(k + 1); pin[k] = crv(k + 1 - p.min_disp); }
+        uint32_t clv = clv_at(0);
+        for (int xb = 0; xb < W; xb += PF) {
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const int x = xb + k;
+                if (x < W) {
+                    const bool vx = vrow && x >= p.R && x < W - p.R;
+                    uint32_t Ln[NRR];
+                    M = row_step<D>(p, lane, clv, vx, x - p.min_disp - p.R, wnd, L, M, Ln);
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                    if (active) {
+                        if (DPL == 4)
+                            *reinterpret_cast<uint32_t*>(stash + (long long)x * D + d0) = __byte_perm(L[0], L[NRR - 1], 0x6420);
+                        else
+                            *reinterpret_cast<uint16_t*>(stash + (long long)x * D + d0) = (uint16_t)__byte_perm(L[0], 0u, 0x4420);
+                    }
+                    // slide the window to x+1; refill the prefetch slot with step x+1+PF
+                    const uint32_t in = __shfl_up_sync(FULL, wnd[DPL - 1], 1);
+#pragma unroll
+                    for (int j = DPL - 1; j > 0; --j) wnd[j] = wnd[j - 1];
+                    wnd[0] = lane == 0 ? pin[k] : in;
+                    clv = pcl[k];
+                    pcl[k] = clv_at(x + 1 + PF);
+                    pin[k] = lane == 0 ? crv(x + 1 + PF - p.min_disp) : 0u;
+                }
+            }
+        }
+    }
+    __syncwarp();
+    // ------------------------------------------------ right -> left + WTA
+    auto rowp = [&](int x) -> uint16_t* { return sbuf + (x % NB) * BS; };
+    // right pixels with no defined disparity at all: xr + min_disp >= W
+    for (int xr = max(0, W - p.min_disp) + lane; xr < W; xr += 32) {
+        const long long o = frame * a.px_stride + (long long)y * W + xr;
+        a.fs.dstar_r[o] = -1;
+        a.fs.mask_r[o] = MASK_BORDER;
+        a.fs.dr[o] = 0.0f;
+    }
+    {
+        uint32_t L[NRR], wnd[DPL];
+#pragma unroll
+        for (int k = 0; k < NRR; ++k) L[k] = 0u;
+        uint32_t M = 0u;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) wnd[j] = crv(W - 1 - p.min_disp - d0 - j);
+        // prefetch ring for steps x-1..x-PF: P_AB, stash, cl, window edge (lane ACT-1)
+        uint32_t pP[PF][NRR], pS[PF], pcl[PF], pin[PF];
+        auto load_step = [&](int x, uint32_t (&P)[NRR], uint32_t& S, uint32_t& c, uint32_t& e) {
+            if (x >= 0 && active) {
+                if (DPL == 4) {
+                    const uint2 u = __ldg(reinterpret_cast<const uint2*>(pab + (long long)x * D + d0));
+                    P[0] = u.x; P[NRR - 1] = u.y;
+                    S = __ldg(reinterpret_cast<const uint32_t*>(stash + (long long)x * D + d0));
+                } else {
+                    P[0] = __ldg(reinterpret_cast<const uint32_t*>(pab + (long long)x * D + d0));
+                    S = __ldg(reinterpret_cast<const uint16_t*>(stash + (long long)x * D + d0));
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < NRR; ++r) P[r] = 0u;
+                S = 0u;
+            }
+            c = clv_at(x);
+            e = lane == ACT - 1 ? crv(x - p.min_disp - d0 - (DPL - 1)) : 0u;
+        };
+        uint32_t curP[NRR], curS, clv, dummy;
+        load_step(W - 1, curP, curS, clv, dummy);
+#pragma unroll
+        for (int k = 0; k < PF; ++k) load_step(W - 2 - k, pP[k], pS[k], pcl[k], pin[k]);
+        for (int xb = W - 1; xb >= 0; xb -= PF) {
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const int x = xb - k;
+                if (x >= 0) {
+                    if (lane < 3 && x - PL2 >= 0) {    // pull step x-PL2 into L2
+                        const char* q = lane < 2 ? reinterpret_cast<const char*>(pab + (long long)(x - PL2) * D) + lane * 128
+                                                 : reinterpret_cast<const char*>(stash + (long long)(x - PL2) * D);
+                        prefetch_l2(q);
+                    }
+                    const bool vx = vrow && x >= p.R && x < W - p.R;
+                    uint32_t Ln[NRR];
+                    M = row_step<D>(p, lane, clv, vx, x - p.min_disp - p.R, wnd, L, M, Ln);
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                    // S = P_AB + L_lr + L_rl
+                    uint32_t Sv[NRR];
+                    if (DPL == 4) {
+                        Sv[0] = curP[0] + __byte_perm(curS, 0u, 0x4140) + Ln[0];
+                        Sv[NRR - 1] = curP[NRR - 1] + __byte_perm(curS, 0u, 0x4342) + Ln[NRR - 1];
+                    } else {
+                        Sv[0] = curP[0] + __byte_perm(curS, 0u, 0x4140) + Ln[0];
+                    }
+                    if (active) {
+                        uint16_t* r = rowp(x) + d0;
+                        if (DPL == 4) {
+                            const uint2 v = make_uint2(__byte_perm(Sv[0], Sv[NRR - 1], 0x5410),
+                                                       __byte_perm(Sv[0], Sv[NRR - 1], 0x7632));
+                            *reinterpret_cast<uint2*>(r) = v;
+                            if (a.agg && frame == 0)
+                                *reinterpret_cast<uint2*>(a.agg + rowcell + (long long)x * D + d0) = v;
+                        } else {
+                            *reinterpret_cast<uint32_t*>(r) = Sv[0];
+                            if (a.agg && frame == 0)
+                                *reinterpret_cast<uint32_t*>(a.agg + rowcell + (long long)x * D + d0) = Sv[0];
+                        }
+                    }
+                    // advance the prefetch ring: step x-1 becomes current, load x-1-PF
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) curP[r] = pP[k][r];
+                    curS = pS[k];
+                    const uint32_t clv_next = pcl[k];
+                    const uint32_t edge = pin[k];
+                    load_step(x - 1 - PF, pP[k], pS[k], pcl[k], pin[k]);
+                    __syncwarp();
+                    // ---- left WTA for pixels [x, x+32): their S rows are all in the window
+                    if ((x & 31) == 0) {
+                        const int xp = x + lane;
+                        if (xp < W) {
+                            int ds; bool uf; float disp;
+                            wta_left_lane<D>(p, rowp(xp), ds, uf, disp);
+                            const long long o = frame * a.px_stride + (long long)y * W + xp;
+                            uint8_t m = 0;
+                            if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
+                            if (uf) m |= MASK_UNIQUE;
+                            a.fs.dstar_l[o] = (int16_t)ds;
+                            a.fs.mask_l[o] = m;
+                            a.fs.dl[o] = disp;
+                        }
+                        __syncwarp();
+                    }
+                    // ---- right WTA for right pixels [x - min, x - min + 32) once complete
+                    if (x - p.min_disp >= 0 && ((x - p.min_disp) & 31) == 0) {
+                        const int xr = x - p.min_disp + lane;
+                        const int nd = min(D, W - p.min_disp - xr);
+                        if (xr < W) {
+                            int ds = -1; bool uf = false; float disp = 0.0f;
+                            if (nd > 0) wta_right_lane<D>(p, sbuf, (xr + p.min_disp) % NB, nd, ds, uf, disp);
+                            const long long o = frame * a.px_stride + (long long)y * W + xr;
+                            uint8_t m = 0;
+                            if (!(vrow && xr >= p.R && xr < W - p.R) || nd <= 0) m |= MASK_BORDER;
+                            if (uf) m |= MASK_UNIQUE;
+                            a.fs.dstar_r[o] = (int16_t)ds;
+                            a.fs.mask_r[o] = m;
+                            a.fs.dr[o] = disp;
+                        }
+                        __syncwarp();
+                    }
+                    // slide the census window to x-1
+                    const uint32_t in = __shfl_down_sync(FULL, wnd[0], 1);
+#pragma unroll
+                    for (int j = 0; j < DPL - 1; ++j) wnd[j] = wnd[j + 1];
+                    wnd[DPL - 1] = lane == ACT - 1 ? edge : in;
+                    clv = clv_next;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace v2
+
+// ======================================================================== host
+using v2::VArgs;
+using v2::RArgs;
+
+typedef void (*VKernel)(VArgs);
+typedef void (*RKernel)(RArgs);
+
+template <int DC, int T, int DPL>
+static VKernel vk(int np, bool up)
+{
+    if (np == 3) return up ? v2::vsweep_kernel<DC, T, 3, true, DPL> : v2::vsweep_kernel<DC, T, 3, false, DPL>;
+    return up ? v2::vsweep_kernel<DC, T, 1, true, DPL> : v2::vsweep_kernel<DC, T, 1, false, DPL>;
+}
+
+static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up)
+{
+    if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up);
+    if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up);
+    if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up);
+    if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up);
+    if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up);
+    return nullptr;
+}
+
+static RKernel pick_rkernel(int D)
+{
+    if (D == 16) return v2::row_kernel<16>;
+    if (D == 32) return v2::row_kernel<32>;
+    if (D == 64) return v2::row_kernel<64>;
+    if (D == 128) return v2::row_kernel<128>;
+    return nullptr;
+}
+
+static size_t vsmem_bytes(int w, int D, int T, int DC, int np)
+{
+    const int nw = w * T / 32;
+    (void)D;
+    const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
+    size_t words = 3 * ((size_t)w + (size_t)T * cstr);
+    if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
+    return words * 4;
+}
+
+bool v2_plan(const DevParams& p, int device, V2Plan& pl)
+{
+    pl = V2Plan{};
+    auto no = [&](const char* why) { snprintf(pl.why, sizeof pl.why, "%s", why); pl.ok = false; return false; };
+    if (p.nb > 32) return no("nb > 32 (u64 census)");
+    if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 128) return no("num_disp not in {16,32,64,128}");
+    const int np = p.paths == 8 ? 3 : 1;
+    if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");
+    int ks = 1;
+    while ((1 << ks) < p.D) ++ks;
+    const long long smax = (long long)p.paths * (p.nb + p.p2);
+    if ((smax << ks) + (1 << ks) - 1 > 0xFFFE) return no("S << log2(D) exceeds 16-bit WTA keys");
+    pl.NP = np;
+    pl.DPL = p.D <= 64 ? 2 : 4;
+    if (p.D == 16) { pl.DC = 16; pl.T = 1; }
+    else if (p.D == 32) { pl.DC = 32; pl.T = 1; }
+    else if (p.D == 64) { pl.DC = 32; pl.T = 2; }
+    else { pl.DC = 32; pl.T = 4; }
+    const char* force = getenv("ASD_V2_DC16");
+    if (p.D == 128 && force && force[0] == '1') { pl.DC = 16; pl.T = 8; }
+    const int T = pl.T, CPW = 32 / T;
+    const int maxt = pl.DC == 32 ? 512 : 1024;
+    VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false);
+    VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true);
+    if (!kd || !ku) return no("no sweep kernel instance");
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    double best = -1.0;
+    for (int cs = 1; cs <= 16; ++cs) {
+        int w = (p.W + cs - 1) / cs;
+        w = (w + CPW - 1) / CPW * CPW;
+        if ((long long)w * (cs - 1) >= p.W && cs > 1) continue;     // last CTA would be empty
+        const int threads = w * T;
+        if (threads > maxt) continue;
+        if (np == 1 && cs > 1 && threads < 128) continue;
+        const size_t sm = vsmem_bytes(w, p.D, T, pl.DC, np);
+        if (sm > 200 * 1024) continue;
+        for (VKernel k : {kd, ku}) {
+            cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (cs > 8) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
+        int active = 0;
+        if (np == 3 && cs > 1) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(cs, 64);
+            cfg.blockDim = dim3(threads);
+            cfg.dynamicSmemBytes = sm;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at; cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, (const void*)ku, &cfg) != cudaSuccess) { cudaGetLastError(); continue; }
+            active = nc * cs;
+        } else {
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)ku, threads, sm) != cudaSuccess) { cudaGetLastError(); continue; }
+            active = nb * nsm;
+        }
+        if (active <= 0) continue;
+        // throughput proxy: resident threads, penalising clusters that leave SMs idle
+        const double score = (double)active * threads;
+        if (score > best * 1.02) { best = score; pl.cs = cs; pl.w = w; pl.vthreads = threads; pl.vsmem = sm; pl.active_ctas = active; }
+        if (np == 1) break;
+    }
+    if (best < 0) return no("no feasible cluster configuration");
+    for (VKernel k : {kd, ku})
+        cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+    if (np == 1) {
+        // vertical-only sweeps have no cross-column dependency: 1-CTA strips
+        int w = (256 / T + CPW - 1) / CPW * CPW;
+        if (w > (p.W + CPW - 1) / CPW * CPW) w = (p.W + CPW - 1) / CPW * CPW;
+        pl.w = w;
+        pl.cs = (p.W + w - 1) / w;
+        pl.vthreads = w * T;
+        pl.vsmem = vsmem_bytes(w, p.D, T, pl.DC, np);
+        for (VKernel k : {kd, ku})
+            cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+    }
+    pl.nbuf = p.D + 32;
+    pl.bstride = p.D + 4;
+    pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
+    RKernel rk = pick_rkernel(p.D);
+    cudaFuncSetAttribute((const void*)rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.rsmem);
+    cudaGetLastError();
+    pl.ok = true;
+    return true;
+}
+
+static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const VArgs& a, cudaStream_t s)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.cs, nframes);
+    cfg.blockDim = dim3(pl.vthreads);
+    cfg.dynamicSmemBytes = pl.vsmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pl.cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pl.NP == 3 && pl.cs > 1) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes,
+                    const void* cl, const void* cr, long long sig_stride,
+                    uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,
+                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s)
+{
+    if (stage == 0 || stage == 1) {
+        VArgs a{};
+        a.p = p; a.w = pl.w; a.cs = pl.cs;
+        a.cl = (const uint32_t*)cl; a.cr = (const uint32_t*)cr; a.sig_stride = sig_stride;
+        a.pin = pa; a.pout8 = pa; a.pout16 = pab; a.cell_stride = cell_stride;
+        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1);
+        return launch_vsweep(k, pl, nframes, a, s) == cudaSuccess ? 0 : -1;
+    }
+    RArgs r{};
+    r.p = p; r.cl = (const uint32_t*)cl; r.cr = (const uint32_t*)cr; r.sig_stride = sig_stride;
+    r.pab = pab; r.stash = stash; r.cell_stride = cell_stride; r.fs = fs; r.px_stride = px_stride;
+    r.agg = agg; r.nbuf = pl.nbuf; r.bstride = pl.bstride;
+    RKernel k = pick_rkernel(p.D);
+    k<<<dim3(p.H, nframes), 32, pl.rsmem, s>>>(r);
+    return 0;
+}
+
+}  // namespace asd

@@ -12,10 +12,11 @@ def params_pair(d: dict):
     return asd.Params(**d), oracle.Params(**d)
 
 
-def gpu_debug(d: dict, left: np.ndarray, right: np.ndarray) -> dict:
-    """All stage outputs of one frame via asd_depth_debug."""
+def gpu_debug(d: dict, left: np.ndarray, right: np.ndarray, engine: int = 0) -> dict:
+    """All stage outputs of one frame via asd_depth_debug (engine: 0 auto, 1 D1, 3 D3)."""
+    import pytest
     import torch
-    p = asd.Params(**d)
+    p = asd.Params(**d, engine=engine)
     H, W, D = p.height, p.width, p.num_disp
     dev = "cuda"
     sig = torch.int32 if p.nbits <= 32 else torch.int64
@@ -35,7 +36,14 @@ def gpu_debug(d: dict, left: np.ndarray, right: np.ndarray) -> dict:
     depth = torch.empty(H, W, dtype=torch.float32, device=dev)
     L = torch.from_numpy(np.ascontiguousarray(left)).to(dev)
     R = torch.from_numpy(np.ascontiguousarray(right)).to(dev)
-    with asd.Stereo(p, 0, 1) as st:
+    try:
+        st = asd.Stereo(p, 0, 1)
+    except asd.AsdError as e:
+        if engine == 3 and e.code == asd.ASD_E_UNSUPPORTED:
+            pytest.skip(f"outside the D3 envelope: {e}")
+        raise
+    with st:
+        assert engine == 0 or st.engine == engine
         st.asd_depth_debug(L, R, outs, disp, depth)
         torch.cuda.synchronize()
     g = {k: v.cpu().numpy() for k, v in outs.items()}

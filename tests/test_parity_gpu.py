@@ -13,6 +13,8 @@ from tests.gpu_util import (assert_bits_equal, assert_depth_close, assert_equal,
 
 pytestmark = pytest.mark.gpu
 
+ENGINES = [pytest.param(1, id="D1"), pytest.param(3, id="D3")]
+
 
 def _cfg(name, **kw):
     d = synth.CONFIGS[name].params_dict()
@@ -20,27 +22,30 @@ def _cfg(name, **kw):
     return d
 
 
-def _run(d, left, right):
+def _run(d, left, right, engine=0):
     o = oracle.compute(oracle.Params(**d), left, right, debug=True)
-    g = gpu_debug(d, left, right)
+    g = gpu_debug(d, left, right, engine)
     compare_full(g, o)
     return g, o
 
 
-def test_config_A_shift7():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config_A_shift7(engine):
     left, right, _ = synth.make_pair("A", 0)
-    g, o = _run(_cfg("A"), left, right)
+    g, o = _run(_cfg("A"), left, right, engine)
     assert (g["dstar_l"][2:-2, 9:-2] == 7).mean() >= 0.99
 
 
-def test_config_A_fractional():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config_A_fractional(engine):
     left, right, _ = synth.shift_pair(64, 48, 6.5, frame_idx=3)
-    _run(_cfg("A"), left, right)
+    _run(_cfg("A"), left, right, engine)
 
 
-def test_config_B_full():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config_B_full(engine):
     left, right, _ = synth.make_pair("B", 0)
-    _run(_cfg("B"), left, right)
+    _run(_cfg("B"), left, right, engine)
 
 
 FUZZ = [
@@ -58,8 +63,23 @@ FUZZ = [
 ]
 
 
-@pytest.mark.parametrize("case", FUZZ)
-def test_fuzz(case):
+# inside the D3 envelope (nb <= 32, D in {16,32,64,128}, u8 partial, 16-bit keys):
+# ragged widths, several cluster CTAs, W < D, P1=P2=0, 4-path at D=128, nb = 32
+FUZZ_D3 = [
+    (300, 37, 128, 0, 9, 7, 8, 32, 8, 10, 1.0, 1),
+    (257, 21, 64, 5, 7, 7, 3, 20, 8, 15, 0.5, 1),
+    (129, 40, 32, 0, 5, 5, 0, 0, 8, 10, 1.0, 1),
+    (97, 33, 16, 2, 3, 3, 1, 2, 4, 0, 2.0, 0),
+    (1000, 12, 128, 3, 13, 5, 10, 30, 8, -1, -1.0, 1),
+    (640, 30, 128, 0, 9, 7, 8, 32, 4, 10, 1.0, 1),
+    (33, 50, 64, 0, 9, 7, 8, 32, 8, 10, 1.0, 1),
+    (2000, 8, 128, 0, 9, 7, 8, 32, 8, 10, 1.0, 1),
+]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("case", FUZZ + FUZZ_D3)
+def test_fuzz(case, engine):
     W, H, D, md, cw, ch, p1, p2, paths, u, lr, sp = case
     d = dict(width=W, height=H, num_disp=D, min_disp=md, census_w=cw, census_h=ch, p1=p1, p2=p2,
              paths=paths, uniqueness=u, lr_max_diff=lr, subpixel=sp, focal_px=321.5, baseline_m=0.05)
@@ -70,22 +90,24 @@ def test_fuzz(case):
     right = T[:, shift:shift + W].copy()
     noise = rng.integers(0, 2, size=right.shape, dtype=np.uint8)
     right = np.where(rng.random(right.shape) < 0.1, right ^ noise, right).astype(np.uint8)
-    _run(d, left, right)
+    _run(d, left, right, engine)
 
 
-def test_textureless_and_constant():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_textureless_and_constant(engine):
     d = _cfg("A")
     z = np.zeros((48, 64), np.uint8)
-    g, o = _run(d, z, z)
+    g, o = _run(d, z, z, engine)
     assert (g["mask"] != 0).mean() >= 0.99
     c = np.full((48, 64), 200, np.uint8)
-    _run(d, c, z)
+    _run(d, c, z, engine)
 
 
-def test_config_C_full_frame():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config_C_full_frame(engine):
     """One full 1280x720 D128 8-path frame, every stage, bit-exact."""
     left, right, _ = synth.make_pair("C", 0)
-    _run(_cfg("C"), left, right)
+    _run(_cfg("C"), left, right, engine)
 
 
 def test_config_D_sampled():
