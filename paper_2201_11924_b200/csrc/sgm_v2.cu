@@ -51,6 +51,16 @@ __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b)
     return r;
 }
 
+// 4-byte asynchronous global->shared copy (LDGSTS); src_size 0 zero-fills.
+__device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc, bool valid)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" :: "r"(sa), "l"(gsrc), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
+
 __device__ __forceinline__ void cluster_arrive()
 {
     asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -74,14 +84,16 @@ struct VArgs {
 };
 
 // ---------------------------------------------------------------- helpers
+// Mp is the predecessor's min over d packed in both halves (M | M << 16);
+// mout returns the new one the same way, so no scalar->packed IMAD is needed
+// and the normalisation folds into one IADD3 per register.
 template <int NR, int T>
 __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const uint32_t (&P)[NR],
                                             uint32_t Mp, const uint32_t (&C)[NR], uint32_t (&Ln)[NR],
                                             uint32_t& mout)
 {
     const uint32_t P1P1 = (uint32_t)p.p1 * 0x10001u;
-    const uint32_t MP2 = (Mp + (uint32_t)p.p2) * 0x10001u;
-    const uint32_t negMM = 0u - Mp * 0x10001u;
+    const uint32_t MP2 = Mp + (uint32_t)p.p2 * 0x10001u;
     uint32_t Q[NR];
 #pragma unroll
     for (int k = 0; k < NR; ++k) Q[k] = P[k] + P1P1;
@@ -99,12 +111,12 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
         const uint32_t dp1 = k < NR - 1 ? Q[k + 1] : __byte_perm(Q[0], qnext, 0x5432);
         uint32_t t = vmin2(vmin2(dm1, dp1), P[k]);
         t = vmin2(t, MP2);
-        Ln[k] = t + C[k] + negMM;
+        Ln[k] = t + C[k] - Mp;
         macc = vmin2(macc, Ln[k]);
     }
-    uint32_t m = min(macc & 0xFFFFu, macc >> 16);
+    uint32_t m = vmin2(macc, __byte_perm(macc, macc, 0x1032));      // (min, min)
 #pragma unroll
-    for (int o = 1; o < T; o <<= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+    for (int o = 1; o < T; o <<= 1) m = vmin2(m, __shfl_xor_sync(FULL, m, o));
     mout = m;
 }
 
@@ -145,8 +157,8 @@ vsweep_kernel(VArgs a)
     const int sw = G::slot_words(w);
     const bool clustered = NP == 3 && a.cs > 1;
 
-    uint32_t* cens = smem;                   // [3][sw]: left row, then T right-row slices
-    uint32_t* hL = cens + 3 * sw;            // [2][nw][T][NR]   (NP == 3)
+    uint32_t* cens = smem;                   // [4][sw]: left row, then T right-row slices
+    uint32_t* hL = cens + 4 * sw;            // [2][nw][T][NR]   (NP == 3)
     uint32_t* hR = hL + 2 * nw * T * NR;
     uint32_t* hLM = hR + 2 * nw * T * NR;    // [2][nw]
     uint32_t* hRM = hLM + 2 * nw;
@@ -158,23 +170,31 @@ vsweep_kernel(VArgs a)
         for (int i = threadIdx.x; i < 4 * nw * T * NR + 4 * nw; i += blockDim.x) hL[i] = 0u;
     }
     auto row_of = [&](int i) { return UP ? H - 1 - i : i; };
+    // census rows -> shared memory with asynchronous copies (one commit group per row)
     auto stage = [&](int yrow, int slot) {
         uint32_t* sl = cens + slot * sw;
         const uint32_t* rl = cl + (long long)yrow * W;
         const uint32_t* rr = cr + (long long)yrow * W;
         for (int i = threadIdx.x; i < w; i += blockDim.x) {
             const int gx = x0 + i;
-            sl[i] = gx < W ? __ldg(rl + gx) : 0u;
+            cp_async4(sl + i, gx < W ? rl + gx : rl, gx < W);
         }
         const int n = w + DC - 1;
-        for (int i = threadIdx.x; i < T * n; i += blockDim.x) {
-            const int k = i / n, ii = i - k * n;
-            const int gx = x0 - p.min_disp - DC * k - (DC - 1) + ii;
-            sl[w + k * cstr + G::coff(k) + ii] = (gx >= 0 && gx < W) ? __ldg(rr + gx) : 0u;
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+            uint32_t* dst = sl + w + k * cstr + G::coff(k);
+            const int g0 = x0 - p.min_disp - DC * k - (DC - 1);
+            for (int ii = threadIdx.x; ii < n; ii += blockDim.x) {
+                const int gx = g0 + ii;
+                const bool ok = gx >= 0 && gx < W;
+                cp_async4(dst + ii, ok ? rr + gx : rr, ok);
+            }
         }
+        cp_async_commit();
     };
+    const bool vcol = x >= p.R && x < W - p.R;
     auto cost = [&](int yrow, int slot, uint32_t (&C)[NR]) {
-        const bool vx = yrow >= p.Q && yrow < H - p.Q && x >= p.R && x < W - p.R;
+        const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q;
         const uint32_t nbnb = (uint32_t)p.nb * 0x10001u;
         if (!vx) {
 #pragma unroll
@@ -222,6 +242,8 @@ vsweep_kernel(VArgs a)
 
     stage(row_of(0), 0);
     if (H > 1) stage(row_of(1), 1);
+    if (H > 2) stage(row_of(2), 2);
+    cp_async_wait<0>();
     arrive();
     wait();
     cost(row_of(0), 0, C);
@@ -246,9 +268,12 @@ vsweep_kernel(VArgs a)
             for (int k = 0; k < NR; ++k) Pp[k] = __shfl_up_sync(FULL, Ll[k], T);
             Mp = __shfl_up_sync(FULL, Ml, T);
             if (col == 0) {
-                const uint32_t* h = hL + ((rs * nw + warp) * T + chunk) * NR;
+                const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * NR);
 #pragma unroll
-                for (int k = 0; k < NR; ++k) Pp[k] = h[k];
+                for (int q = 0; q < NR / 4; ++q) {
+                    const uint4 v = h[q];
+                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
+                }
                 Mp = hLM[rs * nw + warp];
             }
             path_update<NR, T>(p, chunk, Pp, Mp, C, Ll, Ml);
@@ -257,9 +282,12 @@ vsweep_kernel(VArgs a)
             for (int k = 0; k < NR; ++k) Pp[k] = __shfl_down_sync(FULL, Lr[k], T);
             Mp = __shfl_down_sync(FULL, Mr, T);
             if (col == CPW - 1) {
-                const uint32_t* h = hR + ((rs * nw + warp) * T + chunk) * NR;
+                const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * NR);
 #pragma unroll
-                for (int k = 0; k < NR; ++k) Pp[k] = h[k];
+                for (int q = 0; q < NR / 4; ++q) {
+                    const uint4 v = h[q];
+                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
+                }
                 Mp = hRM[rs * nw + warp];
             }
             path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
@@ -270,7 +298,52 @@ vsweep_kernel(VArgs a)
             for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
             Mv = Ml = Mr = 0u;
         }
-        // ---- partial sum out
+        // ---- halos for the next row (slot i & 1)
+        if (NP == 3) {
+            const int ws = i & 1;
+            if (col == CPW - 1) {            // my "L" state feeds column x+1 next row
+                uint32_t* dst = nullptr;
+                uint32_t* dstm = nullptr;
+                if (warp + 1 < nw) {
+                    dst = hL + ((ws * nw + warp + 1) * T + chunk) * NR;
+                    dstm = hLM + ws * nw + warp + 1;
+                } else if (rank + 1 < a.cs) {
+                    cg::cluster_group cl_g = cg::this_cluster();
+                    dst = cl_g.map_shared_rank(hL + ((ws * nw + 0) * T + chunk) * NR, rank + 1);
+                    dstm = cl_g.map_shared_rank(hLM + ws * nw + 0, rank + 1);
+                }
+                if (dst) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                    for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]);
+                    if (chunk == 0) *dstm = Ml;
+                }
+            }
+            if (col == 0) {                  // my "R" state feeds column x-1 next row
+                uint32_t* dst = nullptr;
+                uint32_t* dstm = nullptr;
+                if (warp > 0) {
+                    dst = hR + ((ws * nw + warp - 1) * T + chunk) * NR;
+                    dstm = hRM + ws * nw + warp - 1;
+                } else if (rank > 0) {
+                    cg::cluster_group cl_g = cg::this_cluster();
+                    dst = cl_g.map_shared_rank(hR + ((ws * nw + nw - 1) * T + chunk) * NR, rank - 1);
+                    dstm = cl_g.map_shared_rank(hRM + ws * nw + nw - 1, rank - 1);
+                }
+                if (dst) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                    for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
+                    if (chunk == 0) *dstm = Mr;
+                }
+            }
+        }
+        // ---- stage row i+3 (async), make row i+2's copies complete, publish
+        if (i + 3 < H) stage(row_of(i + 3), (i + 3) & 3);
+        else cp_async_commit();                      // keep one group per row
+        cp_async_wait<1>();
+        arrive();
+        // ---- partial sum out (after the release so it does not wait on these stores)
         if (xin) {
             uint32_t s[NR];
 #pragma unroll
@@ -309,49 +382,9 @@ vsweep_kernel(VArgs a)
                 for (int q = 0; q < NR / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
             }
         }
-        // ---- halos for the next row (slot i & 1)
-        if (NP == 3) {
-            const int ws = i & 1;
-            if (col == CPW - 1) {            // my "L" state feeds column x+1 next row
-                uint32_t* dst = nullptr;
-                uint32_t* dstm = nullptr;
-                if (warp + 1 < nw) {
-                    dst = hL + ((ws * nw + warp + 1) * T + chunk) * NR;
-                    dstm = hLM + ws * nw + warp + 1;
-                } else if (rank + 1 < a.cs) {
-                    cg::cluster_group cl_g = cg::this_cluster();
-                    dst = cl_g.map_shared_rank(hL + ((ws * nw + 0) * T + chunk) * NR, rank + 1);
-                    dstm = cl_g.map_shared_rank(hLM + ws * nw + 0, rank + 1);
-                }
-                if (dst) {
-#pragma unroll
-                    for (int k = 0; k < NR; ++k) dst[k] = Ll[k];
-                    if (chunk == 0) *dstm = Ml;
-                }
-            }
-            if (col == 0) {                  // my "R" state feeds column x-1 next row
-                uint32_t* dst = nullptr;
-                uint32_t* dstm = nullptr;
-                if (warp > 0) {
-                    dst = hR + ((ws * nw + warp - 1) * T + chunk) * NR;
-                    dstm = hRM + ws * nw + warp - 1;
-                } else if (rank > 0) {
-                    cg::cluster_group cl_g = cg::this_cluster();
-                    dst = cl_g.map_shared_rank(hR + ((ws * nw + nw - 1) * T + chunk) * NR, rank - 1);
-                    dstm = cl_g.map_shared_rank(hRM + ws * nw + nw - 1, rank - 1);
-                }
-                if (dst) {
-#pragma unroll
-                    for (int k = 0; k < NR; ++k) dst[k] = Lr[k];
-                    if (chunk == 0) *dstm = Mr;
-                }
-            }
-        }
-        // ---- stage row i+2, publish, then compute row i+1's cost during the barrier
-        if (i + 2 < H) stage(row_of(i + 2), (i + 2) % 3);
-        arrive();
+        // ---- next row's cost while the barrier completes
         if (i + 1 < H) {
-            cost(row_of(i + 1), (i + 1) % 3, C);
+            cost(row_of(i + 1), (i + 1) & 3, C);
             if (UP) load_pin(row_of(i + 1), pinw);
         }
     }
@@ -398,7 +431,7 @@ template <int D> struct RowGeom {
     static constexpr int DPL = D == 128 ? 4 : 2;     // disparities per lane
     static constexpr int NRR = DPL / 2;              // u16x2 registers per lane
     static constexpr int ACT = D / DPL;              // active lanes
-    static constexpr int NB = D + 32;                // rows of the S window
+    static constexpr int NB = D + 40;                // rows of the S window (D + 32 + one sub-group)
     static constexpr int BS = D + 4;                 // u16 per window row (8-byte aligned rows)
     static constexpr int KS = D <= 16 ? 4 : D <= 32 ? 5 : D <= 64 ? 6 : 7;   // key shift = log2(D)
 };
@@ -544,8 +577,7 @@ row_kernel(RArgs a)
 {
     using G = RowGeom<D>;
     constexpr int DPL = G::DPL, NRR = G::NRR, ACT = G::ACT, NB = G::NB, BS = G::BS;
-    constexpr int PF = 4;                             // register prefetch distance (steps)
-    constexpr int PL2 = 24;                           // L2 prefetch distance (steps)
+    constexpr int SG = 8;                             // steps per unrolled sub-group
     extern __shared__ __align__(16) uint16_t sbuf[];  // [NB][BS]
     const DevParams& p = a.p;
     const int W = p.W;
@@ -556,11 +588,20 @@ row_kernel(RArgs a)
     const uint32_t* cl = a.cl + frame * a.sig_stride + (long long)y * W;
     const uint32_t* cr = a.cr + frame * a.sig_stride + (long long)y * W;
     const long long rowcell = (long long)y * W * D;
-    uint8_t* stash = a.stash + frame * a.cell_stride + rowcell;
-    const uint16_t* pab = a.pab + frame * a.cell_stride + rowcell;
+    uint8_t* stash = a.stash + frame * a.cell_stride + rowcell + d0;     // lane's slot of pixel 0
+    const uint16_t* pab = a.pab + frame * a.cell_stride + rowcell + d0;
     const bool vrow = y >= p.Q && y < p.H - p.Q;
-    auto crv = [&](int xr) -> uint32_t { return (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u; };
-    auto clv_at = [&](int x) -> uint32_t { return (x >= 0 && x < W) ? __ldg(cl + x) : 0u; };
+    const int lim0 = -p.min_disp - p.R;              // d valid iff d <= x + lim0
+    // a 32-column group is "fast" when every x in it has a valid census window
+    // and every disparity a valid right pixel
+    auto group_fast = [&](int xb) {
+        return vrow && xb + 31 < W && xb >= p.R && xb + 31 < W - p.R && xb + lim0 >= D - 1;
+    };
+    auto blk = [&](const uint32_t* row, int i0) -> uint32_t {
+        const int i = i0 + lane;
+        return (i >= 0 && i < W) ? __ldg(row + i) : 0u;
+    };
+    const int ngrp = (W + 31) >> 5;
 
     // ------------------------------------------------ left -> right, stash L
     {
@@ -569,43 +610,49 @@ row_kernel(RArgs a)
         for (int k = 0; k < NRR; ++k) L[k] = 0u;
         uint32_t M = 0u;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) wnd[j] = crv(0 - p.min_disp - d0 - j);
-        // prefetch ring: census words for steps x+1..x+PF (cl uniform, window edge for lane 0)
-        uint32_t pcl[PF], pin[PF];
+        for (int j = 0; j < DPL; ++j) {
+            const int xr = 0 - p.min_disp - d0 - j;
+            wnd[j] = (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u;
+        }
+        uint32_t clb = blk(cl, 0);                   // cl[32g + j]
+        uint32_t crb = blk(cr, 1 - p.min_disp);      // cr[32g + j + 1 - min]: enters the window after step 32g + j
+        for (int g = 0; g < ngrp; ++g) {
+            const int xb = g << 5;
+            const uint32_t clb_n = blk(cl, xb + 32);
+            const uint32_t crb_n = blk(cr, xb + 33 - p.min_disp);
+            const bool fast = group_fast(xb);
+            uint8_t* sp = stash + (long long)xb * D;
+            for (int s = 0; s < 32; s += SG) {
 #pragma unroll
-        for (int k = 0; k < PF; ++k) { pcl[k] = clv_at(k + 1); pin[k] = crv(k + 1 - p.min_disp); }
-        uint32_t clv = clv_at(0);
-        for (int xb = 0; xb < W; xb += PF) {
+                for (int k = 0; k < SG; ++k) {
+                    const int j = s + k, x = xb + j;
+                    if (x < W) {
+                        const uint32_t clv = __shfl_sync(FULL, clb, j);
+                        const bool vx = fast || (vrow && x >= p.R && x < W - p.R);
+                        uint32_t Ln[NRR];
+                        M = row_step<D>(p, lane, clv, vx, fast ? D : x + lim0, wnd, L, M, Ln);
 #pragma unroll
-            for (int k = 0; k < PF; ++k) {
-                const int x = xb + k;
-                if (x < W) {
-                    const bool vx = vrow && x >= p.R && x < W - p.R;
-                    uint32_t Ln[NRR];
-                    M = row_step<D>(p, lane, clv, vx, x - p.min_disp - p.R, wnd, L, M, Ln);
+                        for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                        if (active) {
+                            if constexpr (DPL == 4)
+                                *reinterpret_cast<uint32_t*>(sp + j * D) = __byte_perm(L[0], L[NRR - 1], 0x6420);
+                            else
+                                *reinterpret_cast<uint16_t*>(sp + j * D) = (uint16_t)__byte_perm(L[0], 0u, 0x4420);
+                        }
+                        const uint32_t in = __shfl_up_sync(FULL, wnd[DPL - 1], 1);
+                        const uint32_t e = __shfl_sync(FULL, crb, j);
 #pragma unroll
-                    for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                    if (active) {
-                        if (DPL == 4)
-                            *reinterpret_cast<uint32_t*>(stash + (long long)x * D + d0) = __byte_perm(L[0], L[NRR - 1], 0x6420);
-                        else
-                            *reinterpret_cast<uint16_t*>(stash + (long long)x * D + d0) = (uint16_t)__byte_perm(L[0], 0u, 0x4420);
+                        for (int q = DPL - 1; q > 0; --q) wnd[q] = wnd[q - 1];
+                        wnd[0] = lane == 0 ? e : in;
                     }
-                    // slide the window to x+1; refill the prefetch slot with step x+1+PF
-                    const uint32_t in = __shfl_up_sync(FULL, wnd[DPL - 1], 1);
-#pragma unroll
-                    for (int j = DPL - 1; j > 0; --j) wnd[j] = wnd[j - 1];
-                    wnd[0] = lane == 0 ? pin[k] : in;
-                    clv = pcl[k];
-                    pcl[k] = clv_at(x + 1 + PF);
-                    pin[k] = lane == 0 ? crv(x + 1 + PF - p.min_disp) : 0u;
                 }
             }
+            clb = clb_n;
+            crb = crb_n;
         }
     }
     __syncwarp();
     // ------------------------------------------------ right -> left + WTA
-    auto rowp = [&](int x) -> uint16_t* { return sbuf + (x % NB) * BS; };
     // right pixels with no defined disparity at all: xr + min_disp >= W
     for (int xr = max(0, W - p.min_disp) + lane; xr < W; xr += 32) {
         const long long o = frame * a.px_stride + (long long)y * W + xr;
@@ -613,123 +660,151 @@ row_kernel(RArgs a)
         a.fs.mask_r[o] = MASK_BORDER;
         a.fs.dr[o] = 0.0f;
     }
+    auto right_batch = [&](int XR) {                  // right pixels [XR, XR+32), all complete
+        const int xr = XR + lane;
+        const int nd = min(D, W - p.min_disp - xr);
+        if (xr >= 0 && xr < W) {
+            int ds = -1; bool uf = false; float disp = 0.0f;
+            if (nd > 0) wta_right_lane<D>(p, sbuf, (xr + p.min_disp) % NB, nd, ds, uf, disp);
+            const long long o = frame * a.px_stride + (long long)y * W + xr;
+            uint8_t m = 0;
+            if (!(vrow && xr >= p.R && xr < W - p.R) || nd <= 0) m |= MASK_BORDER;
+            if (uf) m |= MASK_UNIQUE;
+            a.fs.dstar_r[o] = (int16_t)ds;
+            a.fs.mask_r[o] = m;
+            a.fs.dr[o] = disp;
+        }
+        __syncwarp();
+    };
     {
         uint32_t L[NRR], wnd[DPL];
 #pragma unroll
         for (int k = 0; k < NRR; ++k) L[k] = 0u;
         uint32_t M = 0u;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) wnd[j] = crv(W - 1 - p.min_disp - d0 - j);
-        // prefetch ring for steps x-1..x-PF: P_AB, stash, cl, window edge (lane ACT-1)
-        uint32_t pP[PF][NRR], pS[PF], pcl[PF], pin[PF];
-        auto load_step = [&](int x, uint32_t (&P)[NRR], uint32_t& S, uint32_t& c, uint32_t& e) {
-            if (x >= 0 && active) {
-                if (DPL == 4) {
-                    const uint2 u = __ldg(reinterpret_cast<const uint2*>(pab + (long long)x * D + d0));
-                    P[0] = u.x; P[NRR - 1] = u.y;
-                    S = __ldg(reinterpret_cast<const uint32_t*>(stash + (long long)x * D + d0));
-                } else {
-                    P[0] = __ldg(reinterpret_cast<const uint32_t*>(pab + (long long)x * D + d0));
-                    S = __ldg(reinterpret_cast<const uint16_t*>(stash + (long long)x * D + d0));
-                }
-            } else {
+        for (int j = 0; j < DPL; ++j) {
+            const int xr = W - 1 - p.min_disp - d0 - j;
+            wnd[j] = (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u;
+        }
+        // per sub-group register prefetch of P_AB and the stash (8 steps ahead)
+        uint32_t P[SG][NRR], Sx[SG], Pn[SG][NRR], Sn[SG];
+        auto load_sg = [&](int xb8, uint32_t (&PP)[SG][NRR], uint32_t (&SS)[SG]) {
 #pragma unroll
-                for (int r = 0; r < NRR; ++r) P[r] = 0u;
-                S = 0u;
-            }
-            c = clv_at(x);
-            e = lane == ACT - 1 ? crv(x - p.min_disp - d0 - (DPL - 1)) : 0u;
-        };
-        uint32_t curP[NRR], curS, clv, dummy;
-        load_step(W - 1, curP, curS, clv, dummy);
-#pragma unroll
-        for (int k = 0; k < PF; ++k) load_step(W - 2 - k, pP[k], pS[k], pcl[k], pin[k]);
-        for (int xb = W - 1; xb >= 0; xb -= PF) {
-#pragma unroll
-            for (int k = 0; k < PF; ++k) {
-                const int x = xb - k;
-                if (x >= 0) {
-                    if (lane < 3 && x - PL2 >= 0) {    // pull step x-PL2 into L2
-                        const char* q = lane < 2 ? reinterpret_cast<const char*>(pab + (long long)(x - PL2) * D) + lane * 128
-                                                 : reinterpret_cast<const char*>(stash + (long long)(x - PL2) * D);
-                        prefetch_l2(q);
-                    }
-                    const bool vx = vrow && x >= p.R && x < W - p.R;
-                    uint32_t Ln[NRR];
-                    M = row_step<D>(p, lane, clv, vx, x - p.min_disp - p.R, wnd, L, M, Ln);
-#pragma unroll
-                    for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                    // S = P_AB + L_lr + L_rl
-                    uint32_t Sv[NRR];
-                    if (DPL == 4) {
-                        Sv[0] = curP[0] + __byte_perm(curS, 0u, 0x4140) + Ln[0];
-                        Sv[NRR - 1] = curP[NRR - 1] + __byte_perm(curS, 0u, 0x4342) + Ln[NRR - 1];
+            for (int k = 0; k < SG; ++k) {
+                const int x = xb8 + k;
+                if (x >= 0 && x < W && active) {
+                    const long long off = (long long)x * D;
+                    if constexpr (DPL == 4) {
+                        const uint2 u = __ldg(reinterpret_cast<const uint2*>(pab + off));
+                        PP[k][0] = u.x; PP[k][NRR - 1] = u.y;
+                        SS[k] = __ldg(reinterpret_cast<const uint32_t*>(stash + off));
                     } else {
-                        Sv[0] = curP[0] + __byte_perm(curS, 0u, 0x4140) + Ln[0];
+                        PP[k][0] = __ldg(reinterpret_cast<const uint32_t*>(pab + off));
+                        SS[k] = __ldg(reinterpret_cast<const uint16_t*>(stash + off));
                     }
-                    if (active) {
-                        uint16_t* r = rowp(x) + d0;
-                        if (DPL == 4) {
-                            const uint2 v = make_uint2(__byte_perm(Sv[0], Sv[NRR - 1], 0x5410),
-                                                       __byte_perm(Sv[0], Sv[NRR - 1], 0x7632));
-                            *reinterpret_cast<uint2*>(r) = v;
-                            if (a.agg && frame == 0)
-                                *reinterpret_cast<uint2*>(a.agg + rowcell + (long long)x * D + d0) = v;
-                        } else {
-                            *reinterpret_cast<uint32_t*>(r) = Sv[0];
-                            if (a.agg && frame == 0)
-                                *reinterpret_cast<uint32_t*>(a.agg + rowcell + (long long)x * D + d0) = Sv[0];
-                        }
-                    }
-                    // advance the prefetch ring: step x-1 becomes current, load x-1-PF
+                } else {
 #pragma unroll
-                    for (int r = 0; r < NRR; ++r) curP[r] = pP[k][r];
-                    curS = pS[k];
-                    const uint32_t clv_next = pcl[k];
-                    const uint32_t edge = pin[k];
-                    load_step(x - 1 - PF, pP[k], pS[k], pcl[k], pin[k]);
-                    __syncwarp();
-                    // ---- left WTA for pixels [x, x+32): their S rows are all in the window
-                    if ((x & 31) == 0) {
-                        const int xp = x + lane;
-                        if (xp < W) {
-                            int ds; bool uf; float disp;
-                            wta_left_lane<D>(p, rowp(xp), ds, uf, disp);
-                            const long long o = frame * a.px_stride + (long long)y * W + xp;
-                            uint8_t m = 0;
-                            if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
-                            if (uf) m |= MASK_UNIQUE;
-                            a.fs.dstar_l[o] = (int16_t)ds;
-                            a.fs.mask_l[o] = m;
-                            a.fs.dl[o] = disp;
-                        }
-                        __syncwarp();
-                    }
-                    // ---- right WTA for right pixels [x - min, x - min + 32) once complete
-                    if (x - p.min_disp >= 0 && ((x - p.min_disp) & 31) == 0) {
-                        const int xr = x - p.min_disp + lane;
-                        const int nd = min(D, W - p.min_disp - xr);
-                        if (xr < W) {
-                            int ds = -1; bool uf = false; float disp = 0.0f;
-                            if (nd > 0) wta_right_lane<D>(p, sbuf, (xr + p.min_disp) % NB, nd, ds, uf, disp);
-                            const long long o = frame * a.px_stride + (long long)y * W + xr;
-                            uint8_t m = 0;
-                            if (!(vrow && xr >= p.R && xr < W - p.R) || nd <= 0) m |= MASK_BORDER;
-                            if (uf) m |= MASK_UNIQUE;
-                            a.fs.dstar_r[o] = (int16_t)ds;
-                            a.fs.mask_r[o] = m;
-                            a.fs.dr[o] = disp;
-                        }
-                        __syncwarp();
-                    }
-                    // slide the census window to x-1
-                    const uint32_t in = __shfl_down_sync(FULL, wnd[0], 1);
-#pragma unroll
-                    for (int j = 0; j < DPL - 1; ++j) wnd[j] = wnd[j + 1];
-                    wnd[DPL - 1] = lane == ACT - 1 ? edge : in;
-                    clv = clv_next;
+                    for (int r = 0; r < NRR; ++r) PP[k][r] = 0u;
+                    SS[k] = 0u;
                 }
             }
+        };
+        auto l2_sg = [&](int xb8) {                   // pull a sub-group's P_AB + stash lines into L2
+            if (xb8 >= 0 && xb8 < W) {
+                constexpr int PL = SG * D * 2 / 128, SLn = SG * D / 128;     // 128-byte lines
+                if (lane < PL) prefetch_l2(reinterpret_cast<const char*>(pab - d0 + (long long)xb8 * D) + lane * 128);
+                else if (lane < PL + SLn)
+                    prefetch_l2(reinterpret_cast<const char*>(stash - d0 + (long long)xb8 * D) + (lane - PL) * 128);
+            }
+        };
+        const int gtop = ngrp - 1;
+        const int ph = (-p.min_disp) & 7;
+        uint32_t clb = blk(cl, gtop << 5);                            // cl[32g + j]
+        uint32_t crb = blk(cr, (gtop << 5) - p.min_disp - D);         // edge entering after step 32g + j
+        load_sg((gtop << 5) + 32 - SG, P, Sx);
+        int rowx = (((gtop << 5) + 31) % NB);                         // window row of x = 32g + 31
+        for (int g = gtop; g >= 0; --g) {
+            const int xb = g << 5;
+            const uint32_t clb_n = blk(cl, xb - 32);
+            const uint32_t crb_n = blk(cr, xb - 32 - p.min_disp - D);
+            const bool fast = group_fast(xb);
+            for (int s = 32 - SG; s >= 0; s -= SG) {
+                const int xs = xb + s;                                // lowest x of this sub-group
+                load_sg(xs - SG, Pn, Sn);
+                l2_sg(xs - 3 * SG);
+#pragma unroll
+                for (int k = SG - 1; k >= 0; --k) {
+                    const int j = s + k, x = xb + j;
+                    if (x < W) {
+                        const uint32_t clv = __shfl_sync(FULL, clb, j);
+                        const bool vx = fast || (vrow && x >= p.R && x < W - p.R);
+                        uint32_t Ln[NRR];
+                        M = row_step<D>(p, lane, clv, vx, fast ? D : x + lim0, wnd, L, M, Ln);
+#pragma unroll
+                        for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                        uint32_t Sv[NRR];
+                        if constexpr (DPL == 4) {
+                            Sv[0] = P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
+                            Sv[NRR - 1] = P[k][NRR - 1] + __byte_perm(Sx[k], 0u, 0x4342) + Ln[NRR - 1];
+                        } else {
+                            Sv[0] = P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
+                        }
+                        if (active) {
+                            uint16_t* r = sbuf + rowx * BS + d0;
+                            if constexpr (DPL == 4) {
+                                const uint2 v = make_uint2(__byte_perm(Sv[0], Sv[NRR - 1], 0x5410),
+                                                           __byte_perm(Sv[0], Sv[NRR - 1], 0x7632));
+                                *reinterpret_cast<uint2*>(r) = v;
+                                if (a.agg && frame == 0)
+                                    *reinterpret_cast<uint2*>(a.agg + rowcell + (long long)x * D + d0) = v;
+                            } else {
+                                *reinterpret_cast<uint32_t*>(r) = Sv[0];
+                                if (a.agg && frame == 0)
+                                    *reinterpret_cast<uint32_t*>(a.agg + rowcell + (long long)x * D + d0) = Sv[0];
+                            }
+                        }
+                        const uint32_t in = __shfl_down_sync(FULL, wnd[0], 1);
+                        const uint32_t e = __shfl_sync(FULL, crb, j);
+#pragma unroll
+                        for (int q = 0; q < DPL - 1; ++q) wnd[q] = wnd[q + 1];
+                        wnd[DPL - 1] = lane == ACT - 1 ? e : in;
+                    }
+                    rowx = rowx == 0 ? NB - 1 : rowx - 1;
+                }
+#pragma unroll
+                for (int k = 0; k < SG; ++k) {
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) P[k][r] = Pn[k][r];
+                    Sx[k] = Sn[k];
+                }
+                __syncwarp();
+                // right pixel xr is complete once x = xr + min has been processed.
+                // Batches start at XR = ph + 32m, ph = (-min) & 7, so each completes
+                // exactly at a sub-group end; [0, ph) is finished once x <= min.
+                {
+                    const int XR = xs - p.min_disp;
+                    if (XR >= 0 && ((XR - ph) & 31) == 0) right_batch(XR);
+                    if (ph > 0 && xs <= p.min_disp && p.min_disp < xs + SG) right_batch(ph - 32);
+                }
+            }
+            // left pixels [xb, xb+32): all their S rows are in the window
+            {
+                const int xp = xb + lane;
+                if (xp < W) {
+                    int ds; bool uf; float disp;
+                    wta_left_lane<D>(p, sbuf + (xp % NB) * BS, ds, uf, disp);
+                    const long long o = frame * a.px_stride + (long long)y * W + xp;
+                    uint8_t m = 0;
+                    if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
+                    if (uf) m |= MASK_UNIQUE;
+                    a.fs.dstar_l[o] = (int16_t)ds;
+                    a.fs.mask_l[o] = m;
+                    a.fs.dl[o] = disp;
+                }
+                __syncwarp();
+            }
+            clb = clb_n;
+            crb = crb_n;
         }
     }
 }
@@ -774,7 +849,7 @@ static size_t vsmem_bytes(int w, int D, int T, int DC, int np)
     const int nw = w * T / 32;
     (void)D;
     const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
-    size_t words = 3 * ((size_t)w + (size_t)T * cstr);
+    size_t words = 4 * ((size_t)w + (size_t)T * cstr);
     if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
     return words * 4;
 }
@@ -858,8 +933,12 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         for (VKernel k : {kd, ku})
             cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
     }
-    pl.nbuf = p.D + 32;
-    pl.bstride = p.D + 4;
+    switch (p.D) {                      // the row kernel's window geometry (RowGeom<D>)
+        case 16: pl.nbuf = v2::RowGeom<16>::NB; pl.bstride = v2::RowGeom<16>::BS; break;
+        case 32: pl.nbuf = v2::RowGeom<32>::NB; pl.bstride = v2::RowGeom<32>::BS; break;
+        case 64: pl.nbuf = v2::RowGeom<64>::NB; pl.bstride = v2::RowGeom<64>::BS; break;
+        default: pl.nbuf = v2::RowGeom<128>::NB; pl.bstride = v2::RowGeom<128>::BS; break;
+    }
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
     RKernel rk = pick_rkernel(p.D);
     cudaFuncSetAttribute((const void*)rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.rsmem);
