@@ -38,10 +38,10 @@ MAX_BATCH = 32                 # frames in flight per asd_depth_batch chunk
 
 
 KERNEL_NAMES = {"census": "census_kernel (K1)", "dir": "sgm_dir_kernel (D1, one path direction)",
-                "wta": "wta_kernel (D1 K4)", "lr": "lr_depth_kernel (K5)",
+                "wta": "WTA kernel (K4: D1 wta_kernel / D3 wta2_kernel)", "lr": "lr_depth_kernel (K5)",
                 "down": "vsweep_kernel<down> (D3, 3 downward paths)",
                 "up": "vsweep_kernel<up> (D3, 3 upward paths)",
-                "row": "row_kernel (D3, horizontal paths + WTA)"}
+                "row": "hrow_kernel (D3, horizontal paths)"}
 
 
 def peaks():

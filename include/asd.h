@@ -191,11 +191,11 @@ int asd_engine(const asd_ctx* ctx);
  * counted in `dropped` and not timed. */
 #define ASD_STAGE_CENSUS 0   /* K1 census */
 #define ASD_STAGE_DIR    1   /* D1: one SGM path direction per launch */
-#define ASD_STAGE_WTA    2   /* D1: K4 WTA / uniqueness / sub-pixel, both views */
+#define ASD_STAGE_WTA    2   /* K4 WTA / uniqueness / sub-pixel, both views (D1 and D3) */
 #define ASD_STAGE_LR     3   /* K5 LR check + depth (+ stats) */
 #define ASD_STAGE_DOWN   4   /* D3: downward sweep (3 paths, or 1 at 4-path) */
 #define ASD_STAGE_UP     5   /* D3: upward sweep */
-#define ASD_STAGE_ROW    6   /* D3: horizontal paths + WTA, both views */
+#define ASD_STAGE_ROW    6   /* D3: horizontal paths, S written over the partial */
 #define ASD_STAGE_COUNT  7
 typedef struct asd_stage_times {
     double ms[ASD_STAGE_COUNT];

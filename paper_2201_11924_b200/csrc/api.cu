@@ -225,12 +225,14 @@ static double alg_bytes_dir(const DevParams& p, bool first) { return (first ? 2.
 static double alg_bytes_wta(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * (4 + 2 + 1); }
 static double alg_bytes_lr(const DevParams& p) { return p.npx * (2 * (4 + 1) + 2 + 2 * 4.0); }
 // Design D3: down sweep writes the u8 partial (1 B/cell); up sweep reads it and
-// writes the u16 partial (3 B/cell); the row kernel reads the u16 partial and
-// writes + reads the u8 left->right stash (4 B/cell) and writes the per-pixel
+// writes the u16 partial (3 B/cell); the row kernel reads the u16 partial,
+// writes + reads the u8 left->right stash and writes S over the partial
+// (6 B/cell); the WTA kernel reads S once (2 B/cell) and writes the per-pixel
 // maps of both views (2 x (4 + 2 + 1) B/px).  Census reads are L2-resident.
 static double alg_bytes_down(const DevParams& p) { return 1.0 * p.ncell; }
 static double alg_bytes_up(const DevParams& p) { return 3.0 * p.ncell; }
-static double alg_bytes_row(const DevParams& p) { return 4.0 * p.ncell + 2.0 * p.npx * 7; }
+static double alg_bytes_row(const DevParams& p) { return 6.0 * p.ncell; }
+static double alg_bytes_wta3(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * 7; }
 
 // Enqueue the whole path for n <= max_batch frames resident on the device.
 int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
@@ -265,7 +267,17 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         {
             ProfScope ps(c, s, ASD_STAGE_ROW, n * alg_bytes_row(p));
             launch_v2_stage(2, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
-                            p.ncell, fs, npx, agg_debug, s);
+                            p.ncell, fs, npx, nullptr, s);
+        }
+        if (agg_debug)                       // S of frame 0 (natural order) before the WTA
+            cudaMemcpyAsync(agg_debug, c->pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, s);
+        {
+            ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta3(p));
+            if (launch_v2_stage(3, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
+                                p.ncell, fs, npx, nullptr, s) != 0) {
+                set_err(c, "WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return ASD_E_CUDA;
+            }
         }
     }
     for (int r = 0; c->engine == ASD_ENGINE_D1 && r < p.paths; ++r) {
@@ -431,7 +443,7 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 {
     if (!ctx || n <= 0) return 0;
     const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
-    return chunks * (ctx->engine == ASD_ENGINE_D3 ? 5 : 3 + ctx->dp.paths);
+    return chunks * (ctx->engine == ASD_ENGINE_D3 ? 6 : 3 + ctx->dp.paths);
 }
 
 int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }

@@ -31,6 +31,7 @@
 // (or, at CTA edges, the neighbouring CTA through DSMEM) wrote.  One cluster
 // barrier per row, split arrive/wait around the next row's cost computation.
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -397,13 +398,12 @@ struct RArgs {
     const uint32_t* cl;
     const uint32_t* cr;
     long long sig_stride;
-    const uint16_t* pab;      // [frames][H][W][D] row-kernel layout
+    uint16_t* pab;            // [frames][H][W][D]: P_AB in (row-kernel layout); S out (natural order)
     uint8_t* stash;           // [frames][H][W][D] left->right path, u8
     long long cell_stride;
-    FrameScratch fs;          // outputs for K5
+    FrameScratch fs;          // WTA outputs for K5
     long long px_stride;
-    uint16_t* agg;            // debug: S [H][W][D] natural order (frame 0), may be NULL
-    int nbuf;                 // rows of the S window (>= D + 32)
+    int nbuf;                 // rows of the WTA kernel's S window
     int bstride;              // u16 per window row (D + 4)
 };
 
@@ -443,14 +443,14 @@ template <int D>
 __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, int& dstar, bool& uf, float& disp)
 {
     constexpr int KS = RowGeom<D>::KS;
-    uint32_t kmin = 0xFFFFFFFFu;
-#pragma unroll
+    uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
+#pragma unroll 4
     for (int q = 0; q < D; q += 4) {
         const uint2 v = *reinterpret_cast<const uint2*>(r + q);
-        const uint32_t k0 = v.x * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16));
-        const uint32_t k1 = v.y * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16));
-        kmin = vmin2(kmin, vmin2(k0, k1));
+        ka = vmin2(ka, v.x * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
+        kb2 = vmin2(kb2, v.y * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
     }
+    const uint32_t kmin = vmin2(ka, kb2);
     const uint32_t kb = min(kmin & 0xFFFFu, kmin >> 16);
     dstar = (int)(kb & ((1u << KS) - 1u));
     const uint32_t s0 = kb >> KS;
@@ -459,12 +459,14 @@ __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, i
     if (dstar >= 1) r[dstar - 1] = (uint16_t)NONE16;
     r[dstar] = (uint16_t)NONE16;
     if (dstar + 1 < D) r[dstar + 1] = (uint16_t)NONE16;
-    uint32_t vm = 0xFFFFFFFFu;
-#pragma unroll
+    uint32_t vm = 0xFFFFFFFFu, vm2 = 0xFFFFFFFFu;
+#pragma unroll 4
     for (int q = 0; q < D; q += 4) {
         const uint2 v = *reinterpret_cast<const uint2*>(r + q);
-        vm = vmin2(vm, vmin2(v.x, v.y));
+        vm = vmin2(vm, v.x);
+        vm2 = vmin2(vm2, v.y);
     }
+    vm = vmin2(vm, vm2);
     if (dstar >= 1) r[dstar - 1] = (uint16_t)cm;
     r[dstar] = (uint16_t)s0;
     if (dstar + 1 < D) r[dstar + 1] = (uint16_t)cp;
@@ -474,20 +476,30 @@ __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, i
 // Right view, one right pixel per lane: S_R(d) = S(xr + delta(d), d) lies on a
 // diagonal of the window (row (r0 + d) mod NB, column d); nd >= 1 defined d.
 template <int D>
-__device__ __forceinline__ void wta_right_lane(const DevParams& p, uint16_t* sb, int r0, int nd,
+__device__ __forceinline__ void wta_right_lane(const DevParams& p, uint16_t* sb, int NB, int r0, int nd,
                                                int& dstar, bool& uf, float& disp)
 {
-    constexpr int NB = RowGeom<D>::NB, BS = RowGeom<D>::BS, KS = RowGeom<D>::KS;
+    constexpr int BS = RowGeom<D>::BS, KS = RowGeom<D>::KS;
     constexpr int STEP = BS + 1;
     const int dwrap = NB - r0;                       // first d whose row wraps to 0
     const uint16_t* b0 = sb + r0 * BS;
     const uint16_t* b1 = b0 - NB * BS;
     const int n0 = min(nd, dwrap);
-    uint32_t kmin = 0xFFFFFFFFu;
-#pragma unroll 8
-    for (int d = 0; d < n0; ++d) kmin = min(kmin, ((uint32_t)b0[d * STEP] << KS) | (uint32_t)d);
-#pragma unroll 8
-    for (int d = n0; d < nd; ++d) kmin = min(kmin, ((uint32_t)b1[d * STEP] << KS) | (uint32_t)d);
+    uint32_t kmin = 0xFFFFFFFFu, kmin2 = 0xFFFFFFFFu;
+    int d = 0;
+#pragma unroll 2
+    for (; d + 1 < n0; d += 2) {
+        kmin = min(kmin, ((uint32_t)b0[d * STEP] << KS) | (uint32_t)d);
+        kmin2 = min(kmin2, ((uint32_t)b0[(d + 1) * STEP] << KS) | (uint32_t)(d + 1));
+    }
+    if (d < n0) { kmin = min(kmin, ((uint32_t)b0[d * STEP] << KS) | (uint32_t)d); ++d; }
+#pragma unroll 2
+    for (; d + 1 < nd; d += 2) {
+        kmin = min(kmin, ((uint32_t)b1[d * STEP] << KS) | (uint32_t)d);
+        kmin2 = min(kmin2, ((uint32_t)b1[(d + 1) * STEP] << KS) | (uint32_t)(d + 1));
+    }
+    if (d < nd) kmin = min(kmin, ((uint32_t)b1[d * STEP] << KS) | (uint32_t)d);
+    kmin = min(kmin, kmin2);
     dstar = (int)(kmin & ((1u << KS) - 1u));
     const uint32_t s0 = kmin >> KS;
     auto at = [&](int d) -> uint16_t* { return const_cast<uint16_t*>((d < dwrap ? b0 : b1) + d * STEP); };
@@ -496,11 +508,15 @@ __device__ __forceinline__ void wta_right_lane(const DevParams& p, uint16_t* sb,
     if (dstar >= 1) *at(dstar - 1) = (uint16_t)NONE16;
     *at(dstar) = (uint16_t)NONE16;
     if (dstar + 1 < nd) *at(dstar + 1) = (uint16_t)NONE16;
-    uint32_t vm = NONE16;
-#pragma unroll 8
-    for (int d = 0; d < n0; ++d) vm = min(vm, (uint32_t)b0[d * STEP]);
-#pragma unroll 8
-    for (int d = n0; d < nd; ++d) vm = min(vm, (uint32_t)b1[d * STEP]);
+    uint32_t vm = NONE16, vmb = NONE16;
+    d = 0;
+#pragma unroll 2
+    for (; d + 1 < n0; d += 2) { vm = min(vm, (uint32_t)b0[d * STEP]); vmb = min(vmb, (uint32_t)b0[(d + 1) * STEP]); }
+    if (d < n0) { vm = min(vm, (uint32_t)b0[d * STEP]); ++d; }
+#pragma unroll 2
+    for (; d + 1 < nd; d += 2) { vm = min(vm, (uint32_t)b1[d * STEP]); vmb = min(vmb, (uint32_t)b1[(d + 1) * STEP]); }
+    if (d < nd) vm = min(vm, (uint32_t)b1[d * STEP]);
+    vm = min(vm, vmb);
     if (dstar >= 1) *at(dstar - 1) = (uint16_t)cm;
     *at(dstar) = (uint16_t)s0;
     if (dstar + 1 < nd) *at(dstar + 1) = (uint16_t)cp;
@@ -514,7 +530,7 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr)
 
 // One recursion step of a horizontal path for one warp (lane = DPL disparities).
 // Lp: predecessor state (zero at the line start), M: its min (0 at the start).
-template <int D>
+template <int D, bool FAST = false>
 __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint32_t clv, bool vx, int lim,
                                              const uint32_t (&wnd)[RowGeom<D>::DPL],
                                              const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t M,
@@ -523,7 +539,7 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
     constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
     const int d0 = lane * DPL;
     uint32_t c[DPL];
-    if (vx && lim >= D - 1) {                         // warp-uniform fast path: all d valid
+    if (FAST || (vx && lim >= D - 1)) {               // warp-uniform fast path: all d valid
 #pragma unroll
         for (int j = 0; j < DPL; ++j) c[j] = __popc(clv ^ wnd[j]);
     } else {
@@ -541,7 +557,7 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
         uint32_t prevB = __shfl_up_sync(FULL, QB, 1);
         uint32_t nextA = __shfl_down_sync(FULL, QA, 1);
         if (lane == 0) prevB = INF2;
-        if (lane >= ACT - 1) nextA = INF2;
+        if (lane == ACT - 1) nextA = INF2;
         const uint32_t dm1A = __byte_perm(prevB, QB, 0x5432);
         const uint32_t dp1B = __byte_perm(QA, nextA, 0x5432);
         uint32_t tA = vmin2(vmin2(dm1A, QB), Lp[0]);
@@ -559,7 +575,7 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
         uint32_t prev = __shfl_up_sync(FULL, Q, 1);
         uint32_t next = __shfl_down_sync(FULL, Q, 1);
         if (lane == 0) prev = INF2;
-        if (lane >= ACT - 1) next = INF2;
+        if (lane == ACT - 1) next = INF2;
         const uint32_t dm1 = __byte_perm(prev, Q, 0x5432);
         const uint32_t dp1 = __byte_perm(Q, next, 0x5432);
         uint32_t t = vmin2(vmin2(dm1, dp1), Lp[0]);
@@ -567,43 +583,48 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
         Ln[0] = t + C0 + negMM;
         lmin = min(Ln[0] & 0xFFFFu, Ln[0] >> 16);
     }
-    if (lane >= ACT) lmin = 0xFFFFFFFFu;
+    if (ACT < 32 && lane >= ACT) lmin = 0xFFFFFFFFu;
     return __reduce_min_sync(FULL, lmin);
 }
 
+// ---------------------------------------------------------------- K_row
+// Horizontal paths, one warp per row, no shared memory (occupancy bound only by
+// registers).  Left->right: L stashed as u8.  Right->left: S = P_AB + L_lr +
+// L_rl written over P_AB in place, natural d order, for the WTA kernel.
+constexpr int HROW_WARPS = 4;
+
 template <int D>
-__global__ void __launch_bounds__(32)
-row_kernel(RArgs a)
+__global__ void __launch_bounds__(32 * HROW_WARPS)
+hrow_kernel(RArgs a)
 {
     using G = RowGeom<D>;
-    constexpr int DPL = G::DPL, NRR = G::NRR, ACT = G::ACT, NB = G::NB, BS = G::BS;
-    constexpr int SG = 8;                             // steps per unrolled sub-group
-    extern __shared__ __align__(16) uint16_t sbuf[];  // [NB][BS]
+    constexpr int DPL = G::DPL, NRR = G::NRR, ACT = G::ACT;
+    constexpr int SG = 8;
     const DevParams& p = a.p;
-    const int W = p.W;
-    const int y = blockIdx.x, frame = blockIdx.y;
-    const int lane = threadIdx.x;
-    const bool active = lane < ACT;
+    const int W = p.W, H = p.H;
+    const int frame = blockIdx.y;
+    const int y = blockIdx.x * HROW_WARPS + (threadIdx.x >> 5);
+    if (y >= H) return;
+    const int lane = threadIdx.x & 31;
+    const bool active = ACT == 32 || lane < ACT;
     const int d0 = lane * DPL;
+    const int lim0 = -p.min_disp - p.R;
+    const int ngrp = (W + 31) >> 5;
     const uint32_t* cl = a.cl + frame * a.sig_stride + (long long)y * W;
     const uint32_t* cr = a.cr + frame * a.sig_stride + (long long)y * W;
-    const long long rowcell = (long long)y * W * D;
-    uint8_t* stash = a.stash + frame * a.cell_stride + rowcell + d0;     // lane's slot of pixel 0
-    const uint16_t* pab = a.pab + frame * a.cell_stride + rowcell + d0;
-    const bool vrow = y >= p.Q && y < p.H - p.Q;
-    const int lim0 = -p.min_disp - p.R;              // d valid iff d <= x + lim0
-    // a 32-column group is "fast" when every x in it has a valid census window
-    // and every disparity a valid right pixel
-    auto group_fast = [&](int xb) {
-        return vrow && xb + 31 < W && xb >= p.R && xb + 31 < W - p.R && xb + lim0 >= D - 1;
-    };
+    const long long rowcell = frame * a.cell_stride + (long long)y * W * D + d0;
+    uint8_t* stash = a.stash + rowcell;
+    uint16_t* pab = a.pab + rowcell;
+    const bool vrow = y >= p.Q && y < H - p.Q;
     auto blk = [&](const uint32_t* row, int i0) -> uint32_t {
         const int i = i0 + lane;
         return (i >= 0 && i < W) ? __ldg(row + i) : 0u;
     };
-    const int ngrp = (W + 31) >> 5;
+    auto fast_group = [&](int xb) {
+        return vrow && xb + 31 < W && xb >= p.R && xb + 31 < W - p.R && xb + lim0 >= D - 1;
+    };
 
-    // ------------------------------------------------ left -> right, stash L
+    // ------------------------------------------------ left -> right
     {
         uint32_t L[NRR], wnd[DPL];
 #pragma unroll
@@ -614,68 +635,44 @@ row_kernel(RArgs a)
             const int xr = 0 - p.min_disp - d0 - j;
             wnd[j] = (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u;
         }
-        uint32_t clb = blk(cl, 0);                   // cl[32g + j]
-        uint32_t crb = blk(cr, 1 - p.min_disp);      // cr[32g + j + 1 - min]: enters the window after step 32g + j
+        uint32_t clb = blk(cl, 0), crb = blk(cr, 1 - p.min_disp);
         for (int g = 0; g < ngrp; ++g) {
             const int xb = g << 5;
-            const uint32_t clb_n = blk(cl, xb + 32);
-            const uint32_t crb_n = blk(cr, xb + 33 - p.min_disp);
-            const bool fast = group_fast(xb);
-            uint8_t* sp = stash + (long long)xb * D;
-            for (int s = 0; s < 32; s += SG) {
+            const uint32_t clb_n = blk(cl, xb + 32), crb_n = blk(cr, xb + 33 - p.min_disp);
+            auto body = [&](auto ftag) {
+                constexpr bool F = decltype(ftag)::value;
+                for (int s = 0; s < 32; s += SG) {
 #pragma unroll
-                for (int k = 0; k < SG; ++k) {
-                    const int j = s + k, x = xb + j;
-                    if (x < W) {
+                    for (int k = 0; k < SG; ++k) {
+                        const int j = s + k, x = xb + j;
                         const uint32_t clv = __shfl_sync(FULL, clb, j);
-                        const bool vx = fast || (vrow && x >= p.R && x < W - p.R);
-                        uint32_t Ln[NRR];
-                        M = row_step<D>(p, lane, clv, vx, fast ? D : x + lim0, wnd, L, M, Ln);
-#pragma unroll
-                        for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                        if (active) {
-                            if constexpr (DPL == 4)
-                                *reinterpret_cast<uint32_t*>(sp + j * D) = __byte_perm(L[0], L[NRR - 1], 0x6420);
-                            else
-                                *reinterpret_cast<uint16_t*>(sp + j * D) = (uint16_t)__byte_perm(L[0], 0u, 0x4420);
-                        }
-                        const uint32_t in = __shfl_up_sync(FULL, wnd[DPL - 1], 1);
                         const uint32_t e = __shfl_sync(FULL, crb, j);
+                        if (F || x < W) {
+                            const bool vx = F || (vrow && x >= p.R && x < W - p.R);
+                            uint32_t Ln[NRR];
+                            M = row_step<D, F>(p, lane, clv, vx, x + lim0, wnd, L, M, Ln);
 #pragma unroll
-                        for (int q = DPL - 1; q > 0; --q) wnd[q] = wnd[q - 1];
-                        wnd[0] = lane == 0 ? e : in;
+                            for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                            if (active) {
+                                if constexpr (DPL == 4)
+                                    *reinterpret_cast<uint32_t*>(stash + (long long)x * D) = __byte_perm(Ln[0], Ln[NRR - 1], 0x6420);
+                                else
+                                    *reinterpret_cast<uint16_t*>(stash + (long long)x * D) = (uint16_t)__byte_perm(Ln[0], 0u, 0x4420);
+                            }
+                            const uint32_t in = __shfl_up_sync(FULL, wnd[DPL - 1], 1);
+#pragma unroll
+                            for (int q = DPL - 1; q > 0; --q) wnd[q] = wnd[q - 1];
+                            wnd[0] = lane == 0 ? e : in;
+                        }
                     }
                 }
-            }
-            clb = clb_n;
-            crb = crb_n;
+            };
+            if (fast_group(xb)) body(std::true_type{}); else body(std::false_type{});
+            clb = clb_n; crb = crb_n;
         }
     }
     __syncwarp();
-    // ------------------------------------------------ right -> left + WTA
-    // right pixels with no defined disparity at all: xr + min_disp >= W
-    for (int xr = max(0, W - p.min_disp) + lane; xr < W; xr += 32) {
-        const long long o = frame * a.px_stride + (long long)y * W + xr;
-        a.fs.dstar_r[o] = -1;
-        a.fs.mask_r[o] = MASK_BORDER;
-        a.fs.dr[o] = 0.0f;
-    }
-    auto right_batch = [&](int XR) {                  // right pixels [XR, XR+32), all complete
-        const int xr = XR + lane;
-        const int nd = min(D, W - p.min_disp - xr);
-        if (xr >= 0 && xr < W) {
-            int ds = -1; bool uf = false; float disp = 0.0f;
-            if (nd > 0) wta_right_lane<D>(p, sbuf, (xr + p.min_disp) % NB, nd, ds, uf, disp);
-            const long long o = frame * a.px_stride + (long long)y * W + xr;
-            uint8_t m = 0;
-            if (!(vrow && xr >= p.R && xr < W - p.R) || nd <= 0) m |= MASK_BORDER;
-            if (uf) m |= MASK_UNIQUE;
-            a.fs.dstar_r[o] = (int16_t)ds;
-            a.fs.mask_r[o] = m;
-            a.fs.dr[o] = disp;
-        }
-        __syncwarp();
-    };
+    // ------------------------------------------------ right -> left, S out
     {
         uint32_t L[NRR], wnd[DPL];
 #pragma unroll
@@ -686,7 +683,6 @@ row_kernel(RArgs a)
             const int xr = W - 1 - p.min_disp - d0 - j;
             wnd[j] = (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u;
         }
-        // per sub-group register prefetch of P_AB and the stash (8 steps ahead)
         uint32_t P[SG][NRR], Sx[SG], Pn[SG][NRR], Sn[SG];
         auto load_sg = [&](int xb8, uint32_t (&PP)[SG][NRR], uint32_t (&SS)[SG]) {
 #pragma unroll
@@ -695,12 +691,12 @@ row_kernel(RArgs a)
                 if (x >= 0 && x < W && active) {
                     const long long off = (long long)x * D;
                     if constexpr (DPL == 4) {
-                        const uint2 u = __ldg(reinterpret_cast<const uint2*>(pab + off));
+                        const uint2 u = *reinterpret_cast<const uint2*>(pab + off);
                         PP[k][0] = u.x; PP[k][NRR - 1] = u.y;
-                        SS[k] = __ldg(reinterpret_cast<const uint32_t*>(stash + off));
+                        SS[k] = *reinterpret_cast<const uint32_t*>(stash + off);
                     } else {
-                        PP[k][0] = __ldg(reinterpret_cast<const uint32_t*>(pab + off));
-                        SS[k] = __ldg(reinterpret_cast<const uint16_t*>(stash + off));
+                        PP[k][0] = *reinterpret_cast<const uint32_t*>(pab + off);
+                        SS[k] = *reinterpret_cast<const uint16_t*>(stash + off);
                     }
                 } else {
 #pragma unroll
@@ -709,102 +705,139 @@ row_kernel(RArgs a)
                 }
             }
         };
-        auto l2_sg = [&](int xb8) {                   // pull a sub-group's P_AB + stash lines into L2
-            if (xb8 >= 0 && xb8 < W) {
-                constexpr int PL = SG * D * 2 / 128, SLn = SG * D / 128;     // 128-byte lines
-                if (lane < PL) prefetch_l2(reinterpret_cast<const char*>(pab - d0 + (long long)xb8 * D) + lane * 128);
-                else if (lane < PL + SLn)
-                    prefetch_l2(reinterpret_cast<const char*>(stash - d0 + (long long)xb8 * D) + (lane - PL) * 128);
-            }
-        };
         const int gtop = ngrp - 1;
-        const int ph = (-p.min_disp) & 7;
-        uint32_t clb = blk(cl, gtop << 5);                            // cl[32g + j]
-        uint32_t crb = blk(cr, (gtop << 5) - p.min_disp - D);         // edge entering after step 32g + j
+        uint32_t clb = blk(cl, gtop << 5), crb = blk(cr, (gtop << 5) - p.min_disp - D);
         load_sg((gtop << 5) + 32 - SG, P, Sx);
-        int rowx = (((gtop << 5) + 31) % NB);                         // window row of x = 32g + 31
         for (int g = gtop; g >= 0; --g) {
             const int xb = g << 5;
-            const uint32_t clb_n = blk(cl, xb - 32);
-            const uint32_t crb_n = blk(cr, xb - 32 - p.min_disp - D);
-            const bool fast = group_fast(xb);
+            const uint32_t clb_n = blk(cl, xb - 32), crb_n = blk(cr, xb - 32 - p.min_disp - D);
+            const bool fast = fast_group(xb);
             for (int s = 32 - SG; s >= 0; s -= SG) {
-                const int xs = xb + s;                                // lowest x of this sub-group
-                load_sg(xs - SG, Pn, Sn);
-                l2_sg(xs - 3 * SG);
+                load_sg(xb + s - SG, Pn, Sn);
+                auto body = [&](auto ftag) {
+                    constexpr bool F = decltype(ftag)::value;
 #pragma unroll
-                for (int k = SG - 1; k >= 0; --k) {
-                    const int j = s + k, x = xb + j;
-                    if (x < W) {
+                    for (int k = SG - 1; k >= 0; --k) {
+                        const int j = s + k, x = xb + j;
                         const uint32_t clv = __shfl_sync(FULL, clb, j);
-                        const bool vx = fast || (vrow && x >= p.R && x < W - p.R);
-                        uint32_t Ln[NRR];
-                        M = row_step<D>(p, lane, clv, vx, fast ? D : x + lim0, wnd, L, M, Ln);
-#pragma unroll
-                        for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                        uint32_t Sv[NRR];
-                        if constexpr (DPL == 4) {
-                            Sv[0] = P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
-                            Sv[NRR - 1] = P[k][NRR - 1] + __byte_perm(Sx[k], 0u, 0x4342) + Ln[NRR - 1];
-                        } else {
-                            Sv[0] = P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
-                        }
-                        if (active) {
-                            uint16_t* r = sbuf + rowx * BS + d0;
-                            if constexpr (DPL == 4) {
-                                const uint2 v = make_uint2(__byte_perm(Sv[0], Sv[NRR - 1], 0x5410),
-                                                           __byte_perm(Sv[0], Sv[NRR - 1], 0x7632));
-                                *reinterpret_cast<uint2*>(r) = v;
-                                if (a.agg && frame == 0)
-                                    *reinterpret_cast<uint2*>(a.agg + rowcell + (long long)x * D + d0) = v;
-                            } else {
-                                *reinterpret_cast<uint32_t*>(r) = Sv[0];
-                                if (a.agg && frame == 0)
-                                    *reinterpret_cast<uint32_t*>(a.agg + rowcell + (long long)x * D + d0) = Sv[0];
-                            }
-                        }
-                        const uint32_t in = __shfl_down_sync(FULL, wnd[0], 1);
                         const uint32_t e = __shfl_sync(FULL, crb, j);
+                        if (F || x < W) {
+                            const bool vx = F || (vrow && x >= p.R && x < W - p.R);
+                            uint32_t Ln[NRR];
+                            M = row_step<D, F>(p, lane, clv, vx, x + lim0, wnd, L, M, Ln);
 #pragma unroll
-                        for (int q = 0; q < DPL - 1; ++q) wnd[q] = wnd[q + 1];
-                        wnd[DPL - 1] = lane == ACT - 1 ? e : in;
+                            for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                            if (active) {
+                                if constexpr (DPL == 4) {
+                                    const uint32_t s0 = P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
+                                    const uint32_t s1 = P[k][NRR - 1] + __byte_perm(Sx[k], 0u, 0x4342) + Ln[NRR - 1];
+                                    *reinterpret_cast<uint2*>(pab + (long long)x * D) =
+                                        make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
+                                } else {
+                                    *reinterpret_cast<uint32_t*>(pab + (long long)x * D) =
+                                        P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
+                                }
+                            }
+                            const uint32_t in = __shfl_down_sync(FULL, wnd[0], 1);
+#pragma unroll
+                            for (int q = 0; q < DPL - 1; ++q) wnd[q] = wnd[q + 1];
+                            wnd[DPL - 1] = lane == ACT - 1 ? e : in;
+                        }
                     }
-                    rowx = rowx == 0 ? NB - 1 : rowx - 1;
-                }
+                };
+                if (fast) body(std::true_type{}); else body(std::false_type{});
 #pragma unroll
                 for (int k = 0; k < SG; ++k) {
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) P[k][r] = Pn[k][r];
                     Sx[k] = Sn[k];
                 }
-                __syncwarp();
-                // right pixel xr is complete once x = xr + min has been processed.
-                // Batches start at XR = ph + 32m, ph = (-min) & 7, so each completes
-                // exactly at a sub-group end; [0, ph) is finished once x <= min.
-                {
-                    const int XR = xs - p.min_disp;
-                    if (XR >= 0 && ((XR - ph) & 31) == 0) right_batch(XR);
-                    if (ph > 0 && xs <= p.min_disp && p.min_disp < xs + SG) right_batch(ph - 32);
-                }
             }
-            // left pixels [xb, xb+32): all their S rows are in the window
-            {
-                const int xp = xb + lane;
-                if (xp < W) {
-                    int ds; bool uf; float disp;
-                    wta_left_lane<D>(p, sbuf + (xp % NB) * BS, ds, uf, disp);
-                    const long long o = frame * a.px_stride + (long long)y * W + xp;
-                    uint8_t m = 0;
-                    if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
-                    if (uf) m |= MASK_UNIQUE;
-                    a.fs.dstar_l[o] = (int16_t)ds;
-                    a.fs.mask_l[o] = m;
-                    a.fs.dl[o] = disp;
-                }
-                __syncwarp();
+            clb = clb_n; crb = crb_n;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K_wta
+// WTA / uniqueness / sub-pixel for the left view and the re-indexed right view
+// (K4 semantics, post.cu) from S rows staged in a shared-memory ring.  One CTA
+// (4 warps) per image row walks stages of 128 pixels; stage t needs S rows
+// [128t, 128t + 127 + min + D - 1], loaded with 16-byte cp.async once each.
+constexpr int WTA_WARPS = 4;
+constexpr int WTA_TX = 32 * WTA_WARPS;
+
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(gsrc) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(32 * WTA_WARPS)
+wta2_kernel(RArgs a)
+{
+    using G = RowGeom<D>;
+    constexpr int BS = G::BS;
+    extern __shared__ __align__(16) uint16_t sbuf[];  // [NB][BS]
+    const DevParams& p = a.p;
+    const int W = p.W, NB = a.nbuf;
+    const int y = blockIdx.x, frame = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint16_t* S = a.pab + frame * a.cell_stride + (long long)y * W * D;
+    const bool vrow = y >= p.Q && y < p.H - p.Q;
+    // right pixels with no defined disparity at all: xr + min_disp >= W
+    for (int xr = max(0, W - p.min_disp) + threadIdx.x; xr < W; xr += blockDim.x) {
+        const long long o = frame * a.px_stride + (long long)y * W + xr;
+        a.fs.dstar_r[o] = -1;
+        a.fs.mask_r[o] = MASK_BORDER;
+        a.fs.dr[o] = 0.0f;
+    }
+    constexpr int CH = D * 2 / 8;                     // 8-byte chunks per S row (rows are 8-byte aligned)
+    int loaded = 0;                                   // rows [0, loaded) issued
+    const int nstage = (W + WTA_TX - 1) / WTA_TX;
+    for (int t = 0; t < nstage; ++t) {
+        const int x0 = t * WTA_TX;
+        const int hi = min(W, x0 + WTA_TX + p.min_disp + D - 1);
+        __syncthreads();                              // previous stage done with the ring
+        for (int i = threadIdx.x; i < (hi - loaded) * CH; i += blockDim.x) {
+            const int x = loaded + i / CH, c = i % CH;
+            cp_async8(sbuf + (x % NB) * BS + c * 4, S + (long long)x * D + c * 4);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        loaded = max(loaded, hi);
+        __syncthreads();
+        // left view
+        {
+            const int xp = x0 + warp * 32 + lane;
+            if (xp < W) {
+                int ds; bool uf; float disp;
+                wta_left_lane<D>(p, sbuf + (xp % NB) * BS, ds, uf, disp);
+                const long long o = frame * a.px_stride + (long long)y * W + xp;
+                uint8_t m = 0;
+                if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
+                if (uf) m |= MASK_UNIQUE;
+                a.fs.dstar_l[o] = (int16_t)ds;
+                a.fs.mask_l[o] = m;
+                a.fs.dl[o] = disp;
             }
-            clb = clb_n;
-            crb = crb_n;
+        }
+        __syncthreads();                              // left poisoning done before diagonal reads
+        // right view
+        {
+            const int xr = x0 + warp * 32 + lane;
+            const int nd = min(D, W - p.min_disp - xr);
+            if (xr < W && nd > 0) {
+                int ds = -1; bool uf = false; float disp = 0.0f;
+                wta_right_lane<D>(p, sbuf, NB, (xr + p.min_disp) % NB, nd, ds, uf, disp);
+                const long long o = frame * a.px_stride + (long long)y * W + xr;
+                uint8_t m = 0;
+                if (!(vrow && xr >= p.R && xr < W - p.R)) m |= MASK_BORDER;
+                if (uf) m |= MASK_UNIQUE;
+                a.fs.dstar_r[o] = (int16_t)ds;
+                a.fs.mask_r[o] = m;
+                a.fs.dr[o] = disp;
+            }
         }
     }
 }
@@ -837,10 +870,19 @@ static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up)
 
 static RKernel pick_rkernel(int D)
 {
-    if (D == 16) return v2::row_kernel<16>;
-    if (D == 32) return v2::row_kernel<32>;
-    if (D == 64) return v2::row_kernel<64>;
-    if (D == 128) return v2::row_kernel<128>;
+    if (D == 16) return v2::hrow_kernel<16>;
+    if (D == 32) return v2::hrow_kernel<32>;
+    if (D == 64) return v2::hrow_kernel<64>;
+    if (D == 128) return v2::hrow_kernel<128>;
+    return nullptr;
+}
+
+static RKernel pick_wkernel(int D)
+{
+    if (D == 16) return v2::wta2_kernel<16>;
+    if (D == 32) return v2::wta2_kernel<32>;
+    if (D == 64) return v2::wta2_kernel<64>;
+    if (D == 128) return v2::wta2_kernel<128>;
     return nullptr;
 }
 
@@ -933,15 +975,14 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         for (VKernel k : {kd, ku})
             cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
     }
-    switch (p.D) {                      // the row kernel's window geometry (RowGeom<D>)
-        case 16: pl.nbuf = v2::RowGeom<16>::NB; pl.bstride = v2::RowGeom<16>::BS; break;
-        case 32: pl.nbuf = v2::RowGeom<32>::NB; pl.bstride = v2::RowGeom<32>::BS; break;
-        case 64: pl.nbuf = v2::RowGeom<64>::NB; pl.bstride = v2::RowGeom<64>::BS; break;
-        default: pl.nbuf = v2::RowGeom<128>::NB; pl.bstride = v2::RowGeom<128>::BS; break;
-    }
+    // WTA kernel ring: rows [128t, 128t + 127 + min + D - 1] of stage t must
+    // fit beside nothing else; NB > 128 + min + D - 1
+    pl.nbuf = ((v2::WTA_TX + p.min_disp + p.D + 31) / 32) * 32;
+    pl.bstride = p.D + 4;               // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
-    RKernel rk = pick_rkernel(p.D);
-    cudaFuncSetAttribute((const void*)rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.rsmem);
+    if (pl.rsmem > 200 * 1024) return no("min_disp + num_disp too large for the WTA ring");
+    RKernel wk = pick_wkernel(p.D);
+    cudaFuncSetAttribute((const void*)wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.rsmem);
     cudaGetLastError();
     pl.ok = true;
     return true;
@@ -975,13 +1016,19 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1);
         return launch_vsweep(k, pl, nframes, a, s) == cudaSuccess ? 0 : -1;
     }
+    (void)agg;
     RArgs r{};
     r.p = p; r.cl = (const uint32_t*)cl; r.cr = (const uint32_t*)cr; r.sig_stride = sig_stride;
     r.pab = pab; r.stash = stash; r.cell_stride = cell_stride; r.fs = fs; r.px_stride = px_stride;
-    r.agg = agg; r.nbuf = pl.nbuf; r.bstride = pl.bstride;
-    RKernel k = pick_rkernel(p.D);
-    k<<<dim3(p.H, nframes), 32, pl.rsmem, s>>>(r);
-    return 0;
+    r.nbuf = pl.nbuf; r.bstride = pl.bstride;
+    if (stage == 2) {
+        RKernel k = pick_rkernel(p.D);
+        k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
+    } else {
+        RKernel k = pick_wkernel(p.D);
+        k<<<dim3(p.H, nframes), 32 * v2::WTA_WARPS, pl.rsmem, s>>>(r);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace asd
