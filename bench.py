@@ -194,7 +194,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="asd", choices=["asd", "reference"])
     ap.add_argument("--frames", type=int, default=FRAMES_PER_STEP, help="frames per step per GPU")
-    ap.add_argument("--max-batch", type=int, default=MAX_BATCH)
+    ap.add_argument("--max-batch", type=int, default=0,
+                    help="frames per asd_depth_batch chunk (0: a whole number of cluster waves, ~32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -227,6 +228,11 @@ def main():
     disp = torch.empty(B, H, W, device=dev)
     depth = torch.empty(B, H, W, device=dev)
     stats = torch.zeros(B, 4, dtype=torch.int32, device=dev)
+    if args.max_batch <= 0:
+        probe = asd.Stereo(asd.Params(**cfg.params_dict()), local, 1)
+        fpw = probe.frames_per_wave
+        probe.close()
+        args.max_batch = max(1, (MAX_BATCH // fpw) * fpw) if fpw > 0 else MAX_BATCH
     st = asd.Stereo(asd.Params(**cfg.params_dict()), local, args.max_batch)
     stream = torch.cuda.current_stream(dev)
 

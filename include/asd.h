@@ -180,6 +180,15 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n);
 /* The engine the context runs (ASD_ENGINE_D1 or ASD_ENGINE_D3). */
 int asd_engine(const asd_ctx* ctx);
 
+/* Frames the engine's widest kernel keeps resident at once on this device
+ * (D3: thread-block clusters of the sweep kernels that fit; D1: 0 = any).
+ * Choosing max_batch as a multiple of it avoids a partial last wave. */
+int asd_frames_per_wave(const asd_ctx* ctx);
+
+/* Human-readable description of the chosen kernel geometry (cluster size,
+ * CTA shape, residency), NUL-terminated into buf[0..n).  Returns its length. */
+int asd_plan_info(const asd_ctx* ctx, char* buf, int n);
+
 /* ---- live stage timing (CUDA events on the caller's stream) ----
  * asd_profile_begin(ctx, max_launches) pre-creates events for up to
  * max_launches kernel launches; from then on every launch the context enqueues

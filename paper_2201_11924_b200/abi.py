@@ -70,6 +70,8 @@ SYMBOLS = [
     ("asd_depth_debug", _I, [_VP, _VP, _VP, ctypes.POINTER(asd_debug_out), _VP, _VP, _VP]),
     ("asd_launches_per_batch", _I, [_VP, _I]),
     ("asd_engine", _I, [_VP]),
+    ("asd_frames_per_wave", _I, [_VP]),
+    ("asd_plan_info", _I, [_VP, ctypes.c_char_p, _I]),
     ("asd_profile_begin", _I, [_VP, _I]),
     ("asd_profile_end", _I, [_VP, ctypes.POINTER(asd_stage_times)]),
     ("asd_strerror", ctypes.c_char_p, [_I]),
@@ -205,6 +207,16 @@ class Stereo:
     @property
     def engine(self) -> int:
         return int(self._lib.asd_engine(self._ctx))
+
+    @property
+    def frames_per_wave(self) -> int:
+        return int(self._lib.asd_frames_per_wave(self._ctx))
+
+    @property
+    def plan_info(self) -> str:
+        buf = ctypes.create_string_buffer(512)
+        self._lib.asd_plan_info(self._ctx, buf, 512)
+        return buf.value.decode()
 
     def launches_per_batch(self, n: int) -> int:
         return int(self._lib.asd_launches_per_batch(self._ctx, n))

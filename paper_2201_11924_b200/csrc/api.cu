@@ -448,6 +448,26 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 
 int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }
 
+int asd_plan_info(const asd_ctx* ctx, char* buf, int n)
+{
+    if (!ctx || !buf || n <= 0) return 0;
+    if (ctx->engine != ASD_ENGINE_D3)
+        return snprintf(buf, n, "engine D1: %d direction kernels (warp per line), WTA kernel", ctx->dp.paths);
+    const V2Plan& q = ctx->plan;
+    return snprintf(buf, n,
+                    "engine D3: sweeps DC=%d T=%d paths/sweep=%d cluster=%d CTA=%d cols x %d thr, "
+                    "%d resident CTAs (%d frames/wave), smem %zu B; WTA ring %d rows",
+                    q.DC, q.T, q.NP, q.cs, q.w, q.vthreads, q.active_ctas,
+                    q.NP == 3 ? q.active_ctas / q.cs : 0, q.vsmem, q.nbuf);
+}
+
+int asd_frames_per_wave(const asd_ctx* ctx)
+{
+    if (!ctx || ctx->engine != ASD_ENGINE_D3) return 0;
+    const int per = ctx->plan.NP == 3 ? ctx->plan.cs : 1;
+    return ctx->plan.NP == 3 ? ctx->plan.active_ctas / per : 0;
+}
+
 int asd_depth_batch(asd_ctx* ctx, int n, const uint8_t* left, const uint8_t* right,
                     float* out_disp, float* out_depth, asd_frame_stats* stats, void* cuda_stream)
 {

@@ -136,7 +136,7 @@ struct VGeom {
 };
 
 template <int DC, int T, int NP, bool UP, int DPL_ROW>
-__global__ void __launch_bounds__(DC == 32 ? 512 : 1024)
+__global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
 {
     using G = VGeom<DC, T>;
@@ -253,14 +253,6 @@ vsweep_kernel(VArgs a)
     for (int i = 0; i < H; ++i) {
         const int y = row_of(i);
         if (i > 0) wait();
-        // ---- vertical path: predecessor = own column
-        {
-            uint32_t Ln[NR], mnew;
-            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
-#pragma unroll
-            for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
-            Mv = mnew;
-        }
         if (NP == 3) {
             const int rs = (i + 1) & 1;              // slot written at row i-1
             uint32_t Pp[NR], Mp;
@@ -294,12 +286,13 @@ vsweep_kernel(VArgs a)
             path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
         }
         // columns beyond the image act as "outside" predecessors: zero state
-        if (!xin) {
+        if (NP == 3 && !xin) {
 #pragma unroll
-            for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
-            Mv = Ml = Mr = 0u;
+            for (int k = 0; k < NR; ++k) { Ll[k] = 0u; Lr[k] = 0u; }
+            Ml = Mr = 0u;
         }
-        // ---- halos for the next row (slot i & 1)
+        // ---- halos for the next row (slot i & 1): written before the vertical
+        // path so the DSMEM stores are in flight while it runs
         if (NP == 3) {
             const int ws = i & 1;
             if (col == CPW - 1) {            // my "L" state feeds column x+1 next row
@@ -338,6 +331,19 @@ vsweep_kernel(VArgs a)
                     if (chunk == 0) *dstm = Mr;
                 }
             }
+        }
+        // ---- vertical path: predecessor = own column (after the halo stores)
+        {
+            uint32_t Ln[NR], mnew;
+            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
+            Mv = mnew;
+        }
+        if (!xin) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Lv[k] = 0u;
+            Mv = 0u;
         }
         // ---- stage row i+3 (async), make row i+2's copies complete, publish
         if (i + 3 < H) stage(row_of(i + 3), (i + 3) & 3);
@@ -917,14 +923,17 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     const char* force = getenv("ASD_V2_DC16");
     if (p.D == 128 && force && force[0] == '1') { pl.DC = 16; pl.T = 8; }
     const int T = pl.T, CPW = 32 / T;
-    const int maxt = pl.DC == 32 ? 512 : 1024;
+    const int maxt = pl.DC == 32 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
     VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false);
     VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true);
     if (!kd || !ku) return no("no sweep kernel instance");
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double best = -1.0;
+    const char* fcs = getenv("ASD_V2_CS");            // testing aid: force a cluster size
+    const int force_cs = fcs ? atoi(fcs) : 0;
     for (int cs = 1; cs <= 16; ++cs) {
+        if (force_cs > 0 && cs != force_cs) continue;
         int w = (p.W + cs - 1) / cs;
         w = (w + CPW - 1) / CPW * CPW;
         if ((long long)w * (cs - 1) >= p.W && cs > 1) continue;     // last CTA would be empty

@@ -1,0 +1,50 @@
+"""Per-stage device times (libasd live CUDA-event timing) for one configuration.
+
+    python tools/stage_times.py [--config C] [--paths 8] [--frames 32] [--max-batch 32] [--engine 0]
+"""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2201_11924_b200 as asd
+import synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C")
+ap.add_argument("--paths", type=int, default=None)
+ap.add_argument("--frames", type=int, default=32)
+ap.add_argument("--max-batch", type=int, default=0)
+ap.add_argument("--engine", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+args = ap.parse_args()
+cfg = synth.CONFIGS[args.config]
+d = cfg.params_dict()
+if args.paths:
+    d["paths"] = args.paths
+Lp, Rp = synth.frame_pool(cfg, 4)
+idx = [i % 4 for i in range(args.frames)]
+L = torch.from_numpy(Lp[idx]).cuda(); R = torch.from_numpy(Rp[idx]).cuda()
+out = torch.empty(args.frames, cfg.height, cfg.width, device="cuda")
+if args.max_batch <= 0:
+    probe = asd.Stereo(asd.Params(**d, engine=args.engine), 0, 1)
+    fpw = probe.frames_per_wave
+    probe.close()
+    args.max_batch = max(1, (32 // fpw) * fpw) if fpw > 0 else 32
+    print("frames per wave", fpw, "max_batch", args.max_batch)
+st = asd.Stereo(asd.Params(**d, engine=args.engine), 0, args.max_batch)
+print(st.plan_info)
+st.asd_depth_batch(L, R, out, out)
+torch.cuda.synchronize()
+st.profile_begin(4096)
+for _ in range(args.reps):
+    st.asd_depth_batch(L, R, out, out)
+torch.cuda.synchronize()
+prof = st.profile_end()
+n = args.frames * args.reps
+tot = sum(prof[k]["ms"] for k in asd.abi.STAGES)
+print(f"config {args.config} paths {d['paths']} engine {st.engine}: {1000 * tot / n:.1f} us/frame, "
+      f"{n / (tot / 1000):.0f} frames/s (sum of stages)")
+for k in asd.abi.STAGES:
+    if prof[k]["launches"]:
+        us = 1000 * prof[k]["ms"] / n
+        gbs = prof[k]["alg_bytes"] / (prof[k]["ms"] / 1000) / 1e9
+        print(f"  {k:7s} {us:8.1f} us/frame  {gbs:8.1f} GB/s algorithmic  launches {prof[k]['launches']}")
