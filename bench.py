@@ -208,6 +208,7 @@ def main():
 
     import paper_2201_11924_b200 as asd
     import synth
+    from paper_2201_11924_b200.dist import gather_frame_stats, max_over_ranks, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -222,7 +223,8 @@ def main():
     B = args.frames
     H, W = cfg.height, cfg.width
     pool_L, pool_R = synth.frame_pool(cfg, POOL)
-    idx = [(rank * B + i) % POOL for i in range(B)]
+    f0, f1 = shard_range(world * B, rank, world)          # this rank's frames of the job
+    idx = [f % POOL for f in range(f0, f1)]
     L = torch.from_numpy(pool_L[idx]).to(dev)
     R = torch.from_numpy(pool_R[idx]).to(dev)
     disp = torch.empty(B, H, W, device=dev)
@@ -262,20 +264,12 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1)
     prof = st.profile_end()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, dev)
     frames_total = world * B * args.steps
     value = frames_total / (ms_max / 1000.0)
 
     # ---- per-frame stats gather (NCCL, after timing) + parity of checksums
-    st_all = stats
-    if world > 1:
-        gathered = torch.empty(world * B, 4, dtype=torch.int32, device=dev)
-        dist.all_gather_into_tensor(gathered, stats)
-        st_all = gathered
-    st_all = st_all.cpu().numpy()
+    st_all = gather_frame_stats(stats).cpu().numpy()
 
     # ---- end-to-end through the host entry point (pinned host buffers)
     e2e = None
@@ -296,10 +290,8 @@ def main():
         h1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        t2 = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(frames_total / (float(t2.item()) / 1000.0), 3), "unit": "frames/s",
+        t2 = max_over_ranks(h0.elapsed_time(h1), dev)
+        e2e = {"value": round(frames_total / (t2 / 1000.0), 3), "unit": "frames/s",
                "h2d_bytes_per_step": int(Lh.numel() + Rh.numel()),
                "d2h_bytes_per_step": int(4 * (dh.numel() + zh.numel()) + 16 * B),
                "api": "asd_depth_batch_host"}
@@ -307,22 +299,43 @@ def main():
     if rank == 0:
         pk = peaks()
         hbm_peak = pk["hbm_gbs"] if pk else 6650.0
+        sm_mhz = pk.get("sm_max_mhz", 1965.0) if pk else 1965.0
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        alu_peak = nsm * 128 * sm_mhz * 1e6 / 1e12       # T int lane-ops/s
         top = max(asd.abi.STAGES, key=lambda k: prof[k]["ms"])
-        agg = prof[top]
-        avg_ms = agg["ms"] / max(1, agg["launches"])
-        alg_per_launch = agg["alg_bytes"] / max(1, agg["launches"])
-        achieved = alg_per_launch / (avg_ms / 1000.0) / 1e9
-        stage_share = {k: round(prof[k]["ms"] / max(1e-9, sum(prof[s]["ms"] for s in asd.abi.STAGES)), 4)
-                       for k in asd.abi.STAGES}
+        tp = prof[top]
+        nl = max(1, tp["launches"])
+        avg_ms = tp["ms"] / nl
+        alg_b = tp["alg_bytes"] / nl
+        alg_o = tp["alg_ops"] / nl
+        hbm_ach = alg_b / (avg_ms / 1000.0) / 1e9
+        tot_ms = sum(prof[k]["ms"] for k in asd.abi.STAGES)
+        stage_share = {k: round(prof[k]["ms"] / max(1e-9, tot_ms), 4) for k in asd.abi.STAGES
+                       if prof[k]["launches"]}
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tp)).get("agg_bytes_per_launch_per_frame")
-                if traffic is not None:
-                    traffic = traffic * min(args.max_batch, B)
+                per_frame = json.load(open(tpath)).get(top)
+                if per_frame is not None:
+                    traffic = per_frame * min(args.max_batch, B)
             except Exception:
                 traffic = None
+        if alg_o > 0:
+            ach = alg_o / (avg_ms / 1000.0) / 1e12
+            roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2),
+                    "unit": "Tops/s", "frac": round(ach / alu_peak, 4), "traffic": traffic,
+                    "alg_ops_per_launch": alg_o,
+                    "peak_source": f"{nsm} SMs x 128 int lane-ops/clk x {sm_mhz:.0f} MHz "
+                                   "(tools/ubench.cu measured 123.5/clk/SM)",
+                    "hbm_view": {"achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": round(hbm_ach / hbm_peak, 4)}}
+        else:
+            roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(hbm_ach / hbm_peak, 4), "traffic": traffic,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md"}
+        roof.update({"kernel": KERNEL_NAMES[top], "alg_bytes_per_launch": alg_b,
+                     "avg_launch_ms": round(avg_ms, 4), "launches": nl})
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, pool_L, pool_R)
@@ -336,15 +349,10 @@ def main():
                                    "uniqueness 10%, LR 1 px, sub-pixel, depth",
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
-                       "l2": "inputs larger than L2 (236 MB/step/GPU; plus 236 MB S scratch per frame)",
-                       "engine": {1: "D1: one SGM kernel per path direction",
-                                  3: "D3: grouped sweeps (cluster down/up kernels + fused row/WTA kernel)"}[st.engine]},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                         "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                         "kernel": KERNEL_NAMES[top],
-                         "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": round(avg_ms, 4),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md"},
-            "stage_ms": {k: round(prof[k]["ms"], 3) for k in asd.abi.STAGES},
+                       "l2": "inputs larger than L2 (236 MB/step/GPU) + per-frame scratch > L2",
+                       "engine": st.plan_info},
+            "roofline": roof,
+            "stage_ms": {k: round(prof[k]["ms"], 3) for k in asd.abi.STAGES if prof[k]["launches"]},
             "stage_share": stage_share,
             "clocks": clk.summary(),
             "gpu_launches": lp * args.steps,

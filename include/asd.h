@@ -194,8 +194,9 @@ int asd_plan_info(const asd_ctx* ctx, char* buf, int n);
  * max_launches kernel launches; from then on every launch the context enqueues
  * is bracketed by an event pair on the launching stream (no host sync).
  * asd_profile_end synchronises on those events and fills `out` with, per
- * stage, the summed device time, the number of launches, and the ALGORITHMIC
- * bytes those launches must move at minimum (DESIGN.md §6 per-unit figures x
+ * stage, the summed device time, the number of launches, the ALGORITHMIC
+ * bytes those launches must move at minimum and, for the integer-bound D3
+ * kernels, the algorithmic integer lane-ops (DESIGN.md §5 per-unit figures x
  * units processed), then stops profiling.  Launches beyond max_launches are
  * counted in `dropped` and not timed. */
 #define ASD_STAGE_CENSUS 0   /* K1 census */
@@ -209,6 +210,7 @@ int asd_plan_info(const asd_ctx* ctx, char* buf, int n);
 typedef struct asd_stage_times {
     double ms[ASD_STAGE_COUNT];
     double alg_bytes[ASD_STAGE_COUNT];
+    double alg_ops[ASD_STAGE_COUNT];     /* integer lane-ops, 0 if not ALU-modelled */
     int32_t launches[ASD_STAGE_COUNT];
     int32_t dropped;
     int32_t reserved;

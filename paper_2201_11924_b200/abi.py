@@ -53,6 +53,7 @@ STAGES = ("census", "dir", "wta", "lr", "down", "up", "row")
 
 class asd_stage_times(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 7), ("alg_bytes", ctypes.c_double * 7),
+                ("alg_ops", ctypes.c_double * 7),
                 ("launches", ctypes.c_int32 * 7), ("dropped", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
@@ -201,7 +202,8 @@ class Stereo:
     def profile_end(self) -> dict:
         t = asd_stage_times()
         _check(self._lib.asd_profile_end(self._ctx, ctypes.byref(t)), self._ctx)
-        return {name: {"ms": t.ms[i], "alg_bytes": t.alg_bytes[i], "launches": t.launches[i]}
+        return {name: {"ms": t.ms[i], "alg_bytes": t.alg_bytes[i], "alg_ops": t.alg_ops[i],
+                       "launches": t.launches[i]}
                 for i, name in enumerate(STAGES)} | {"dropped": t.dropped}
 
     @property

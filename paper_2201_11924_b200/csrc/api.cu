@@ -53,7 +53,7 @@ struct asd_ctx {
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
     cudaEvent_t ev_comp[2] = {nullptr, nullptr};
     // live stage timing (asd_profile_begin/end)
-    struct Mark { int stage; double bytes; };
+    struct Mark { int stage; double bytes; double ops; };
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;   // 2 per launch
     std::vector<Mark> prof_marks;
@@ -202,12 +202,12 @@ FrameScratch frame_scratch(asd_ctx* c)
 // Bracket one kernel launch with an event pair when profiling is on.
 struct ProfScope {
     asd_ctx* c; cudaStream_t s; int idx = -1;
-    ProfScope(asd_ctx* c_, cudaStream_t s_, int stage, double bytes) : c(c_), s(s_) {
+    ProfScope(asd_ctx* c_, cudaStream_t s_, int stage, double bytes, double ops = 0.0) : c(c_), s(s_) {
         if (!c->prof) return;
         const size_t k = c->prof_marks.size();
         if (2 * k + 1 >= c->prof_ev.size()) { ++c->prof_dropped; return; }
         idx = (int)k;
-        c->prof_marks.push_back({stage, bytes});
+        c->prof_marks.push_back({stage, bytes, ops});
         cudaEventRecord(c->prof_ev[2 * k], s);
     }
     ~ProfScope() { if (idx >= 0) cudaEventRecord(c->prof_ev[2 * idx + 1], s); }
@@ -233,6 +233,14 @@ static double alg_bytes_down(const DevParams& p) { return 1.0 * p.ncell; }
 static double alg_bytes_up(const DevParams& p) { return 3.0 * p.ncell; }
 static double alg_bytes_row(const DevParams& p) { return 6.0 * p.ncell; }
 static double alg_bytes_wta3(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * 7; }
+// Integer lane-ops per cell of the minimal packed formulation:
+// 2.5 per cell-path of recursion (5 u16x2 instructions per two disparities),
+// 2.5 per cell of cost (XOR, POPC, half a pack), 0.5 per cell of partial
+// output; hrow evaluates the cost twice and adds S (1); the WTA 1.5 per cell
+// and view (half a key IMAD, half a min, half a second-pass min).
+static double alg_ops_sweep(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2.5 * p.ncell + 3.0 * p.ncell; }
+static double alg_ops_row(const DevParams& p) { return 2 * 2.5 * p.ncell + 2 * 2.5 * p.ncell + 1.0 * p.ncell; }
+static double alg_ops_wta3(const DevParams& p) { return 3.0 * p.ncell; }
 
 // Enqueue the whole path for n <= max_batch frames resident on the device.
 int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
@@ -249,7 +257,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
     FrameScratch fs = frame_scratch(c);
     if (c->engine == ASD_ENGINE_D3) {
         {
-            ProfScope ps(c, s, ASD_STAGE_DOWN, n * alg_bytes_down(p));
+            ProfScope ps(c, s, ASD_STAGE_DOWN, n * alg_bytes_down(p), n * alg_ops_sweep(p));
             if (launch_v2_stage(0, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
                                 p.ncell, fs, npx, nullptr, s) != 0) {
                 set_err(c, "down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -257,7 +265,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             }
         }
         {
-            ProfScope ps(c, s, ASD_STAGE_UP, n * alg_bytes_up(p));
+            ProfScope ps(c, s, ASD_STAGE_UP, n * alg_bytes_up(p), n * alg_ops_sweep(p));
             if (launch_v2_stage(1, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
                                 p.ncell, fs, npx, nullptr, s) != 0) {
                 set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -265,14 +273,14 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             }
         }
         {
-            ProfScope ps(c, s, ASD_STAGE_ROW, n * alg_bytes_row(p));
+            ProfScope ps(c, s, ASD_STAGE_ROW, n * alg_bytes_row(p), n * alg_ops_row(p));
             launch_v2_stage(2, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
                             p.ncell, fs, npx, nullptr, s);
         }
         if (agg_debug)                       // S of frame 0 (natural order) before the WTA
             cudaMemcpyAsync(agg_debug, c->pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, s);
         {
-            ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta3(p));
+            ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta3(p), n * alg_ops_wta3(p));
             if (launch_v2_stage(3, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
                                 p.ncell, fs, npx, nullptr, s) != 0) {
                 set_err(c, "WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -618,6 +626,7 @@ int asd_profile_end(asd_ctx* ctx, asd_stage_times* out)
         const int st = ctx->prof_marks[k].stage;
         out->ms[st] += ms;
         out->alg_bytes[st] += ctx->prof_marks[k].bytes;
+        out->alg_ops[st] += ctx->prof_marks[k].ops;
         out->launches[st] += 1;
     }
     out->dropped = ctx->prof_dropped;
