@@ -41,7 +41,7 @@ struct asd_ctx {
     // design D3 scratch
     int engine = ASD_ENGINE_D1;
     V2Plan plan{};
-    uint8_t* pa = nullptr;        // [B][H][W][D] u8 partial (down sweep)
+    uint8_t* pa = nullptr;        // [B][H][W][D] u16 P_A | C << 8 (down sweep)
     uint16_t* pab = nullptr;      // [B][H][W][D] u16 partial (down + up)
     uint8_t* stash = nullptr;     // [B][H][W][D] u8 left->right path
     // host-path staging: two chunk buffers (inputs u8, outputs f32) + stats
@@ -172,7 +172,7 @@ Layout layout(const DevParams& d, int max_batch, int engine)
     const size_t B = (size_t)max_batch;
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
     L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
-    L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
+    L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;     // P_A | C << 8, u16
     L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
     L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
     L.px_f32 = align_up(B * d.npx * 4);
@@ -224,13 +224,13 @@ static double alg_bytes_census(const DevParams& p, size_t sig) { return 2.0 * p.
 static double alg_bytes_dir(const DevParams& p, bool first) { return (first ? 2.0 : 4.0) * p.ncell; }
 static double alg_bytes_wta(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * (4 + 2 + 1); }
 static double alg_bytes_lr(const DevParams& p) { return p.npx * (2 * (4 + 1) + 2 + 2 * 4.0); }
-// Design D3: down sweep writes the u8 partial (1 B/cell); up sweep reads it and
-// writes the u16 partial (3 B/cell); the row kernel reads the u16 partial,
+// Design D3: down sweep writes P_A | C << 8 (u16, 2 B/cell); up sweep reads it
+// and writes P_AB | C << 9 (4 B/cell); the row kernel reads the latter,
 // writes + reads the u8 left->right stash and writes S over the partial
 // (6 B/cell); the WTA kernel reads S once (2 B/cell) and writes the per-pixel
 // maps of both views (2 x (4 + 2 + 1) B/px).  Census reads are L2-resident.
-static double alg_bytes_down(const DevParams& p) { return 1.0 * p.ncell; }
-static double alg_bytes_up(const DevParams& p) { return 3.0 * p.ncell; }
+static double alg_bytes_down(const DevParams& p) { return 2.0 * p.ncell; }
+static double alg_bytes_up(const DevParams& p) { return 4.0 * p.ncell; }
 static double alg_bytes_row(const DevParams& p) { return 6.0 * p.ncell; }
 static double alg_bytes_wta3(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * 7; }
 // Integer lane-ops per cell of the minimal packed formulation:
@@ -239,7 +239,8 @@ static double alg_bytes_wta3(const DevParams& p) { return 2.0 * p.ncell + 2.0 * 
 // output; hrow evaluates the cost twice and adds S (1); the WTA 1.5 per cell
 // and view (half a key IMAD, half a min, half a second-pass min).
 static double alg_ops_sweep(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2.5 * p.ncell + 3.0 * p.ncell; }
-static double alg_ops_row(const DevParams& p) { return 2 * 2.5 * p.ncell + 2 * 2.5 * p.ncell + 1.0 * p.ncell; }
+static double alg_ops_up(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2.5 * p.ncell + 2.0 * p.ncell; }
+static double alg_ops_row(const DevParams& p) { return 2 * 2.5 * p.ncell + 2.5 * p.ncell + 2.0 * p.ncell; }
 static double alg_ops_wta3(const DevParams& p) { return 3.0 * p.ncell; }
 
 // Enqueue the whole path for n <= max_batch frames resident on the device.
@@ -265,7 +266,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             }
         }
         {
-            ProfScope ps(c, s, ASD_STAGE_UP, n * alg_bytes_up(p), n * alg_ops_sweep(p));
+            ProfScope ps(c, s, ASD_STAGE_UP, n * alg_bytes_up(p), n * alg_ops_up(p));
             if (launch_v2_stage(1, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
                                 p.ncell, fs, npx, nullptr, s) != 0) {
                 set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -401,7 +402,12 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
             return ASD_E_UNSUPPORTED;
         }
     }
-    const Layout L = layout(c->dp, max_batch, c->engine);
+    Layout L = layout(c->dp, max_batch, c->engine);
+    if (c->engine == ASD_ENGINE_D3) {           // P_A rows are padded to the sweep grid (cs*w columns)
+        const size_t padded = align_up((size_t)max_batch * c->dp.H * c->plan.cs * c->plan.w * c->dp.D * 2);
+        L.total += padded - L.pa;
+        L.pa = padded;
+    }
     bool ok = true;
     auto alloc = [&](void** q, size_t bytes) {
         if (ok && cudaMalloc(q, bytes) != cudaSuccess) ok = false;

@@ -15,7 +15,8 @@ namespace asd {
 
 constexpr int CT_X = 32, CT_Y = 8, CMAX_R = 7, CMAX_Q = 7;
 
-template <typename SigT>
+// CW, CH > 0: compile-time window (fully unrolled pair loop); 0: runtime window.
+template <typename SigT, int CW = 0, int CH = 0>
 __global__ void __launch_bounds__(CT_X * CT_Y)
 census_kernel(DevParams p, const uint8_t* __restrict__ left, const uint8_t* __restrict__ right,
               long long img_stride, SigT* __restrict__ out_l, SigT* __restrict__ out_r,
@@ -38,12 +39,21 @@ census_kernel(DevParams p, const uint8_t* __restrict__ left, const uint8_t* __re
     SigT sig = 0;
     if (census_valid(p, x, y)) {
         const int cx = threadIdx.x + p.R, cy = threadIdx.y + p.Q;
-        int i = 0;
-        for (int ky = 0; ky < p.ch && i < p.nb; ++ky) {
-            const int dy = ky - p.Q;
-            for (int kx = 0; kx < p.cw && i < p.nb; ++kx, ++i) {
-                const int dx = kx - p.R;
-                if (tile[cy + dy][cx + dx] > tile[cy - dy][cx - dx]) sig |= (SigT)1 << i;
+        if constexpr (CW > 0) {
+            constexpr int R = CW / 2, Q = CH / 2, NB = (CW * CH) / 2;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const int dy = i / CW - Q, dx = i % CW - R;
+                sig |= (SigT)(tile[cy + dy][cx + dx] > tile[cy - dy][cx - dx]) << i;
+            }
+        } else {
+            int i = 0;
+            for (int ky = 0; ky < p.ch && i < p.nb; ++ky) {
+                const int dy = ky - p.Q;
+                for (int kx = 0; kx < p.cw && i < p.nb; ++kx, ++i) {
+                    const int dx = kx - p.R;
+                    if (tile[cy + dy][cx + dx] > tile[cy - dy][cx - dx]) sig |= (SigT)1 << i;
+                }
             }
         }
     }
@@ -56,7 +66,16 @@ void launch_census(const DevParams& p, int nframes, const uint8_t* left, const u
 {
     dim3 grid((p.W + CT_X - 1) / CT_X, (p.H + CT_Y - 1) / CT_Y, 2 * nframes);
     dim3 block(CT_X, CT_Y);
-    if (p.nb <= 32)
+    if (p.cw == 9 && p.ch == 7)
+        census_kernel<uint32_t, 9, 7><<<grid, block, 0, s>>>(p, left, right, img_stride,
+            (uint32_t*)out_l, (uint32_t*)out_r, sig_stride);
+    else if (p.cw == 7 && p.ch == 7)
+        census_kernel<uint32_t, 7, 7><<<grid, block, 0, s>>>(p, left, right, img_stride,
+            (uint32_t*)out_l, (uint32_t*)out_r, sig_stride);
+    else if (p.cw == 5 && p.ch == 5)
+        census_kernel<uint32_t, 5, 5><<<grid, block, 0, s>>>(p, left, right, img_stride,
+            (uint32_t*)out_l, (uint32_t*)out_r, sig_stride);
+    else if (p.nb <= 32)
         census_kernel<uint32_t><<<grid, block, 0, s>>>(p, left, right, img_stride,
             (uint32_t*)out_l, (uint32_t*)out_r, sig_stride);
     else

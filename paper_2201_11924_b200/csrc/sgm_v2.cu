@@ -66,6 +66,16 @@ __device__ __forceinline__ void cluster_arrive()
 {
     asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
+// Relaxed arrive: no implicit release, so the partial-sum stores in flight are
+// not waited for; the warps that wrote DSMEM halos fence first.
+__device__ __forceinline__ void cluster_arrive_relaxed()
+{
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_cluster()
+{
+    asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait()
 {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -78,10 +88,12 @@ struct VArgs {
     const uint32_t* cl;       // census, [frames][H][W]
     const uint32_t* cr;
     long long sig_stride;
-    const uint8_t* pin;       // K_up input P_A  [frames][H][W][D] (chunk-interleaved u8)
-    uint8_t* pout8;           // K_down output P_A
+    const uint16_t* pin;      // K_up input: P_A | C << 8, u16 per cell, K_down's register order
+    uint16_t* pouta;          // K_down output (same)
     uint16_t* pout16;         // K_up output P_AB (row-kernel layout)
     long long cell_stride;    // H*W*D
+    long long pa_stride;      // frame stride of the P_A buffer: H * (cs*w) * D
+    int ablate;               // timing experiments only (ASD_V2_ABLATE); 0 in production
 };
 
 // ---------------------------------------------------------------- helpers
@@ -156,13 +168,20 @@ vsweep_kernel(VArgs a)
     const int x = x0 + xl;
     const int cstr = G::cstride(w);
     const int sw = G::slot_words(w);
-    const bool clustered = NP == 3 && a.cs > 1;
+    const bool clustered = NP == 3 && a.cs > 1 && !(a.ablate & 1);
 
     uint32_t* cens = smem;                   // [4][sw]: left row, then T right-row slices
     uint32_t* hL = cens + 4 * sw;            // [2][nw][T][NR]   (NP == 3)
     uint32_t* hR = hL + 2 * nw * T * NR;
     uint32_t* hLM = hR + 2 * nw * T * NR;    // [2][nw]
     uint32_t* hRM = hLM + 2 * nw;
+    // K_up output staging: one (CPW columns x D) u16 block per warp, so the
+    // global stores of P_AB can be issued as contiguous 512-byte warp stores
+    uint32_t* stg = (NP == 3 ? hRM + 2 * nw : cens + 4 * sw) + warp * (16 * DC);
+    // K_down -> K_up handoff in a private layout: the warp's (CPW columns x D)
+    // block is contiguous and instruction q of lane l covers 16 bytes at
+    // 512*q + 16*l, i.e. warp-contiguous stores and loads (row stride cs*w).
+    const int wpad = a.cs * a.w;
 
     const uint32_t* cl = a.cl + frame * a.sig_stride;
     const uint32_t* cr = a.cr + frame * a.sig_stride;
@@ -171,8 +190,10 @@ vsweep_kernel(VArgs a)
         for (int i = threadIdx.x; i < 4 * nw * T * NR + 4 * nw; i += blockDim.x) hL[i] = 0u;
     }
     auto row_of = [&](int i) { return UP ? H - 1 - i : i; };
-    // census rows -> shared memory with asynchronous copies (one commit group per row)
+    // census rows -> shared memory with asynchronous copies (one commit group per
+    // row).  K_up reads its costs from K_down's packed output instead.
     auto stage = [&](int yrow, int slot) {
+        if (UP) return;
         uint32_t* sl = cens + slot * sw;
         const uint32_t* rl = cl + (long long)yrow * W;
         const uint32_t* rr = cr + (long long)yrow * W;
@@ -195,7 +216,7 @@ vsweep_kernel(VArgs a)
     };
     const bool vcol = x >= p.R && x < W - p.R;
     auto cost = [&](int yrow, int slot, uint32_t (&C)[NR]) {
-        const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q;
+        const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q && !(a.ablate & 8);
         const uint32_t nbnb = (uint32_t)p.nb * 0x10001u;
         if (!vx) {
 #pragma unroll
@@ -220,18 +241,32 @@ vsweep_kernel(VArgs a)
             }
         }
     };
-    constexpr int PW = DC / 4;                       // u32 words of the u8 partial per thread
     const bool xin = x < W;
-    auto load_pin = [&](int yrow, uint32_t (&pw)[PW]) {
+    // K_up: P_A and C of one row from K_down's packed words (reg k = cells d0+k, d0+NR+k)
+    auto load_pin = [&](int yrow, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
         const uint4* src = reinterpret_cast<const uint4*>(
-            a.pin + frame * a.cell_stride + ((long long)yrow * W + (xin ? x : 0)) * D + chunk * DC);
+            a.pin + frame * a.pa_stride + ((long long)yrow * wpad + (x - col)) * D) + lane;
 #pragma unroll
-        for (int q = 0; q < PW / 4; ++q) {
-            const uint4 v = __ldg(src + q);
-            pw[4 * q] = v.x; pw[4 * q + 1] = v.y; pw[4 * q + 2] = v.z; pw[4 * q + 3] = v.w;
+        for (int q = 0; q < NR / 4; ++q) {
+            const uint4 v = __ldg(src + 32 * q);
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                pa[4 * q + j] = w4[j] & 0x00FF00FFu;
+                c[4 * q + j] = (w4[j] >> 8) & 0x00FF00FFu;
+            }
         }
     };
-    auto arrive = [&]() { if (clustered) cluster_arrive(); else __syncthreads(); };
+    // Publish this row: __syncthreads orders the intra-CTA halos and staged census
+    // rows; only the edge warps wrote into neighbouring CTAs (DSMEM), so only they
+    // pay a cluster-scope fence before the relaxed cluster arrive.
+    auto arrive = [&]() {
+        __syncthreads();
+        if (clustered) {
+            if (warp == 0 || warp == nw - 1) fence_cluster();
+            cluster_arrive_relaxed();
+        }
+    };
     auto wait = [&]() { if (clustered) cluster_wait(); };
 
     uint32_t Lv[NR], Ll[NR], Lr[NR];
@@ -239,7 +274,7 @@ vsweep_kernel(VArgs a)
     for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
     uint32_t Mv = 0u, Ml = 0u, Mr = 0u;
     uint32_t C[NR];
-    uint32_t pinw[PW];
+    uint32_t PA[NR];
 
     stage(row_of(0), 0);
     if (H > 1) stage(row_of(1), 1);
@@ -247,13 +282,13 @@ vsweep_kernel(VArgs a)
     cp_async_wait<0>();
     arrive();
     wait();
-    cost(row_of(0), 0, C);
-    if (UP) load_pin(row_of(0), pinw);
+    if (UP) load_pin(row_of(0), PA, C);
+    else cost(row_of(0), 0, C);
 
     for (int i = 0; i < H; ++i) {
         const int y = row_of(i);
         if (i > 0) wait();
-        if (NP == 3) {
+        if (NP == 3 && !(a.ablate & 4)) {
             const int rs = (i + 1) & 1;              // slot written at row i-1
             uint32_t Pp[NR], Mp;
             // path "L": predecessor column x-1 (down-right / up-right)
@@ -351,22 +386,22 @@ vsweep_kernel(VArgs a)
         cp_async_wait<1>();
         arrive();
         // ---- partial sum out (after the release so it does not wait on these stores)
-        if (xin) {
+        if (!(a.ablate & 2)) {
             uint32_t s[NR];
 #pragma unroll
             for (int k = 0; k < NR; ++k) s[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
-            const long long cell = ((long long)y * W + x) * D + chunk * DC;
             if (!UP) {
-                uint32_t o[PW];
+                // P_A (<= 255) | C << 8 (C <= 63): the up sweep needs no census
+                uint4* dst = reinterpret_cast<uint4*>(a.pouta + frame * a.pa_stride +
+                                                      ((long long)y * wpad + (x - col)) * D) + lane;
 #pragma unroll
-                for (int q = 0; q < PW; ++q) o[q] = __byte_perm(s[2 * q], s[2 * q + 1], 0x6420);
-                uint4* dst = reinterpret_cast<uint4*>(a.pout8 + frame * a.cell_stride + cell);
-#pragma unroll
-                for (int q = 0; q < PW / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                for (int q = 0; q < NR / 4; ++q)
+                    dst[32 * q] = make_uint4(s[4 * q] + C[4 * q] * 256u, s[4 * q + 1] + C[4 * q + 1] * 256u,
+                                             s[4 * q + 2] + C[4 * q + 2] * 256u, s[4 * q + 3] + C[4 * q + 3] * 256u);
             } else {
+                // P_AB (<= 510) | C << 9: the right->left row sweep needs no census
 #pragma unroll
-                for (int k = 0; k < NR; ++k)
-                    s[k] += __byte_perm(pinw[k >> 1], 0u, (k & 1) ? 0x4342 : 0x4140);
+                for (int k = 0; k < NR; ++k) s[k] += PA[k] + C[k] * 512u;
                 uint32_t o[NR];
                 if (DPL_ROW == 4) {
 #pragma unroll
@@ -384,15 +419,25 @@ vsweep_kernel(VArgs a)
                         o[g] = __byte_perm(s[kk], s[kk + 1], sel);
                     }
                 }
-                uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + cell);
+                // natural [x][d] layout through the warp's staging block
+                uint4* sb = reinterpret_cast<uint4*>(stg + (col * D + chunk * DC) / 2);
 #pragma unroll
-                for (int q = 0; q < NR / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                for (int q = 0; q < NR / 4; ++q) sb[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                __syncwarp();
+                const uint4* rb = reinterpret_cast<const uint4*>(stg);
+                uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + ((long long)y * W + (x - col)) * D);
+#pragma unroll
+                for (int q = 0; q < NR / 4; ++q) {
+                    const int pi = 32 * q + lane;                 // 16-byte piece of the block
+                    if (x - col + (pi * 8) / D < W) dst[pi] = rb[pi];
+                }
+                __syncwarp();
             }
         }
         // ---- next row's cost while the barrier completes
         if (i + 1 < H) {
-            cost(row_of(i + 1), (i + 1) & 3, C);
-            if (UP) load_pin(row_of(i + 1), pinw);
+            if (UP) load_pin(row_of(i + 1), PA, C);
+            else cost(row_of(i + 1), (i + 1) & 3, C);
         }
     }
     wait();                                          // pairs with the last arrive
@@ -534,15 +579,15 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr)
     asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
 }
 
-// One recursion step of a horizontal path for one warp (lane = DPL disparities).
-// Lp: predecessor state (zero at the line start), M: its min (0 at the start).
+// Horizontal-path step for one warp (lane = DPL disparities).  Register
+// layout: DPL == 4 -> A = (d0, d0+2), B = (d0+1, d0+3); DPL == 2 -> (d0, d0+1).
+// row_cost: the matching costs of this lane's disparities at x (census).
 template <int D, bool FAST = false>
-__device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint32_t clv, bool vx, int lim,
-                                             const uint32_t (&wnd)[RowGeom<D>::DPL],
-                                             const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t M,
-                                             uint32_t (&Ln)[RowGeom<D>::NRR])
+__device__ __forceinline__ void row_cost(const DevParams& p, int lane, uint32_t clv, bool vx, int lim,
+                                         const uint32_t (&wnd)[RowGeom<D>::DPL],
+                                         uint32_t (&C)[RowGeom<D>::NRR])
 {
-    constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
+    constexpr int DPL = RowGeom<D>::DPL;
     const int d0 = lane * DPL;
     uint32_t c[DPL];
     if (FAST || (vx && lim >= D - 1)) {               // warp-uniform fast path: all d valid
@@ -552,13 +597,27 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
 #pragma unroll
         for (int j = 0; j < DPL; ++j) c[j] = (vx && d0 + j <= lim) ? (uint32_t)__popc(clv ^ wnd[j]) : (uint32_t)p.nb;
     }
+    if constexpr (DPL == 4) {
+        C[0] = __byte_perm(c[0], c[2], 0x5410);
+        C[1] = __byte_perm(c[1], c[3], 0x5410);
+    } else {
+        C[0] = __byte_perm(c[0], c[1], 0x5410);
+    }
+}
+
+// row_rec: L_r(x) from the predecessor state Lp (zero at the line start) and
+// its min M (0 at the start); returns the new min.
+template <int D>
+__device__ __forceinline__ uint32_t row_rec(const DevParams& p, int lane, const uint32_t (&C)[RowGeom<D>::NRR],
+                                            const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t M,
+                                            uint32_t (&Ln)[RowGeom<D>::NRR])
+{
+    constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
     const uint32_t P1P1 = (uint32_t)p.p1 * 0x10001u;
     const uint32_t MP2 = (M + (uint32_t)p.p2) * 0x10001u;
     const uint32_t negMM = 0u - M * 0x10001u;
     uint32_t lmin;
     if constexpr (DPL == 4) {
-        // registers: A = (d0, d0+2), B = (d0+1, d0+3)
-        const uint32_t CA = __byte_perm(c[0], c[2], 0x5410), CB = __byte_perm(c[1], c[3], 0x5410);
         const uint32_t QA = Lp[0] + P1P1, QB = Lp[NRR - 1] + P1P1;
         uint32_t prevB = __shfl_up_sync(FULL, QB, 1);
         uint32_t nextA = __shfl_down_sync(FULL, QA, 1);
@@ -570,13 +629,11 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
         uint32_t tB = vmin2(vmin2(QA, dp1B), Lp[NRR - 1]);
         tA = vmin2(tA, MP2);
         tB = vmin2(tB, MP2);
-        Ln[0] = tA + CA + negMM;
-        Ln[NRR - 1] = tB + CB + negMM;
+        Ln[0] = tA + C[0] + negMM;
+        Ln[NRR - 1] = tB + C[NRR - 1] + negMM;
         const uint32_t mm = vmin2(Ln[0], Ln[NRR - 1]);
         lmin = min(mm & 0xFFFFu, mm >> 16);
     } else {
-        // register: (d0, d0+1)
-        const uint32_t C0 = __byte_perm(c[0], c[1], 0x5410);
         const uint32_t Q = Lp[0] + P1P1;
         uint32_t prev = __shfl_up_sync(FULL, Q, 1);
         uint32_t next = __shfl_down_sync(FULL, Q, 1);
@@ -586,7 +643,7 @@ __device__ __forceinline__ uint32_t row_step(const DevParams& p, int lane, uint3
         const uint32_t dp1 = __byte_perm(Q, next, 0x5432);
         uint32_t t = vmin2(vmin2(dm1, dp1), Lp[0]);
         t = vmin2(t, MP2);
-        Ln[0] = t + C0 + negMM;
+        Ln[0] = t + C[0] + negMM;
         lmin = min(Ln[0] & 0xFFFFu, Ln[0] >> 16);
     }
     if (ACT < 32 && lane >= ACT) lmin = 0xFFFFFFFFu;
@@ -655,8 +712,9 @@ hrow_kernel(RArgs a)
                         const uint32_t e = __shfl_sync(FULL, crb, j);
                         if (F || x < W) {
                             const bool vx = F || (vrow && x >= p.R && x < W - p.R);
-                            uint32_t Ln[NRR];
-                            M = row_step<D, F>(p, lane, clv, vx, x + lim0, wnd, L, M, Ln);
+                            uint32_t Cc[NRR], Ln[NRR];
+                            row_cost<D, F>(p, lane, clv, vx, x + lim0, wnd, Cc);
+                            M = row_rec<D>(p, lane, Cc, L, M, Ln);
 #pragma unroll
                             for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                             if (active) {
@@ -679,16 +737,12 @@ hrow_kernel(RArgs a)
     }
     __syncwarp();
     // ------------------------------------------------ right -> left, S out
+    // input: P_AB | C << 9 per cell (K_up), so no census is needed here
     {
-        uint32_t L[NRR], wnd[DPL];
+        uint32_t L[NRR];
 #pragma unroll
         for (int k = 0; k < NRR; ++k) L[k] = 0u;
         uint32_t M = 0u;
-#pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-            const int xr = W - 1 - p.min_disp - d0 - j;
-            wnd[j] = (xr >= 0 && xr < W) ? __ldg(cr + xr) : 0u;
-        }
         uint32_t P[SG][NRR], Sx[SG], Pn[SG][NRR], Sn[SG];
         auto load_sg = [&](int xb8, uint32_t (&PP)[SG][NRR], uint32_t (&SS)[SG]) {
 #pragma unroll
@@ -711,55 +765,42 @@ hrow_kernel(RArgs a)
                 }
             }
         };
-        const int gtop = ngrp - 1;
-        uint32_t clb = blk(cl, gtop << 5), crb = blk(cr, (gtop << 5) - p.min_disp - D);
-        load_sg((gtop << 5) + 32 - SG, P, Sx);
-        for (int g = gtop; g >= 0; --g) {
-            const int xb = g << 5;
-            const uint32_t clb_n = blk(cl, xb - 32), crb_n = blk(cr, xb - 32 - p.min_disp - D);
-            const bool fast = fast_group(xb);
-            for (int s = 32 - SG; s >= 0; s -= SG) {
-                load_sg(xb + s - SG, Pn, Sn);
-                auto body = [&](auto ftag) {
-                    constexpr bool F = decltype(ftag)::value;
+        const int xtop = ((W - 1) / SG) * SG;              // sub-groups aligned to SG
+        load_sg(xtop, P, Sx);
+        for (int xs = xtop; xs >= 0; xs -= SG) {
+            load_sg(xs - SG, Pn, Sn);
 #pragma unroll
-                    for (int k = SG - 1; k >= 0; --k) {
-                        const int j = s + k, x = xb + j;
-                        const uint32_t clv = __shfl_sync(FULL, clb, j);
-                        const uint32_t e = __shfl_sync(FULL, crb, j);
-                        if (F || x < W) {
-                            const bool vx = F || (vrow && x >= p.R && x < W - p.R);
-                            uint32_t Ln[NRR];
-                            M = row_step<D, F>(p, lane, clv, vx, x + lim0, wnd, L, M, Ln);
+            for (int k = SG - 1; k >= 0; --k) {
+                const int x = xs + k;
+                if (x < W) {
+                    uint32_t Cc[NRR], Pv[NRR], Ln[NRR];
 #pragma unroll
-                            for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                            if (active) {
-                                if constexpr (DPL == 4) {
-                                    const uint32_t s0 = P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
-                                    const uint32_t s1 = P[k][NRR - 1] + __byte_perm(Sx[k], 0u, 0x4342) + Ln[NRR - 1];
-                                    *reinterpret_cast<uint2*>(pab + (long long)x * D) =
-                                        make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
-                                } else {
-                                    *reinterpret_cast<uint32_t*>(pab + (long long)x * D) =
-                                        P[k][0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
-                                }
-                            }
-                            const uint32_t in = __shfl_down_sync(FULL, wnd[0], 1);
+                    for (int r = 0; r < NRR; ++r) {
+                        Pv[r] = P[k][r] & 0x01FF01FFu;
+                        Cc[r] = (P[k][r] >> 9) & 0x003F003Fu;
+                    }
+                    M = row_rec<D>(p, lane, Cc, L, M, Ln);
 #pragma unroll
-                            for (int q = 0; q < DPL - 1; ++q) wnd[q] = wnd[q + 1];
-                            wnd[DPL - 1] = lane == ACT - 1 ? e : in;
+                    for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                    if (active) {
+                        if constexpr (DPL == 4) {
+                            const uint32_t s0 = Pv[0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
+                            const uint32_t s1 = Pv[NRR - 1] + __byte_perm(Sx[k], 0u, 0x4342) + Ln[NRR - 1];
+                            *reinterpret_cast<uint2*>(pab + (long long)x * D) =
+                                make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
+                        } else {
+                            *reinterpret_cast<uint32_t*>(pab + (long long)x * D) =
+                                Pv[0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
                         }
                     }
-                };
-                if (fast) body(std::true_type{}); else body(std::false_type{});
-#pragma unroll
-                for (int k = 0; k < SG; ++k) {
-#pragma unroll
-                    for (int r = 0; r < NRR; ++r) P[k][r] = Pn[k][r];
-                    Sx[k] = Sn[k];
                 }
             }
-            clb = clb_n; crb = crb_n;
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+#pragma unroll
+                for (int r = 0; r < NRR; ++r) P[k][r] = Pn[k][r];
+                Sx[k] = Sn[k];
+            }
         }
     }
 }
@@ -899,6 +940,7 @@ static size_t vsmem_bytes(int w, int D, int T, int DC, int np)
     const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
     size_t words = 4 * ((size_t)w + (size_t)T * cstr);
     if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
+    words += (size_t)nw * 16 * DC;                    // K_up output staging
     return words * 4;
 }
 
@@ -1021,7 +1063,11 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         VArgs a{};
         a.p = p; a.w = pl.w; a.cs = pl.cs;
         a.cl = (const uint32_t*)cl; a.cr = (const uint32_t*)cr; a.sig_stride = sig_stride;
-        a.pin = pa; a.pout8 = pa; a.pout16 = pab; a.cell_stride = cell_stride;
+        static const int ablate = getenv("ASD_V2_ABLATE") ? atoi(getenv("ASD_V2_ABLATE")) : 0;
+        a.ablate = ablate;
+        a.pin = reinterpret_cast<const uint16_t*>(pa); a.pouta = reinterpret_cast<uint16_t*>(pa);
+        a.pa_stride = (long long)p.H * pl.cs * pl.w * p.D;
+        a.pout16 = pab; a.cell_stride = cell_stride;
         VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1);
         return launch_vsweep(k, pl, nframes, a, s) == cudaSuccess ? 0 : -1;
     }
