@@ -32,7 +32,7 @@ void launch_lr_depth(const DevParams& p, int nframes, const FrameScratch& fs, lo
 struct V2Plan {
     bool ok;
     int DC, T, NP, cs, w, vthreads, active_ctas;
-    size_t vsmem;
+    size_t vsmem, vsmem_up;
     int DPL, nbuf, bstride;
     size_t rsmem;
     char why[128];

@@ -66,6 +66,27 @@ __device__ __forceinline__ void cluster_arrive()
 {
     asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
+// mbarrier + TMA bulk copy (cp.async.bulk) helpers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar)
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity)
+{
+    asm volatile("{\n .reg .pred P;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+                 " @!P bra WAIT_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 // Relaxed arrive: no implicit release, so the partial-sum stores in flight are
 // not waited for; the warps that wrote DSMEM halos fence first.
 __device__ __forceinline__ void cluster_arrive_relaxed()
@@ -138,6 +159,9 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
 // slice of the right row its DC disparities read (w + DC - 1 words), placed at
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
+constexpr int NSLOT = 6;          // census rows in flight (K_down): rows i+1 .. i+5
+constexpr int KU = 3;             // K_up input rows in flight (TMA bulk ring)
+
 template <int DC, int T>
 struct VGeom {
     static constexpr int NR = DC / 2;
@@ -170,14 +194,19 @@ vsweep_kernel(VArgs a)
     const int sw = G::slot_words(w);
     const bool clustered = NP == 3 && a.cs > 1 && !(a.ablate & 1);
 
-    uint32_t* cens = smem;                   // [4][sw]: left row, then T right-row slices
-    uint32_t* hL = cens + 4 * sw;            // [2][nw][T][NR]   (NP == 3)
+    const int nslot = UP ? 0 : NSLOT;
+    uint32_t* cens = smem;                   // [NSLOT][sw] (K_down): left row, then T right-row slices
+    uint32_t* hL = cens + nslot * sw;        // [2][nw][T][NR]   (NP == 3)
     uint32_t* hR = hL + 2 * nw * T * NR;
     uint32_t* hLM = hR + 2 * nw * T * NR;    // [2][nw]
     uint32_t* hRM = hLM + 2 * nw;
     // K_up output staging: one (CPW columns x D) u16 block per warp, so the
     // global stores of P_AB can be issued as contiguous 512-byte warp stores
-    uint32_t* stg = (NP == 3 ? hRM + 2 * nw : cens + 4 * sw) + warp * (16 * DC);
+    uint32_t* stg0 = NP == 3 ? hRM + 2 * nw : cens + nslot * sw;
+    uint32_t* stg = stg0 + warp * (16 * DC);
+    // K_up input ring: KU rows of this CTA's (w columns x D) u16 block, TMA-loaded
+    uint16_t* ring = reinterpret_cast<uint16_t*>(stg0 + (UP ? nw * 16 * DC : 0));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + (UP ? KU * w * D : 0));
     // K_down -> K_up handoff in a private layout: the warp's (CPW columns x D)
     // block is contiguous and instruction q of lane l covers 16 bytes at
     // 512*q + 16*l, i.e. warp-contiguous stores and loads (row stride cs*w).
@@ -243,17 +272,24 @@ vsweep_kernel(VArgs a)
     };
     const bool xin = x < W;
     // K_up: P_A and C of one row from K_down's packed words (reg k = cells d0+k, d0+NR+k)
-    auto load_pin = [&](int yrow, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
-        const uint4* src = reinterpret_cast<const uint4*>(
-            a.pin + frame * a.pa_stride + ((long long)yrow * wpad + (x - col)) * D) + lane;
+    const unsigned row_bytes = (unsigned)(w * D * 2);
+    auto issue_row = [&](int i) {                    // K_up: TMA the i-th processed row into the ring
+        if (UP && threadIdx.x == 0 && i < H)
+            bulk_g2s(ring + (i % KU) * w * D,
+                     a.pin + frame * a.pa_stride + ((long long)row_of(i) * wpad + x0) * D, row_bytes,
+                     mbar + (i % KU));
+    };
+    auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
+        mbar_wait(mbar + (i % KU), (unsigned)((i / KU) & 1));
+        const uint4* src = reinterpret_cast<const uint4*>(ring + (i % KU) * w * D + (warp * CPW) * D) + lane;
 #pragma unroll
         for (int q = 0; q < NR / 4; ++q) {
-            const uint4 v = __ldg(src + 32 * q);
+            const uint4 v = src[32 * q];
             const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 pa[4 * q + j] = w4[j] & 0x00FF00FFu;
-                c[4 * q + j] = (w4[j] >> 8) & 0x00FF00FFu;
+                c[4 * q + j] = __byte_perm(w4[j], 0u, 0x4341);    // (C_lo, C_hi) as u16x2
             }
         }
     };
@@ -276,13 +312,22 @@ vsweep_kernel(VArgs a)
     uint32_t C[NR];
     uint32_t PA[NR];
 
-    stage(row_of(0), 0);
-    if (H > 1) stage(row_of(1), 1);
-    if (H > 2) stage(row_of(2), 2);
-    cp_async_wait<0>();
+    if (NP == 3 && a.cs > 1 && (a.ablate & 1)) { cluster_arrive(); cluster_wait(); }
+    if (UP) {
+        if (threadIdx.x == 0) {
+            for (int s2 = 0; s2 < KU; ++s2) mbar_init(mbar + s2, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        for (int i0 = 0; i0 < KU; ++i0) issue_row(i0);
+    } else {
+        for (int i0 = 0; i0 < NSLOT - 1; ++i0)
+            if (i0 < H) stage(row_of(i0), i0);
+        cp_async_wait<0>();
+    }
     arrive();
     wait();
-    if (UP) load_pin(row_of(0), PA, C);
+    if (UP) load_pin(0, PA, C);
     else cost(row_of(0), 0, C);
 
     for (int i = 0; i < H; ++i) {
@@ -368,7 +413,7 @@ vsweep_kernel(VArgs a)
             }
         }
         // ---- vertical path: predecessor = own column (after the halo stores)
-        {
+        if (!(a.ablate & 32)) {
             uint32_t Ln[NR], mnew;
             path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
 #pragma unroll
@@ -380,11 +425,14 @@ vsweep_kernel(VArgs a)
             for (int k = 0; k < NR; ++k) Lv[k] = 0u;
             Mv = 0u;
         }
-        // ---- stage row i+3 (async), make row i+2's copies complete, publish
-        if (i + 3 < H) stage(row_of(i + 3), (i + 3) & 3);
-        else cp_async_commit();                      // keep one group per row
-        cp_async_wait<1>();
+        // ---- K_down: stage row i+5 (async), make row i+1's copies complete, publish
+        if (!UP) {
+            if (i + NSLOT - 1 < H) stage(row_of(i + NSLOT - 1), (i + NSLOT - 1) % NSLOT);
+            else cp_async_commit();                  // keep one group per row
+            cp_async_wait<NSLOT - 2>();
+        }
         arrive();
+        issue_row(i + KU);                            // K_up: row i's ring slot is free now
         // ---- partial sum out (after the release so it does not wait on these stores)
         if (!(a.ablate & 2)) {
             uint32_t s[NR];
@@ -429,18 +477,19 @@ vsweep_kernel(VArgs a)
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q) {
                     const int pi = 32 * q + lane;                 // 16-byte piece of the block
-                    if (x - col + (pi * 8) / D < W) dst[pi] = rb[pi];
+                    if (x - col + (pi * 8) / (DC * T) < W) dst[pi] = rb[pi];
                 }
                 __syncwarp();
             }
         }
         // ---- next row's cost while the barrier completes
         if (i + 1 < H) {
-            if (UP) load_pin(row_of(i + 1), PA, C);
-            else cost(row_of(i + 1), (i + 1) & 3, C);
+            if (UP) load_pin(i + 1, PA, C);
+            else cost(row_of(i + 1), (i + 1) % NSLOT, C);
         }
     }
     wait();                                          // pairs with the last arrive
+    if (NP == 3 && a.cs > 1 && (a.ablate & 1)) { cluster_arrive(); cluster_wait(); }
 }
 
 // ---------------------------------------------------------------- K_row
@@ -933,14 +982,14 @@ static RKernel pick_wkernel(int D)
     return nullptr;
 }
 
-static size_t vsmem_bytes(int w, int D, int T, int DC, int np)
+static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up)
 {
     const int nw = w * T / 32;
-    (void)D;
     const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
-    size_t words = 4 * ((size_t)w + (size_t)T * cstr);
+    size_t words = up ? 0 : (size_t)v2::NSLOT * ((size_t)w + (size_t)T * cstr);
     if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
     words += (size_t)nw * 16 * DC;                    // K_up output staging
+    if (up) words += (size_t)v2::KU * w * D / 2 + 2 * v2::KU + 4;   // TMA ring + mbarriers (+ align)
     return words * 4;
 }
 
@@ -982,12 +1031,13 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         const int threads = w * T;
         if (threads > maxt) continue;
         if (np == 1 && cs > 1 && threads < 128) continue;
-        const size_t sm = vsmem_bytes(w, p.D, T, pl.DC, np);
-        if (sm > 200 * 1024) continue;
-        for (VKernel k : {kd, ku}) {
-            cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const size_t smd = vsmem_bytes(w, p.D, T, pl.DC, np, false);
+        const size_t sm = vsmem_bytes(w, p.D, T, pl.DC, np, true);
+        if (sm > 220 * 1024 || smd > 220 * 1024) continue;
+        cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smd);
+        cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        for (VKernel k : {kd, ku})
             if (cs > 8) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        }
         int active = 0;
         if (np == 3 && cs > 1) {
             cudaLaunchConfig_t cfg = {};
@@ -1009,12 +1059,15 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         if (active <= 0) continue;
         // throughput proxy: resident threads, penalising clusters that leave SMs idle
         const double score = (double)active * threads;
-        if (score > best * 1.02) { best = score; pl.cs = cs; pl.w = w; pl.vthreads = threads; pl.vsmem = sm; pl.active_ctas = active; }
+        if (score > best * 1.02) {
+            best = score; pl.cs = cs; pl.w = w; pl.vthreads = threads; pl.vsmem = smd; pl.vsmem_up = sm;
+            pl.active_ctas = active;
+        }
         if (np == 1) break;
     }
     if (best < 0) return no("no feasible cluster configuration");
-    for (VKernel k : {kd, ku})
-        cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+    cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+    cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     if (np == 1) {
         // vertical-only sweeps have no cross-column dependency: 1-CTA strips
         int w = (256 / T + CPW - 1) / CPW * CPW;
@@ -1022,9 +1075,10 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         pl.w = w;
         pl.cs = (p.W + w - 1) / w;
         pl.vthreads = w * T;
-        pl.vsmem = vsmem_bytes(w, p.D, T, pl.DC, np);
-        for (VKernel k : {kd, ku})
-            cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+        pl.vsmem = vsmem_bytes(w, p.D, T, pl.DC, np, false);
+        pl.vsmem_up = vsmem_bytes(w, p.D, T, pl.DC, np, true);
+        cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+        cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     }
     // WTA kernel ring: rows [128t, 128t + 127 + min + D - 1] of stage t must
     // fit beside nothing else; NB > 128 + min + D - 1
@@ -1039,12 +1093,12 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     return true;
 }
 
-static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const VArgs& a, cudaStream_t s)
+static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const VArgs& a, bool up, cudaStream_t s)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.cs, nframes);
     cfg.blockDim = dim3(pl.vthreads);
-    cfg.dynamicSmemBytes = pl.vsmem;
+    cfg.dynamicSmemBytes = up ? pl.vsmem_up : pl.vsmem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1069,7 +1123,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         a.pa_stride = (long long)p.H * pl.cs * pl.w * p.D;
         a.pout16 = pab; a.cell_stride = cell_stride;
         VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1);
-        return launch_vsweep(k, pl, nframes, a, s) == cudaSuccess ? 0 : -1;
+        return launch_vsweep(k, pl, nframes, a, stage == 1, s) == cudaSuccess ? 0 : -1;
     }
     (void)agg;
     RArgs r{};
