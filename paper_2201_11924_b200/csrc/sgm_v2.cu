@@ -968,9 +968,17 @@ wta2_kernel(RArgs a)
         const int x0 = t * WTA_TX;
         const int hi = min(W, x0 + WTA_TX + p.min_disp + D - 1);
         __syncthreads();                              // previous stage done with the ring
-        for (int i = threadIdx.x; i < (hi - loaded) * CH; i += blockDim.x) {
-            const int x = loaded + i / CH, c = i % CH;
-            cp_async8(sbuf + (x % NB) * BS + c * 4, S + (long long)x * D + c * 4);
+        {   // thread t copies 8-byte chunk t % CH of rows loaded + t / CH, + RSTEP, ...
+            constexpr int RSTEP = 32 * WTA_WARPS / CH;
+            const int c = threadIdx.x % CH;
+            int x = loaded + threadIdx.x / CH;
+            int slot = x % NB;
+            const uint16_t* src = S + (long long)x * D + c * 4;
+            for (; x < hi; x += RSTEP, src += RSTEP * D) {
+                cp_async8(sbuf + slot * BS + c * 4, src);
+                slot += RSTEP;
+                if (slot >= NB) slot -= NB;
+            }
         }
         cp_async_commit();
         cp_async_wait<0>();
