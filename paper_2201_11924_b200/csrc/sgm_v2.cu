@@ -222,7 +222,7 @@ vsweep_kernel(VArgs a)
     // census rows -> shared memory with asynchronous copies (one commit group per
     // row).  K_up reads its costs from K_down's packed output instead.
     auto stage = [&](int yrow, int slot) {
-        if (UP) return;
+        if (UP || (a.ablate & 64)) { if (!UP) cp_async_commit(); return; }
         uint32_t* sl = cens + slot * sw;
         const uint32_t* rl = cl + (long long)yrow * W;
         const uint32_t* rr = cr + (long long)yrow * W;
@@ -274,13 +274,13 @@ vsweep_kernel(VArgs a)
     // K_up: P_A and C of one row from K_down's packed words (reg k = cells d0+k, d0+NR+k)
     const unsigned row_bytes = (unsigned)(w * D * 2);
     auto issue_row = [&](int i) {                    // K_up: TMA the i-th processed row into the ring
-        if (UP && threadIdx.x == 0 && i < H)
+        if (UP && threadIdx.x == 0 && i < H && !(a.ablate & 64))
             bulk_g2s(ring + (i % KU) * w * D,
                      a.pin + frame * a.pa_stride + ((long long)row_of(i) * wpad + x0) * D, row_bytes,
                      mbar + (i % KU));
     };
     auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
-        mbar_wait(mbar + (i % KU), (unsigned)((i / KU) & 1));
+        if (!(a.ablate & 64)) mbar_wait(mbar + (i % KU), (unsigned)((i / KU) & 1));
         const uint4* src = reinterpret_cast<const uint4*>(ring + (i % KU) * w * D + (warp * CPW) * D) + lane;
 #pragma unroll
         for (int q = 0; q < NR / 4; ++q) {
@@ -304,6 +304,33 @@ vsweep_kernel(VArgs a)
         }
     };
     auto wait = [&]() { if (clustered) cluster_wait(); };
+
+    // halo write targets of this thread, slot 0 (slot 1 = + hslot / + nw), fixed for the kernel
+    const int hslot = nw * T * NR;
+    uint32_t* wL = nullptr; uint32_t* wLm = nullptr;   // edge lane col == CPW-1 -> column x+1
+    uint32_t* wR = nullptr; uint32_t* wRm = nullptr;   // edge lane col == 0     -> column x-1
+    if (NP == 3) {
+        if (col == CPW - 1) {
+            if (warp + 1 < nw) {
+                wL = hL + ((warp + 1) * T + chunk) * NR;
+                wLm = hLM + warp + 1;
+            } else if (rank + 1 < a.cs) {
+                cg::cluster_group cl_g = cg::this_cluster();
+                wL = cl_g.map_shared_rank(hL + chunk * NR, rank + 1);
+                wLm = cl_g.map_shared_rank(hLM, rank + 1);
+            }
+        }
+        if (col == 0) {
+            if (warp > 0) {
+                wR = hR + ((warp - 1) * T + chunk) * NR;
+                wRm = hRM + warp - 1;
+            } else if (rank > 0) {
+                cg::cluster_group cl_g = cg::this_cluster();
+                wR = cl_g.map_shared_rank(hR + ((nw - 1) * T + chunk) * NR, rank - 1);
+                wRm = cl_g.map_shared_rank(hRM + nw - 1, rank - 1);
+            }
+        }
+    }
 
     uint32_t Lv[NR], Ll[NR], Lr[NR];
 #pragma unroll
@@ -375,41 +402,17 @@ vsweep_kernel(VArgs a)
         // path so the DSMEM stores are in flight while it runs
         if (NP == 3) {
             const int ws = i & 1;
-            if (col == CPW - 1) {            // my "L" state feeds column x+1 next row
-                uint32_t* dst = nullptr;
-                uint32_t* dstm = nullptr;
-                if (warp + 1 < nw) {
-                    dst = hL + ((ws * nw + warp + 1) * T + chunk) * NR;
-                    dstm = hLM + ws * nw + warp + 1;
-                } else if (rank + 1 < a.cs) {
-                    cg::cluster_group cl_g = cg::this_cluster();
-                    dst = cl_g.map_shared_rank(hL + ((ws * nw + 0) * T + chunk) * NR, rank + 1);
-                    dstm = cl_g.map_shared_rank(hLM + ws * nw + 0, rank + 1);
-                }
-                if (dst) {
-                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+            if (wL) {                        // my "L" state feeds column x+1 next row
+                uint4* d4 = reinterpret_cast<uint4*>(wL + ws * hslot);
 #pragma unroll
-                    for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]);
-                    if (chunk == 0) *dstm = Ml;
-                }
+                for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]);
+                if (chunk == 0) wLm[ws * nw] = Ml;
             }
-            if (col == 0) {                  // my "R" state feeds column x-1 next row
-                uint32_t* dst = nullptr;
-                uint32_t* dstm = nullptr;
-                if (warp > 0) {
-                    dst = hR + ((ws * nw + warp - 1) * T + chunk) * NR;
-                    dstm = hRM + ws * nw + warp - 1;
-                } else if (rank > 0) {
-                    cg::cluster_group cl_g = cg::this_cluster();
-                    dst = cl_g.map_shared_rank(hR + ((ws * nw + nw - 1) * T + chunk) * NR, rank - 1);
-                    dstm = cl_g.map_shared_rank(hRM + ws * nw + nw - 1, rank - 1);
-                }
-                if (dst) {
-                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+            if (wR) {                        // my "R" state feeds column x-1 next row
+                uint4* d4 = reinterpret_cast<uint4*>(wR + ws * hslot);
 #pragma unroll
-                    for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
-                    if (chunk == 0) *dstm = Mr;
-                }
+                for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
+                if (chunk == 0) wRm[ws * nw] = Mr;
             }
         }
         // ---- vertical path: predecessor = own column (after the halo stores)
