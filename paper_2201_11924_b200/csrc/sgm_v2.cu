@@ -138,7 +138,6 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
         if (chunk > 0) qprev = u;
         if (chunk < T - 1) qnext = v;
     }
-    uint32_t macc = 0xFFFFFFFFu;
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
         const uint32_t dm1 = k > 0 ? Q[k - 1] : __byte_perm(qprev, Q[NR - 1], 0x5432);
@@ -146,8 +145,18 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
         uint32_t t = vmin2(vmin2(dm1, dp1), P[k]);
         t = vmin2(t, MP2);
         Ln[k] = t + C[k] - Mp;
-        macc = vmin2(macc, Ln[k]);
     }
+    // min over the NR registers as a balanced tree (the asm min is opaque to the
+    // compiler, so a running min would be a serial chain of NR dependent ops)
+    uint32_t tr[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) tr[k] = Ln[k];
+#pragma unroll
+    for (int h = NR / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int k = 0; k < h; ++k) tr[k] = vmin2(tr[k], tr[k + h]);
+    }
+    const uint32_t macc = tr[0];
     uint32_t m = vmin2(macc, __byte_perm(macc, macc, 0x1032));      // (min, min)
 #pragma unroll
     for (int o = 1; o < T; o <<= 1) m = vmin2(m, __shfl_xor_sync(FULL, m, o));
