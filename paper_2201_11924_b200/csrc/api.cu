@@ -166,13 +166,14 @@ struct Layout {
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
-Layout layout(const DevParams& d, int max_batch, int engine)
+// pa_cols: columns of a P_A row (D3 pads it to the sweep grid, cs*w >= W).
+Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
 {
     Layout L{};
     const size_t B = (size_t)max_batch;
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
     L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
-    L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;     // P_A | C << 8, u16
+    L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.H * pa_cols * d.D * 2) : 0;   // P_A | C << 8, u16
     L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
     L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
     L.px_f32 = align_up(B * d.npx * 4);
@@ -364,10 +365,10 @@ size_t asd_scratch_bytes(const asd_params* p, int max_batch)
         int dev = 0;
         cudaGetDevice(&dev);
         V2Plan pl;
-        if (v2_plan(d, dev, pl)) engine = ASD_ENGINE_D3;
+        if (v2_plan(d, dev, pl)) return layout(d, max_batch, ASD_ENGINE_D3, pl.cs * pl.w).total;
         cudaGetLastError();
     }
-    return layout(d, max_batch, engine).total;
+    return layout(d, max_batch, engine, d.W).total;
 }
 
 int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
@@ -402,12 +403,8 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
             return ASD_E_UNSUPPORTED;
         }
     }
-    Layout L = layout(c->dp, max_batch, c->engine);
-    if (c->engine == ASD_ENGINE_D3) {           // P_A rows are padded to the sweep grid (cs*w columns)
-        const size_t padded = align_up((size_t)max_batch * c->dp.H * c->plan.cs * c->plan.w * c->dp.D * 2);
-        L.total += padded - L.pa;
-        L.pa = padded;
-    }
+    Layout L = layout(c->dp, max_batch, c->engine,
+                      c->engine == ASD_ENGINE_D3 ? c->plan.cs * c->plan.w : c->dp.W);
     bool ok = true;
     auto alloc = [&](void** q, size_t bytes) {
         if (ok && cudaMalloc(q, bytes) != cudaSuccess) ok = false;
