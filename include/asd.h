@@ -189,7 +189,7 @@ int asd_frames_per_wave(const asd_ctx* ctx);
  * CTA shape, residency), NUL-terminated into buf[0..n).  Returns its length. */
 int asd_plan_info(const asd_ctx* ctx, char* buf, int n);
 
-/* ---- live stage timing (CUDA events on the caller's stream) ----
+/* ---- live stage timing (CUDA events on the launching stream) ----
  * asd_profile_begin(ctx, max_launches) pre-creates events for up to
  * max_launches kernel launches; from then on every launch the context enqueues
  * is bracketed by an event pair on the launching stream (no host sync).
@@ -218,6 +218,14 @@ typedef struct asd_stage_times {
 
 int asd_profile_begin(asd_ctx* ctx, int max_launches);
 int asd_profile_end(asd_ctx* ctx, asd_stage_times* out);
+
+/* Per-launch timeline of the launches recorded since asd_profile_begin (call
+ * it BEFORE asd_profile_end, which discards them): synchronises on the events
+ * and writes, for up to max launches in enqueue order, the stage id and the
+ * start/end time in ms relative to the first launch's start.  Host arrays of
+ * max elements, owned by the caller.  Returns the number written, or a
+ * negative ASD_E_* code. */
+int asd_profile_timeline(asd_ctx* ctx, int max, int32_t* stage, float* t_start_ms, float* t_end_ms);
 
 /* Static strings; never NULL. */
 const char* asd_strerror(int code);

@@ -75,6 +75,8 @@ SYMBOLS = [
     ("asd_plan_info", _I, [_VP, ctypes.c_char_p, _I]),
     ("asd_profile_begin", _I, [_VP, _I]),
     ("asd_profile_end", _I, [_VP, ctypes.POINTER(asd_stage_times)]),
+    ("asd_profile_timeline", _I, [_VP, _I, ctypes.POINTER(ctypes.c_int32),
+                                  ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     ("asd_strerror", ctypes.c_char_p, [_I]),
     ("asd_last_error", ctypes.c_char_p, [_VP]),
 ]
@@ -205,6 +207,16 @@ class Stereo:
         return {name: {"ms": t.ms[i], "alg_bytes": t.alg_bytes[i], "alg_ops": t.alg_ops[i],
                        "launches": t.launches[i]}
                 for i, name in enumerate(STAGES)} | {"dropped": t.dropped}
+
+    def profile_timeline(self, max_launches: int = 65536) -> list:
+        """[(stage name, start ms, end ms)] per launch since profile_begin, in
+        enqueue order (call before profile_end)."""
+        st = (ctypes.c_int32 * max_launches)()
+        a = (ctypes.c_float * max_launches)()
+        b = (ctypes.c_float * max_launches)()
+        k = self._lib.asd_profile_timeline(self._ctx, max_launches, st, a, b)
+        _check(min(k, 0), self._ctx)
+        return [(STAGES[st[i]], a[i], b[i]) for i in range(k)]
 
     @property
     def engine(self) -> int:

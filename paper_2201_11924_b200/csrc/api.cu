@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -52,6 +53,13 @@ struct asd_ctx {
     cudaEvent_t ev_in[2] = {nullptr, nullptr};
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
     cudaEvent_t ev_comp[2] = {nullptr, nullptr};
+    // D3 overlap: the cluster sweeps of group g+1 run on s_hi (high priority)
+    // while the row pass and WTA of group g run on s_lo on the SMs the sweep
+    // clusters leave free; fork from / join back to the caller's stream.
+    cudaStream_t s_hi = nullptr, s_lo = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_sw = nullptr, ev_hi = nullptr, ev_lo = nullptr;
+    int group = 0;                // frames per overlap group (D3)
+    std::vector<cudaEvent_t> ev_free;   // one per scratch slot (max_batch / group)
     // live stage timing (asd_profile_begin/end)
     struct Mark { int stage; double bytes; double ops; };
     bool prof = false;
@@ -244,11 +252,105 @@ static double alg_ops_up(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2
 static double alg_ops_row(const DevParams& p) { return 2 * 2.5 * p.ncell + 2.5 * p.ncell + 2.0 * p.ncell; }
 static double alg_ops_wta3(const DevParams& p) { return 3.0 * p.ncell; }
 
-// Enqueue the whole path for n <= max_batch frames resident on the device.
+// Design D3: the whole path for any n frames resident on the device, as a
+// software pipeline over groups of G frames (one wave of sweep clusters) and a
+// ring of max_batch / G scratch slots.  Group g: census + down + up sweeps on
+// s_hi (high priority; the cluster kernels occupy cs * (clusters per wave)
+// SMs), then row + WTA + LR on s_lo, which fill the SMs the clusters leave
+// free while the sweeps of group g + 1 run.  ev_free[slot] orders the reuse of
+// a slot after the LR pass of the group that last used it.
+int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
+           float* out_disp, float* out_depth, asd_frame_stats* stats,
+           uint8_t* mask_out, cudaStream_t s, uint16_t* agg_debug)
+{
+    const DevParams& p = c->dp;
+    if (n <= 0) return ASD_OK;
+    const long long npx = p.npx;
+    const FrameScratch fs = frame_scratch(c);
+    const int G = c->group;
+    const int nslots = (int)c->ev_free.size();
+    const long long pa_frame = (long long)p.H * c->plan.cs * c->plan.w * p.D;   // u16 elements
+    cudaEventRecord(c->ev_fork, s);                    // inputs (and outputs) are ordered on s
+    cudaStreamWaitEvent(c->s_hi, c->ev_fork, 0);
+    cudaStreamWaitEvent(c->s_lo, c->ev_fork, 0);
+    for (int gi = 0, f0 = 0; f0 < n; ++gi, f0 += G) {
+        const int m = (n - f0) < G ? (n - f0) : G;
+        const int slot = gi % nslots;
+        const long long b0 = (long long)slot * G;       // first scratch frame of the slot
+        void* cl = (char*)c->census_l + b0 * npx * (long long)c->sig_bytes;
+        void* cr = (char*)c->census_r + b0 * npx * (long long)c->sig_bytes;
+        uint8_t* pa = c->pa + b0 * pa_frame * 2;
+        uint16_t* pab = c->pab + b0 * p.ncell;
+        uint8_t* stash = c->stash + b0 * p.ncell;
+        FrameScratch g = fs;
+        g.census_l = cl; g.census_r = cr;
+        g.dl += b0 * npx; g.dr += b0 * npx; g.dstar_l += b0 * npx; g.dstar_r += b0 * npx;
+        g.mask_l += b0 * npx; g.mask_r += b0 * npx;
+        if (gi >= nslots) cudaStreamWaitEvent(c->s_hi, c->ev_free[slot], 0);
+        {
+            ProfScope ps(c, c->s_hi, ASD_STAGE_CENSUS, m * alg_bytes_census(p, c->sig_bytes));
+            launch_census(p, m, left + f0 * npx, right + f0 * npx, npx, cl, cr, npx, c->s_hi);
+        }
+        {
+            ProfScope ps(c, c->s_hi, ASD_STAGE_DOWN, m * alg_bytes_down(p), m * alg_ops_sweep(p));
+            if (launch_v2_stage(0, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx,
+                                nullptr, c->s_hi) != 0) {
+                set_err(c, "down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return ASD_E_CUDA;
+            }
+        }
+        {
+            ProfScope ps(c, c->s_hi, ASD_STAGE_UP, m * alg_bytes_up(p), m * alg_ops_up(p));
+            if (launch_v2_stage(1, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx,
+                                nullptr, c->s_hi) != 0) {
+                set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return ASD_E_CUDA;
+            }
+        }
+        cudaEventRecord(c->ev_sw, c->s_hi);
+        cudaStreamWaitEvent(c->s_lo, c->ev_sw, 0);
+        {
+            ProfScope ps(c, c->s_lo, ASD_STAGE_ROW, m * alg_bytes_row(p), m * alg_ops_row(p));
+            launch_v2_stage(2, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx, nullptr, c->s_lo);
+        }
+        if (agg_debug && f0 == 0)            // S of frame 0 (natural order) before the WTA
+            cudaMemcpyAsync(agg_debug, pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, c->s_lo);
+        {
+            ProfScope ps(c, c->s_lo, ASD_STAGE_WTA, m * alg_bytes_wta3(p), m * alg_ops_wta3(p));
+            if (launch_v2_stage(3, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx,
+                                nullptr, c->s_lo) != 0) {
+                set_err(c, "WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return ASD_E_CUDA;
+            }
+        }
+        if (stats) cudaMemsetAsync(stats + f0, 0, sizeof(asd_frame_stats) * m, c->s_lo);
+        {
+            ProfScope ps(c, c->s_lo, ASD_STAGE_LR, m * alg_bytes_lr(p));
+            launch_lr_depth(p, m, g, npx, out_disp ? out_disp + f0 * npx : nullptr,
+                            out_depth ? out_depth + f0 * npx : nullptr, npx,
+                            mask_out ? mask_out + f0 * npx : nullptr, stats ? stats + f0 : nullptr, c->s_lo);
+        }
+        cudaEventRecord(c->ev_free[slot], c->s_lo);
+    }
+    cudaEventRecord(c->ev_hi, c->s_hi);              // join back to the caller's stream
+    cudaEventRecord(c->ev_lo, c->s_lo);
+    cudaStreamWaitEvent(s, c->ev_hi, 0);
+    cudaStreamWaitEvent(s, c->ev_lo, 0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_err(c, "CUDA launch failed: %s", cudaGetErrorString(e));
+        return ASD_E_CUDA;
+    }
+    return ASD_OK;
+}
+
+// Design D1: the whole path for n <= max_batch frames resident on the device.
 int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
               float* out_disp, float* out_depth, asd_frame_stats* stats,
               uint8_t* mask_out, cudaStream_t s, uint16_t* agg_debug = nullptr)
 {
+    if (c->engine == ASD_ENGINE_D3)
+        return run_d3(c, n, left, right, out_disp, out_depth, stats, mask_out, s, agg_debug);
     const DevParams& p = c->dp;
     if (n <= 0) return ASD_OK;
     const long long npx = p.npx;
@@ -257,39 +359,6 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         launch_census(p, n, left, right, npx, c->census_l, c->census_r, npx, s);
     }
     FrameScratch fs = frame_scratch(c);
-    if (c->engine == ASD_ENGINE_D3) {
-        {
-            ProfScope ps(c, s, ASD_STAGE_DOWN, n * alg_bytes_down(p), n * alg_ops_sweep(p));
-            if (launch_v2_stage(0, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
-                                p.ncell, fs, npx, nullptr, s) != 0) {
-                set_err(c, "down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-                return ASD_E_CUDA;
-            }
-        }
-        {
-            ProfScope ps(c, s, ASD_STAGE_UP, n * alg_bytes_up(p), n * alg_ops_up(p));
-            if (launch_v2_stage(1, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
-                                p.ncell, fs, npx, nullptr, s) != 0) {
-                set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-                return ASD_E_CUDA;
-            }
-        }
-        {
-            ProfScope ps(c, s, ASD_STAGE_ROW, n * alg_bytes_row(p), n * alg_ops_row(p));
-            launch_v2_stage(2, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
-                            p.ncell, fs, npx, nullptr, s);
-        }
-        if (agg_debug)                       // S of frame 0 (natural order) before the WTA
-            cudaMemcpyAsync(agg_debug, c->pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, s);
-        {
-            ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta3(p), n * alg_ops_wta3(p));
-            if (launch_v2_stage(3, p, c->plan, n, c->census_l, c->census_r, npx, c->pa, c->pab, c->stash,
-                                p.ncell, fs, npx, nullptr, s) != 0) {
-                set_err(c, "WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-                return ASD_E_CUDA;
-            }
-        }
-    }
     for (int r = 0; c->engine == ASD_ENGINE_D1 && r < p.paths; ++r) {
         ProfScope ps(c, s, ASD_STAGE_DIR, n * alg_bytes_dir(p, r == 0));
         if (!launch_sgm_dir(p, n, kDirs[r][0], kDirs[r][1], r == 0, c->census_l, c->census_r, npx,
@@ -331,6 +400,9 @@ void free_ctx(asd_ctx* c)
         if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (cudaStream_t q : {c->s_hi, c->s_lo}) if (q) cudaStreamDestroy(q);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_sw, c->ev_hi, c->ev_lo}) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_free) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     delete c;
 }
@@ -429,6 +501,23 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         return ASD_E_OOM;
     }
     if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) ok = false;
+    {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (ok && (cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi) != cudaSuccess ||
+                   cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo) != cudaSuccess))
+            ok = false;
+        for (cudaEvent_t* e : {&c->ev_fork, &c->ev_sw, &c->ev_hi, &c->ev_lo})
+            if (ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) ok = false;
+        // overlap group: one wave of sweep clusters (env ASD_GROUP overrides), at
+        // most max_batch; max_batch / group scratch slots
+        c->group = c->plan.cs > 0 ? c->plan.active_ctas / c->plan.cs : 1;
+        if (const char* g = getenv("ASD_GROUP")) c->group = atoi(g);
+        if (c->group < 1 || c->group > max_batch) c->group = max_batch;
+        c->ev_free.assign(c->engine == ASD_ENGINE_D3 ? max_batch / c->group : 0, nullptr);
+        for (cudaEvent_t& e : c->ev_free)
+            if (ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) ok = false;
+    }
     for (int i = 0; i < 2 && ok; ++i)
         if (cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -454,7 +543,8 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 {
     if (!ctx || n <= 0) return 0;
     const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
-    return chunks * (ctx->engine == ASD_ENGINE_D3 ? 6 : 3 + ctx->dp.paths);
+    if (ctx->engine != ASD_ENGINE_D3) return chunks * (3 + ctx->dp.paths);
+    return 6 * ((n + ctx->group - 1) / ctx->group);   // per group: census, down, up, row, WTA, LR
 }
 
 int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }
@@ -489,6 +579,8 @@ int asd_depth_batch(asd_ctx* ctx, int n, const uint8_t* left, const uint8_t* rig
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const long long npx = ctx->dp.npx;
+    if (ctx->engine == ASD_ENGINE_D3)               // pipelined over scratch slots, any n
+        return run_d3(ctx, n, left, right, out_disp, out_depth, stats, nullptr, s, nullptr);
     for (int f0 = 0; f0 < n; f0 += ctx->max_batch) {
         const int m = (n - f0) < ctx->max_batch ? (n - f0) : ctx->max_batch;
         int rc = run_chunk(ctx, m, left + f0 * npx, right + f0 * npx,
@@ -611,6 +703,29 @@ int asd_profile_begin(asd_ctx* ctx, int max_launches)
     ctx->prof_dropped = 0;
     ctx->prof = true;
     return ASD_OK;
+}
+
+int asd_profile_timeline(asd_ctx* ctx, int max, int32_t* stage, float* t_start_ms, float* t_end_ms)
+{
+    if (!ctx || max < 0 || (max > 0 && (!stage || !t_start_ms || !t_end_ms))) {
+        set_err(ctx, "asd_profile_timeline: bad arguments");
+        return ASD_E_INVALID_ARG;
+    }
+    DeviceGuard g(ctx->device);
+    const int k = (int)ctx->prof_marks.size() < max ? (int)ctx->prof_marks.size() : max;
+    for (int i = 0; i < k; ++i) {
+        float a = 0.0f, b = 0.0f;
+        if (cudaEventSynchronize(ctx->prof_ev[2 * i + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&a, ctx->prof_ev[0], ctx->prof_ev[2 * i]) != cudaSuccess ||
+            cudaEventElapsedTime(&b, ctx->prof_ev[0], ctx->prof_ev[2 * i + 1]) != cudaSuccess) {
+            set_err(ctx, "event timing failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return ASD_E_CUDA;
+        }
+        stage[i] = ctx->prof_marks[i].stage;
+        t_start_ms[i] = a;
+        t_end_ms[i] = b;
+    }
+    return k;
 }
 
 int asd_profile_end(asd_ctx* ctx, asd_stage_times* out)

@@ -15,6 +15,7 @@ ap.add_argument("--frames", type=int, default=32)
 ap.add_argument("--max-batch", type=int, default=0)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--timeline", action="store_true", help="print the per-launch timeline")
 args = ap.parse_args()
 cfg = synth.CONFIGS[args.config]
 d = cfg.params_dict()
@@ -35,14 +36,21 @@ print(st.plan_info)
 st.asd_depth_batch(L, R, out, out)
 torch.cuda.synchronize()
 st.profile_begin(4096)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
 for _ in range(args.reps):
     st.asd_depth_batch(L, R, out, out)
+e1.record()
 torch.cuda.synchronize()
+wall = e0.elapsed_time(e1)
+tl = st.profile_timeline(4096) if args.timeline else []
 prof = st.profile_end()
 n = args.frames * args.reps
 tot = sum(prof[k]["ms"] for k in asd.abi.STAGES)
-print(f"config {args.config} paths {d['paths']} engine {st.engine}: {1000 * tot / n:.1f} us/frame, "
-      f"{n / (tot / 1000):.0f} frames/s (sum of stages)")
+print(f"config {args.config} paths {d['paths']} engine {st.engine}: {1000 * tot / n:.1f} us/frame "
+      f"sum of stages, {1000 * wall / n:.1f} us/frame wall, {n / (wall / 1000):.0f} frames/s")
+for name, a, b in tl:
+    print(f"  {name:7s} {a:9.3f} {b:9.3f}  {b - a:7.3f} ms")
 for k in asd.abi.STAGES:
     if prof[k]["launches"]:
         us = 1000 * prof[k]["ms"] / n
