@@ -34,6 +34,7 @@ METRIC = "frames/s and Gcell/s (W·H·D) at 1280×720×D128 8-path; HBM GB/s vs 
 CONFIG = "C"
 FRAMES_PER_STEP = 128          # inputs 128 x 2 x 0.92 MB = 236 MB per step > 126 MB L2
 POOL = 8                       # distinct synthetic frames (kernels are data-oblivious)
+CRITICAL = ("census", "down", "up")   # D3 stages on the high-priority (critical) stream
 MAX_BATCH = 32                 # frames in flight per asd_depth_batch chunk
 
 
@@ -263,6 +264,7 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
     ms = e0.elapsed_time(e1)
+    timeline = st.profile_timeline(lp * args.steps + 16)
     prof = st.profile_end()
     ms_max = max_over_ranks(ms, dev)
     frames_total = world * B * args.steps
@@ -302,7 +304,12 @@ def main():
         sm_mhz = pk.get("sm_max_mhz", 1965.0) if pk else 1965.0
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         alu_peak = nsm * 128 * sm_mhz * 1e6 / 1e12       # T int lane-ops/s
-        top = max(asd.abi.STAGES, key=lambda k: prof[k]["ms"])
+        # Dominant kernel: D3 runs the cluster sweeps (and the census feeding
+        # them) back to back on a high-priority stream -- the step's critical
+        # path -- while row/WTA/LR fill the SMs the clusters leave free, so their
+        # event durations include waiting for SMs; D1 runs serially.
+        crit = CRITICAL if st.engine == 3 else asd.abi.STAGES
+        top = max(crit, key=lambda k: prof[k]["ms"])
         tp = prof[top]
         nl = max(1, tp["launches"])
         avg_ms = tp["ms"] / nl
@@ -318,7 +325,7 @@ def main():
             try:
                 per_frame = json.load(open(tpath)).get(top)
                 if per_frame is not None:
-                    traffic = per_frame * min(args.max_batch, B)
+                    traffic = per_frame * (st.group if st.engine == 3 else min(args.max_batch, B))
             except Exception:
                 traffic = None
         if alg_o > 0:
@@ -336,6 +343,24 @@ def main():
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md"}
         roof.update({"kernel": KERNEL_NAMES[top], "alg_bytes_per_launch": alg_b,
                      "avg_launch_ms": round(avg_ms, 4), "launches": nl})
+        # share of the timed region the critical (sweep) stream is busy
+        pipeline = None
+        if timeline and st.engine == 3:
+            iv = sorted((a, b) for k, a, b in timeline if k in CRITICAL)
+            busy, cur0, cur1 = 0.0, None, None
+            for a, b in iv:
+                if cur1 is None or a > cur1:
+                    if cur1 is not None:
+                        busy += cur1 - cur0
+                    cur0, cur1 = a, b
+                else:
+                    cur1 = max(cur1, b)
+            if cur1 is not None:
+                busy += cur1 - cur0
+            span = max(b for _, _, b in timeline) - min(a for _, a, _ in timeline)
+            pipeline = {"group_frames": st.group, "critical_stages": list(CRITICAL),
+                        "critical_stream_busy": round(busy / max(1e-9, span), 4),
+                        "note": "stage_ms are per-kernel event sums; row/wta/lr overlap the sweeps"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, pool_L, pool_R)
@@ -354,6 +379,7 @@ def main():
             "roofline": roof,
             "stage_ms": {k: round(prof[k]["ms"], 3) for k in asd.abi.STAGES if prof[k]["launches"]},
             "stage_share": stage_share,
+            "pipeline": pipeline,
             "clocks": clk.summary(),
             "gpu_launches": lp * args.steps,
             "checksum_frames": int(len(st_all)),

@@ -185,6 +185,15 @@ int asd_engine(const asd_ctx* ctx);
  * Choosing max_batch as a multiple of it avoids a partial last wave. */
 int asd_frames_per_wave(const asd_ctx* ctx);
 
+/* D3 pipeline: a batch runs as groups of `group` frames over
+ * max_batch / group scratch slots; the cluster sweeps of one group overlap the
+ * row/WTA/LR passes of the previous one on the SMs the clusters leave free.
+ * Default: one wave (asd_frames_per_wave, capped at max_batch).  group must be
+ * in [1, max_batch]; asd_set_group synchronises the device first.  Returns
+ * ASD_OK or ASD_E_INVALID_ARG / ASD_E_CUDA.  D1 ignores it. */
+int asd_set_group(asd_ctx* ctx, int group);
+int asd_group(const asd_ctx* ctx);
+
 /* Human-readable description of the chosen kernel geometry (cluster size,
  * CTA shape, residency), NUL-terminated into buf[0..n).  Returns its length. */
 int asd_plan_info(const asd_ctx* ctx, char* buf, int n);

@@ -70,6 +70,8 @@ SYMBOLS = [
     ("asd_depth_batch_host", _I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     ("asd_depth_debug", _I, [_VP, _VP, _VP, ctypes.POINTER(asd_debug_out), _VP, _VP, _VP]),
     ("asd_launches_per_batch", _I, [_VP, _I]),
+    ("asd_set_group", _I, [_VP, _I]),
+    ("asd_group", _I, [_VP]),
     ("asd_engine", _I, [_VP]),
     ("asd_frames_per_wave", _I, [_VP]),
     ("asd_plan_info", _I, [_VP, ctypes.c_char_p, _I]),
@@ -217,6 +219,15 @@ class Stereo:
         k = self._lib.asd_profile_timeline(self._ctx, max_launches, st, a, b)
         _check(min(k, 0), self._ctx)
         return [(STAGES[st[i]], a[i], b[i]) for i in range(k)]
+
+    @property
+    def group(self) -> int:
+        """Frames per D3 pipeline group (asd_set_group)."""
+        return int(self._lib.asd_group(self._ctx))
+
+    @group.setter
+    def group(self, g: int):
+        _check(self._lib.asd_set_group(self._ctx, int(g)), self._ctx)
 
     @property
     def engine(self) -> int:

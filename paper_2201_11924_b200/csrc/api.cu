@@ -56,8 +56,8 @@ struct asd_ctx {
     // D3 overlap: the cluster sweeps of group g+1 run on s_hi (high priority)
     // while the row pass and WTA of group g run on s_lo on the SMs the sweep
     // clusters leave free; fork from / join back to the caller's stream.
-    cudaStream_t s_hi = nullptr, s_lo = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_sw = nullptr, ev_hi = nullptr, ev_lo = nullptr;
+    cudaStream_t s_hi = nullptr, s_lo = nullptr, s_cen = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_sw = nullptr, ev_hi = nullptr, ev_lo = nullptr, ev_cen = nullptr;
     int group = 0;                // frames per overlap group (D3)
     std::vector<cudaEvent_t> ev_free;   // one per scratch slot (max_batch / group)
     // live stage timing (asd_profile_begin/end)
@@ -252,13 +252,33 @@ static double alg_ops_up(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2
 static double alg_ops_row(const DevParams& p) { return 2 * 2.5 * p.ncell + 2.5 * p.ncell + 2.0 * p.ncell; }
 static double alg_ops_wta3(const DevParams& p) { return 3.0 * p.ncell; }
 
+// Frames per D3 pipeline group; max_batch / group scratch slots, one
+// slot-free event each.
+int set_group(asd_ctx* c, int group)
+{
+    if (group < 1 || group > c->max_batch) return ASD_E_INVALID_ARG;
+    for (cudaEvent_t e : c->ev_free) if (e) cudaEventDestroy(e);
+    c->ev_free.assign(c->engine == ASD_ENGINE_D3 ? c->max_batch / group : 0, nullptr);
+    for (cudaEvent_t& e : c->ev_free)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return ASD_E_CUDA;
+    c->group = group;
+    return ASD_OK;
+}
+
 // Design D3: the whole path for any n frames resident on the device, as a
 // software pipeline over groups of G frames (one wave of sweep clusters) and a
-// ring of max_batch / G scratch slots.  Group g: census + down + up sweeps on
-// s_hi (high priority; the cluster kernels occupy cs * (clusters per wave)
-// SMs), then row + WTA + LR on s_lo, which fill the SMs the clusters leave
-// free while the sweeps of group g + 1 run.  ev_free[slot] orders the reuse of
-// a slot after the LR pass of the group that last used it.
+// ring of max_batch / G scratch slots, on three streams forked from the
+// caller's:
+//   s_cen (high priority): census of group g, once its slot is free;
+//   s_hi  (high priority): down + up sweeps of group g (the cluster kernels
+//                          occupy cs * clusters-per-wave SMs);
+//   s_lo  (low priority):  row + WTA + LR of group g, which fill the SMs the
+//                          clusters leave free while group g + 1 sweeps.
+// The census of group g + 1 is enqueued ahead, so when the up sweep of group
+// g ends the down sweep of g + 1 and the row pass of g become ready together
+// and the stream priorities hand the freed SMs to the clusters first.
+// ev_free[slot] orders the reuse of a slot after the LR pass of the group that
+// last used it.
 int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
            float* out_disp, float* out_depth, asd_frame_stats* stats,
            uint8_t* mask_out, cudaStream_t s, uint16_t* agg_debug)
@@ -269,39 +289,56 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
     const FrameScratch fs = frame_scratch(c);
     const int G = c->group;
     const int nslots = (int)c->ev_free.size();
+    const int ngroups = (n + G - 1) / G;
     const long long pa_frame = (long long)p.H * c->plan.cs * c->plan.w * p.D;   // u16 elements
-    cudaEventRecord(c->ev_fork, s);                    // inputs (and outputs) are ordered on s
-    cudaStreamWaitEvent(c->s_hi, c->ev_fork, 0);
-    cudaStreamWaitEvent(c->s_lo, c->ev_fork, 0);
-    for (int gi = 0, f0 = 0; f0 < n; ++gi, f0 += G) {
-        const int m = (n - f0) < G ? (n - f0) : G;
-        const int slot = gi % nslots;
-        const long long b0 = (long long)slot * G;       // first scratch frame of the slot
-        void* cl = (char*)c->census_l + b0 * npx * (long long)c->sig_bytes;
-        void* cr = (char*)c->census_r + b0 * npx * (long long)c->sig_bytes;
-        uint8_t* pa = c->pa + b0 * pa_frame * 2;
-        uint16_t* pab = c->pab + b0 * p.ncell;
-        uint8_t* stash = c->stash + b0 * p.ncell;
-        FrameScratch g = fs;
-        g.census_l = cl; g.census_r = cr;
-        g.dl += b0 * npx; g.dr += b0 * npx; g.dstar_l += b0 * npx; g.dstar_r += b0 * npx;
-        g.mask_l += b0 * npx; g.mask_r += b0 * npx;
-        if (gi >= nslots) cudaStreamWaitEvent(c->s_hi, c->ev_free[slot], 0);
+    struct Slot { void* cl; void* cr; uint8_t* pa; uint16_t* pab; uint8_t* stash; FrameScratch g; };
+    auto slot_of = [&](int gi) {
+        const long long b0 = (long long)(gi % nslots) * G;   // first scratch frame of the slot
+        Slot q;
+        q.cl = (char*)c->census_l + b0 * npx * (long long)c->sig_bytes;
+        q.cr = (char*)c->census_r + b0 * npx * (long long)c->sig_bytes;
+        q.pa = c->pa + b0 * pa_frame * 2;
+        q.pab = c->pab + b0 * p.ncell;
+        q.stash = c->stash + b0 * p.ncell;
+        q.g = fs;
+        q.g.census_l = q.cl; q.g.census_r = q.cr;
+        q.g.dl += b0 * npx; q.g.dr += b0 * npx; q.g.dstar_l += b0 * npx; q.g.dstar_r += b0 * npx;
+        q.g.mask_l += b0 * npx; q.g.mask_r += b0 * npx;
+        return q;
+    };
+    auto frames = [&](int gi) { return (n - gi * G) < G ? (n - gi * G) : G; };
+    auto census = [&](int gi) {
+        const Slot q = slot_of(gi);
+        const int m = frames(gi);
+        const long long f0 = (long long)gi * G;
+        if (gi >= nslots) cudaStreamWaitEvent(c->s_cen, c->ev_free[gi % nslots], 0);
         {
-            ProfScope ps(c, c->s_hi, ASD_STAGE_CENSUS, m * alg_bytes_census(p, c->sig_bytes));
-            launch_census(p, m, left + f0 * npx, right + f0 * npx, npx, cl, cr, npx, c->s_hi);
+            ProfScope ps(c, c->s_cen, ASD_STAGE_CENSUS, m * alg_bytes_census(p, c->sig_bytes));
+            launch_census(p, m, left + f0 * npx, right + f0 * npx, npx, q.cl, q.cr, npx, c->s_cen);
         }
+        cudaEventRecord(c->ev_cen, c->s_cen);
+    };
+    cudaEventRecord(c->ev_fork, s);                    // inputs (and outputs) are ordered on s
+    for (cudaStream_t q : {c->s_cen, c->s_hi, c->s_lo}) cudaStreamWaitEvent(q, c->ev_fork, 0);
+    census(0);
+    for (int gi = 0; gi < ngroups; ++gi) {
+        const Slot q = slot_of(gi);
+        const int m = frames(gi);
+        const long long f0 = (long long)gi * G;
+        cudaStreamWaitEvent(c->s_hi, c->ev_cen, 0);   // census of this group (and so its slot) ready
         {
             ProfScope ps(c, c->s_hi, ASD_STAGE_DOWN, m * alg_bytes_down(p), m * alg_ops_sweep(p));
-            if (launch_v2_stage(0, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx,
+            if (launch_v2_stage(0, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
                                 nullptr, c->s_hi) != 0) {
                 set_err(c, "down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                 return ASD_E_CUDA;
             }
         }
+        // with a single slot the next census must wait for this group's LR
+        if (gi + 1 < ngroups && nslots > 1) census(gi + 1);
         {
             ProfScope ps(c, c->s_hi, ASD_STAGE_UP, m * alg_bytes_up(p), m * alg_ops_up(p));
-            if (launch_v2_stage(1, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx,
+            if (launch_v2_stage(1, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
                                 nullptr, c->s_hi) != 0) {
                 set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                 return ASD_E_CUDA;
@@ -311,13 +348,14 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         cudaStreamWaitEvent(c->s_lo, c->ev_sw, 0);
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_ROW, m * alg_bytes_row(p), m * alg_ops_row(p));
-            launch_v2_stage(2, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx, nullptr, c->s_lo);
+            launch_v2_stage(2, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
+                            nullptr, c->s_lo);
         }
-        if (agg_debug && f0 == 0)            // S of frame 0 (natural order) before the WTA
-            cudaMemcpyAsync(agg_debug, pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, c->s_lo);
+        if (agg_debug && gi == 0)            // S of frame 0 (natural order) before the WTA
+            cudaMemcpyAsync(agg_debug, q.pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, c->s_lo);
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_WTA, m * alg_bytes_wta3(p), m * alg_ops_wta3(p));
-            if (launch_v2_stage(3, p, c->plan, m, cl, cr, npx, pa, pab, stash, p.ncell, g, npx,
+            if (launch_v2_stage(3, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
                                 nullptr, c->s_lo) != 0) {
                 set_err(c, "WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                 return ASD_E_CUDA;
@@ -326,11 +364,12 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         if (stats) cudaMemsetAsync(stats + f0, 0, sizeof(asd_frame_stats) * m, c->s_lo);
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_LR, m * alg_bytes_lr(p));
-            launch_lr_depth(p, m, g, npx, out_disp ? out_disp + f0 * npx : nullptr,
+            launch_lr_depth(p, m, q.g, npx, out_disp ? out_disp + f0 * npx : nullptr,
                             out_depth ? out_depth + f0 * npx : nullptr, npx,
                             mask_out ? mask_out + f0 * npx : nullptr, stats ? stats + f0 : nullptr, c->s_lo);
         }
-        cudaEventRecord(c->ev_free[slot], c->s_lo);
+        cudaEventRecord(c->ev_free[gi % nslots], c->s_lo);
+        if (gi + 1 < ngroups && nslots == 1) census(gi + 1);
     }
     cudaEventRecord(c->ev_hi, c->s_hi);              // join back to the caller's stream
     cudaEventRecord(c->ev_lo, c->s_lo);
@@ -400,8 +439,8 @@ void free_ctx(asd_ctx* c)
         if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-    for (cudaStream_t q : {c->s_hi, c->s_lo}) if (q) cudaStreamDestroy(q);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_sw, c->ev_hi, c->ev_lo}) if (e) cudaEventDestroy(e);
+    for (cudaStream_t q : {c->s_hi, c->s_lo, c->s_cen}) if (q) cudaStreamDestroy(q);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_sw, c->ev_hi, c->ev_lo, c->ev_cen}) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_free) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     delete c;
@@ -505,18 +544,14 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if (ok && (cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi) != cudaSuccess ||
-                   cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo) != cudaSuccess))
+                   cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo) != cudaSuccess ||
+                   cudaStreamCreateWithPriority(&c->s_cen, cudaStreamNonBlocking, hi) != cudaSuccess))
             ok = false;
-        for (cudaEvent_t* e : {&c->ev_fork, &c->ev_sw, &c->ev_hi, &c->ev_lo})
+        for (cudaEvent_t* e : {&c->ev_fork, &c->ev_sw, &c->ev_hi, &c->ev_lo, &c->ev_cen})
             if (ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) ok = false;
-        // overlap group: one wave of sweep clusters (env ASD_GROUP overrides), at
-        // most max_batch; max_batch / group scratch slots
-        c->group = c->plan.cs > 0 ? c->plan.active_ctas / c->plan.cs : 1;
-        if (const char* g = getenv("ASD_GROUP")) c->group = atoi(g);
-        if (c->group < 1 || c->group > max_batch) c->group = max_batch;
-        c->ev_free.assign(c->engine == ASD_ENGINE_D3 ? max_batch / c->group : 0, nullptr);
-        for (cudaEvent_t& e : c->ev_free)
-            if (ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) ok = false;
+        // overlap group: one wave of sweep clusters, at most max_batch
+        const int wave = c->plan.cs > 0 ? c->plan.active_ctas / c->plan.cs : 1;
+        if (ok && set_group(c, wave < 1 ? 1 : wave > max_batch ? max_batch : wave) != ASD_OK) ok = false;
     }
     for (int i = 0; i < 2 && ok; ++i)
         if (cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -548,6 +583,22 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 }
 
 int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }
+
+int asd_set_group(asd_ctx* ctx, int group)
+{
+    if (!ctx) { set_err(nullptr, "ctx is NULL"); return ASD_E_INVALID_ARG; }
+    if (group < 1 || group > ctx->max_batch) {
+        set_err(ctx, "group %d outside [1, max_batch=%d]", group, ctx->max_batch);
+        return ASD_E_INVALID_ARG;
+    }
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();                 // no batch of this context may be in flight
+    const int rc = set_group(ctx, group);
+    if (rc != ASD_OK) set_err(ctx, "event creation failed");
+    return rc;
+}
+
+int asd_group(const asd_ctx* ctx) { return ctx ? ctx->group : 0; }
 
 int asd_plan_info(const asd_ctx* ctx, char* buf, int n)
 {

@@ -479,17 +479,23 @@ vsweep_kernel(VArgs a)
                         o[g] = __byte_perm(s[kk], s[kk + 1], sel);
                     }
                 }
-                // natural [x][d] layout through the warp's staging block
-                uint4* sb = reinterpret_cast<uint4*>(stg + (col * D + chunk * DC) / 2);
+                // natural [x][d] layout through the warp's staging block.  16-byte
+                // piece p of the block (column p / PPC) is stored at p ^ (column &
+                // SWZ): without it the 32 lanes of one store instruction fall into
+                // two 16-byte bank groups (a 16-way conflict).
+                constexpr int PPC = DC * T / 8;                   // 16-byte pieces per column
+                constexpr int SWZ = (PPC < 8 ? PPC : 8) - 1;
+                uint4* sb = reinterpret_cast<uint4*>(stg);
+                const int pbase = col * PPC + chunk * (DC / 8);
 #pragma unroll
-                for (int q = 0; q < NR / 4; ++q) sb[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                for (int q = 0; q < NR / 4; ++q)
+                    sb[(pbase + q) ^ (col & SWZ)] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
                 __syncwarp();
-                const uint4* rb = reinterpret_cast<const uint4*>(stg);
                 uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + ((long long)y * W + (x - col)) * D);
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q) {
                     const int pi = 32 * q + lane;                 // 16-byte piece of the block
-                    if (x - col + (pi * 8) / (DC * T) < W) dst[pi] = rb[pi];
+                    if (x - col + pi / PPC < W) dst[pi] = sb[pi ^ ((pi / PPC) & SWZ)];
                 }
                 __syncwarp();
             }

@@ -17,8 +17,12 @@ def _oracle_frame(d, L, R):
     return o, oracle.checksum(o["dstar_l"], o["mask"])
 
 
-@pytest.mark.parametrize("name,n,max_batch", [("A", 7, 3), ("B", 5, 2)])
-def test_batch_matches_oracle(name, n, max_batch):
+# group: frames per D3 pipeline group (None = default).  (A, 7, 6, 2): three
+# scratch slots reused, a ragged last group; (B, 5, 4, 2): two slots; max_batch
+# 1: a single slot.
+@pytest.mark.parametrize("name,n,max_batch,group", [("A", 7, 3, None), ("B", 5, 2, None),
+                                                    ("A", 7, 6, 2), ("B", 5, 4, 2), ("A", 3, 1, 1)])
+def test_batch_matches_oracle(name, n, max_batch, group):
     import torch
     cfg = synth.CONFIGS[name]
     d = cfg.params_dict()
@@ -29,6 +33,9 @@ def test_batch_matches_oracle(name, n, max_batch):
     depth = torch.empty_like(disp)
     stats = torch.zeros(n, 4, dtype=torch.int32, device="cuda")
     with asd.Stereo(asd.Params(**d), 0, max_batch) as st:
+        if group is not None and st.engine == 3:
+            st.group = group
+            assert st.group == group
         st.asd_depth_batch(L, R, disp, depth, stats)
         torch.cuda.synchronize()
     disp, depth, stats = disp.cpu().numpy(), depth.cpu().numpy(), stats.cpu().numpy()
