@@ -550,7 +550,9 @@ template <int D> struct RowGeom {
     static constexpr int NRR = DPL / 2;              // u16x2 registers per lane
     static constexpr int ACT = D / DPL;              // active lanes
     static constexpr int NB = D + 40;                // rows of the S window (D + 32 + one sub-group)
-    static constexpr int BS = D + 4;                 // u16 per window row (8-byte aligned rows)
+    static constexpr int BS = D + 2;                 // u16 per WTA ring row: an odd number of
+                                                     // 4-byte words, so the 32 lanes of the
+                                                     // diagonal (right-view) scan hit 32 banks
     static constexpr int KS = D <= 16 ? 4 : D <= 32 ? 5 : D <= 64 ? 6 : 7;   // key shift = log2(D)
 };
 
@@ -562,11 +564,12 @@ __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, i
 {
     constexpr int KS = RowGeom<D>::KS;
     uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
+    const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);     // rows are 4-byte aligned
 #pragma unroll 4
     for (int q = 0; q < D; q += 4) {
-        const uint2 v = *reinterpret_cast<const uint2*>(r + q);
-        ka = vmin2(ka, v.x * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
-        kb2 = vmin2(kb2, v.y * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
+        const uint32_t v0 = r32[q / 2], v1 = r32[q / 2 + 1];
+        ka = vmin2(ka, v0 * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
+        kb2 = vmin2(kb2, v1 * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
     }
     const uint32_t kmin = vmin2(ka, kb2);
     const uint32_t kb = min(kmin & 0xFFFFu, kmin >> 16);
@@ -580,9 +583,8 @@ __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, i
     uint32_t vm = 0xFFFFFFFFu, vm2 = 0xFFFFFFFFu;
 #pragma unroll 4
     for (int q = 0; q < D; q += 4) {
-        const uint2 v = *reinterpret_cast<const uint2*>(r + q);
-        vm = vmin2(vm, v.x);
-        vm2 = vmin2(vm2, v.y);
+        vm = vmin2(vm, r32[q / 2]);
+        vm2 = vmin2(vm2, r32[q / 2 + 1]);
     }
     vm = vmin2(vm, vm2);
     if (dstar >= 1) r[dstar - 1] = (uint16_t)cm;
@@ -948,9 +950,11 @@ hrow_kernel(RArgs a)
 // ---------------------------------------------------------------- K_wta
 // WTA / uniqueness / sub-pixel for the left view and the re-indexed right view
 // (K4 semantics, post.cu) from S rows staged in a shared-memory ring.  One CTA
-// (4 warps) per image row walks stages of 128 pixels; stage t needs S rows
-// [128t, 128t + 127 + min + D - 1], loaded with 16-byte cp.async once each.
-constexpr int WTA_WARPS = 4;
+// (8 warps, two resident per SM) per image row walks stages of 256 pixels;
+// stage t needs S rows [256t, 256t + 255 + min + D - 1], each loaded once with
+// 4-byte cp.async (ring rows are D + 2 u16: an odd word stride keeps the
+// diagonal right-view reads free of bank conflicts).
+constexpr int WTA_WARPS = 8;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 
 __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc)
@@ -979,21 +983,22 @@ wta2_kernel(RArgs a)
         a.fs.mask_r[o] = MASK_BORDER;
         a.fs.dr[o] = 0.0f;
     }
-    constexpr int CH = D * 2 / 8;                     // 8-byte chunks per S row (rows are 8-byte aligned)
+    constexpr int CH = D * 2 / 4;                     // 4-byte words per S row (ring rows are 4-byte aligned)
     int loaded = 0;                                   // rows [0, loaded) issued
     const int nstage = (W + WTA_TX - 1) / WTA_TX;
     for (int t = 0; t < nstage; ++t) {
         const int x0 = t * WTA_TX;
         const int hi = min(W, x0 + WTA_TX + p.min_disp + D - 1);
         __syncthreads();                              // previous stage done with the ring
-        {   // thread t copies 8-byte chunk t % CH of rows loaded + t / CH, + RSTEP, ...
+        {   // thread t copies word t % CH of rows loaded + t / CH, + RSTEP, ...
             constexpr int RSTEP = 32 * WTA_WARPS / CH;
             const int c = threadIdx.x % CH;
             int x = loaded + threadIdx.x / CH;
             int slot = x % NB;
-            const uint16_t* src = S + (long long)x * D + c * 4;
+            const uint16_t* src = S + (long long)x * D + c * 2;
             for (; x < hi; x += RSTEP, src += RSTEP * D) {
-                cp_async8(sbuf + slot * BS + c * 4, src);
+                cp_async4(reinterpret_cast<uint32_t*>(sbuf + slot * BS + c * 2),
+                          reinterpret_cast<const uint32_t*>(src), true);
                 slot += RSTEP;
                 if (slot >= NB) slot -= NB;
             }
@@ -1185,7 +1190,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     // WTA kernel ring: rows [128t, 128t + 127 + min + D - 1] of stage t must
     // fit beside nothing else; NB > 128 + min + D - 1
     pl.nbuf = ((v2::WTA_TX + p.min_disp + p.D + 31) / 32) * 32;
-    pl.bstride = p.D + 4;               // RowGeom<D>::BS
+    pl.bstride = p.D + 2;               // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
     if (pl.rsmem > 200 * 1024) return no("min_disp + num_disp too large for the WTA ring");
     RKernel wk = pick_wkernel(p.D);
