@@ -279,9 +279,18 @@ int set_group(asd_ctx* c, int group)
 // and the stream priorities hand the freed SMs to the clusters first.
 // ev_free[slot] orders the reuse of a slot after the LR pass of the group that
 // last used it.
+// Host mode (hio != nullptr): inputs are copied per group from pinned host
+// memory into the slot's staging buffer on s_cen ahead of its census, and the
+// slot's outputs go back on copy_stream after its LR pass; the slot is freed
+// once that copy is done.
+struct HostIO {
+    const uint8_t* left; const uint8_t* right;
+    float* disp; float* depth; asd_frame_stats* stats;
+};
+
 int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
            float* out_disp, float* out_depth, asd_frame_stats* stats,
-           uint8_t* mask_out, cudaStream_t s, uint16_t* agg_debug)
+           uint8_t* mask_out, cudaStream_t s, uint16_t* agg_debug, const HostIO* hio = nullptr)
 {
     const DevParams& p = c->dp;
     if (n <= 0) return ASD_OK;
@@ -307,14 +316,25 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         return q;
     };
     auto frames = [&](int gi) { return (n - gi * G) < G ? (n - gi * G) : G; };
+    const long long MB = c->max_batch;
     auto census = [&](int gi) {
         const Slot q = slot_of(gi);
         const int m = frames(gi);
         const long long f0 = (long long)gi * G;
         if (gi >= nslots) cudaStreamWaitEvent(c->s_cen, c->ev_free[gi % nslots], 0);
+        const uint8_t* il = hio ? nullptr : left + f0 * npx;
+        const uint8_t* ir = hio ? nullptr : right + f0 * npx;
+        if (hio) {                                     // H2D of this group into its slot
+            const long long b0 = (long long)(gi % nslots) * G;
+            uint8_t* dl = c->stage_in[0] + b0 * npx;
+            uint8_t* dr = c->stage_in[0] + (MB + b0) * npx;
+            cudaMemcpyAsync(dl, hio->left + f0 * npx, (size_t)m * npx, cudaMemcpyHostToDevice, c->s_cen);
+            cudaMemcpyAsync(dr, hio->right + f0 * npx, (size_t)m * npx, cudaMemcpyHostToDevice, c->s_cen);
+            il = dl; ir = dr;
+        }
         {
             ProfScope ps(c, c->s_cen, ASD_STAGE_CENSUS, m * alg_bytes_census(p, c->sig_bytes));
-            launch_census(p, m, left + f0 * npx, right + f0 * npx, npx, q.cl, q.cr, npx, c->s_cen);
+            launch_census(p, m, il, ir, npx, q.cl, q.cr, npx, c->s_cen);
         }
         cudaEventRecord(c->ev_cen, c->s_cen);
     };
@@ -361,18 +381,34 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
                 return ASD_E_CUDA;
             }
         }
-        if (stats) cudaMemsetAsync(stats + f0, 0, sizeof(asd_frame_stats) * m, c->s_lo);
+        float* od = out_disp ? out_disp + f0 * npx : nullptr;
+        float* oz = out_depth ? out_depth + f0 * npx : nullptr;
+        asd_frame_stats* os = stats ? stats + f0 : nullptr;
+        if (hio) {                                     // outputs into the slot's staging buffers
+            const long long b0 = (long long)(gi % nslots) * G;
+            od = hio->disp ? c->stage_out[0] + b0 * npx : nullptr;
+            oz = hio->depth ? c->stage_out[0] + (MB + b0) * npx : nullptr;
+            os = hio->stats ? c->stage_stats[0] + b0 : nullptr;
+        }
+        if (os) cudaMemsetAsync(os, 0, sizeof(asd_frame_stats) * m, c->s_lo);
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_LR, m * alg_bytes_lr(p));
-            launch_lr_depth(p, m, q.g, npx, out_disp ? out_disp + f0 * npx : nullptr,
-                            out_depth ? out_depth + f0 * npx : nullptr, npx,
-                            mask_out ? mask_out + f0 * npx : nullptr, stats ? stats + f0 : nullptr, c->s_lo);
+            launch_lr_depth(p, m, q.g, npx, od, oz, npx, mask_out ? mask_out + f0 * npx : nullptr, os, c->s_lo);
         }
-        cudaEventRecord(c->ev_free[gi % nslots], c->s_lo);
+        if (hio) {                                     // D2H of this group, then the slot is free
+            cudaEventRecord(c->ev_comp[0], c->s_lo);
+            cudaStreamWaitEvent(c->copy_stream, c->ev_comp[0], 0);
+            if (od) cudaMemcpyAsync(hio->disp + f0 * npx, od, (size_t)m * npx * 4, cudaMemcpyDeviceToHost, c->copy_stream);
+            if (oz) cudaMemcpyAsync(hio->depth + f0 * npx, oz, (size_t)m * npx * 4, cudaMemcpyDeviceToHost, c->copy_stream);
+            if (os) cudaMemcpyAsync(hio->stats + f0, os, m * sizeof(asd_frame_stats), cudaMemcpyDeviceToHost, c->copy_stream);
+            cudaEventRecord(c->ev_free[gi % nslots], c->copy_stream);
+        } else {
+            cudaEventRecord(c->ev_free[gi % nslots], c->s_lo);
+        }
         if (gi + 1 < ngroups && nslots == 1) census(gi + 1);
     }
     cudaEventRecord(c->ev_hi, c->s_hi);              // join back to the caller's stream
-    cudaEventRecord(c->ev_lo, c->s_lo);
+    cudaEventRecord(c->ev_lo, hio ? c->copy_stream : c->s_lo);
     cudaStreamWaitEvent(s, c->ev_hi, 0);
     cudaStreamWaitEvent(s, c->ev_lo, 0);
     cudaError_t e = cudaGetLastError();
@@ -659,6 +695,14 @@ int asd_depth_batch_host(asd_ctx* ctx, int n, const uint8_t* left_host, const ui
     if (!left_host || !right_host) { set_err(ctx, "left/right is NULL"); return ASD_E_INVALID_ARG; }
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (ctx->engine == ASD_ENGINE_D3) {           // per-group copies inside the D3 pipeline
+        const HostIO hio{left_host, right_host, out_disp_host, out_depth_host, stats_host};
+        int rc = run_d3(ctx, n, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, s, nullptr, &hio);
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (rc != ASD_OK) return rc;
+        if (e != cudaSuccess) { set_err(ctx, "host pipeline failed: %s", cudaGetErrorString(e)); return ASD_E_CUDA; }
+        return ASD_OK;
+    }
     cudaStream_t cs = ctx->copy_stream;
     const size_t npx = (size_t)ctx->dp.npx;
     const int B = ctx->max_batch;
