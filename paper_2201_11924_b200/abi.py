@@ -14,7 +14,8 @@ import os
 from dataclasses import dataclass
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libasd.so")
+# ASD_LIB overrides the library path (A/B timing of kernel variants, tools/)
+LIB_PATH = os.environ.get("ASD_LIB") or os.path.join(_PKG, "lib", "libasd.so")
 
 ASD_OK, ASD_E_INVALID_ARG, ASD_E_UNSUPPORTED, ASD_E_CUDA, ASD_E_OOM = 0, -1, -2, -3, -4
 MASK_BORDER, MASK_UNIQUE, MASK_LR, MASK_NONPOS = 1, 2, 4, 8
