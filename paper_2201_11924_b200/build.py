@@ -49,6 +49,8 @@ def _compile(src: str, verbose: bool) -> str:
            "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
     if src in NO_FMA:
         cmd.insert(-4, "--fmad=false")
+    for d in os.environ.get("ASD_NVCC_DEFS", "").split():      # experiment builds only, e.g. -DASD_ABLATE
+        cmd.insert(-4, d)
     if verbose:
         cmd.insert(-4, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

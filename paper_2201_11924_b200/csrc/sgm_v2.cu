@@ -114,8 +114,16 @@ struct VArgs {
     uint16_t* pout16;         // K_up output P_AB (row-kernel layout)
     long long cell_stride;    // H*W*D
     long long pa_stride;      // frame stride of the P_A buffer: H * (cs*w) * D
-    int ablate;               // timing experiments only (ASD_V2_ABLATE); 0 in production
+    int ablate;               // timing experiments only (ASD_V2_ABLATE, builds with -DASD_ABLATE)
 };
+
+// Ablation switches exist only in experiment builds (-DASD_ABLATE); in the
+// production library they are compile-time zero, so no per-row test remains.
+#ifdef ASD_ABLATE
+#define ABL(a, bit) (((a).ablate & (bit)) != 0)
+#else
+#define ABL(a, bit) false
+#endif
 
 // ---------------------------------------------------------------- helpers
 // Mp is the predecessor's min over d packed in both halves (M | M << 16);
@@ -201,7 +209,7 @@ vsweep_kernel(VArgs a)
     const int x = x0 + xl;
     const int cstr = G::cstride(w);
     const int sw = G::slot_words(w);
-    const bool clustered = NP == 3 && a.cs > 1 && !(a.ablate & 1);
+    const bool clustered = NP == 3 && a.cs > 1 && !ABL(a, 1);
 
     const int nslot = UP ? 0 : NSLOT;
     uint32_t* cens = smem;                   // [NSLOT][sw] (K_down): left row, then T right-row slices
@@ -231,7 +239,7 @@ vsweep_kernel(VArgs a)
     // census rows -> shared memory with asynchronous copies (one commit group per
     // row).  K_up reads its costs from K_down's packed output instead.
     auto stage = [&](int yrow, int slot) {
-        if (UP || (a.ablate & 64)) { if (!UP) cp_async_commit(); return; }
+        if (UP || ABL(a, 64)) { if (!UP) cp_async_commit(); return; }
         uint32_t* sl = cens + slot * sw;
         const uint32_t* rl = cl + (long long)yrow * W;
         const uint32_t* rr = cr + (long long)yrow * W;
@@ -254,7 +262,7 @@ vsweep_kernel(VArgs a)
     };
     const bool vcol = x >= p.R && x < W - p.R;
     auto cost = [&](int yrow, int slot, uint32_t (&C)[NR]) {
-        const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q && !(a.ablate & 8);
+        const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q && !ABL(a, 8);
         const uint32_t nbnb = (uint32_t)p.nb * 0x10001u;
         if (!vx) {
 #pragma unroll
@@ -283,13 +291,13 @@ vsweep_kernel(VArgs a)
     // K_up: P_A and C of one row from K_down's packed words (reg k = cells d0+k, d0+NR+k)
     const unsigned row_bytes = (unsigned)(w * D * 2);
     auto issue_row = [&](int i) {                    // K_up: TMA the i-th processed row into the ring
-        if (UP && threadIdx.x == 0 && i < H && !(a.ablate & 64))
+        if (UP && threadIdx.x == 0 && i < H && !ABL(a, 64))
             bulk_g2s(ring + (i % KU) * w * D,
                      a.pin + frame * a.pa_stride + ((long long)row_of(i) * wpad + x0) * D, row_bytes,
                      mbar + (i % KU));
     };
     auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
-        if (!(a.ablate & 64)) mbar_wait(mbar + (i % KU), (unsigned)((i / KU) & 1));
+        if (!ABL(a, 64)) mbar_wait(mbar + (i % KU), (unsigned)((i / KU) & 1));
         const uint4* src = reinterpret_cast<const uint4*>(ring + (i % KU) * w * D + (warp * CPW) * D) + lane;
 #pragma unroll
         for (int q = 0; q < NR / 4; ++q) {
@@ -348,7 +356,7 @@ vsweep_kernel(VArgs a)
     uint32_t C[NR];
     uint32_t PA[NR];
 
-    if (NP == 3 && a.cs > 1 && (a.ablate & 1)) { cluster_arrive(); cluster_wait(); }
+    if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
     if (UP) {
         if (threadIdx.x == 0) {
             for (int s2 = 0; s2 < KU; ++s2) mbar_init(mbar + s2, 1);
@@ -369,7 +377,7 @@ vsweep_kernel(VArgs a)
     for (int i = 0; i < H; ++i) {
         const int y = row_of(i);
         if (i > 0) wait();
-        if (NP == 3 && !(a.ablate & 4)) {
+        if (NP == 3 && !ABL(a, 4)) {
             const int rs = (i + 1) & 1;              // slot written at row i-1
             uint32_t Pp[NR], Mp;
             // path "L": predecessor column x-1 (down-right / up-right)
@@ -425,7 +433,7 @@ vsweep_kernel(VArgs a)
             }
         }
         // ---- vertical path: predecessor = own column (after the halo stores)
-        if (!(a.ablate & 32)) {
+        if (!ABL(a, 32)) {
             uint32_t Ln[NR], mnew;
             path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
 #pragma unroll
@@ -446,7 +454,7 @@ vsweep_kernel(VArgs a)
         arrive();
         issue_row(i + KU);                            // K_up: row i's ring slot is free now
         // ---- partial sum out (after the release so it does not wait on these stores)
-        if (!(a.ablate & 2)) {
+        if (!ABL(a, 2)) {
             uint32_t s[NR];
 #pragma unroll
             for (int k = 0; k < NR; ++k) s[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
@@ -507,7 +515,7 @@ vsweep_kernel(VArgs a)
         }
     }
     wait();                                          // pairs with the last arrive
-    if (NP == 3 && a.cs > 1 && (a.ablate & 1)) { cluster_arrive(); cluster_wait(); }
+    if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
 }
 
 // ---------------------------------------------------------------- K_row
