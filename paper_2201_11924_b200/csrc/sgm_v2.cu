@@ -176,7 +176,7 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
 // slice of the right row its DC disparities read (w + DC - 1 words), placed at
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
-constexpr int NSLOT = 6;          // census rows in flight (K_down): rows i+1 .. i+5
+constexpr int NSLOT = 4;          // census rows in flight (K_down): rows i+1 .. i+3
 constexpr int KU = 3;             // K_up input rows in flight (TMA bulk ring)
 
 template <int DC, int T>
