@@ -41,7 +41,8 @@ class OracleParams(ctypes.Structure):
                 ("p1", ctypes.c_int32), ("p2", ctypes.c_int32),
                 ("paths", ctypes.c_int32), ("uniqueness", ctypes.c_int32),
                 ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
-                ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float)]
+                ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
+                ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32)]
 
 
 @dataclass
@@ -61,6 +62,8 @@ class Params:
     subpixel: int = 1
     focal_px: float = 430.0
     baseline_m: float = 0.055
+    block_w: int = 1          # SGBM block; 1 x 1 = plain SGM
+    block_h: int = 1
 
     @property
     def nbits(self) -> int:
@@ -70,7 +73,7 @@ class Params:
         return OracleParams(self.width, self.height, self.min_disp, self.num_disp,
                             self.census_w, self.census_h, self.p1, self.p2, self.paths,
                             self.uniqueness, self.lr_max_diff, self.subpixel,
-                            self.focal_px, self.baseline_m)
+                            self.focal_px, self.baseline_m, self.block_w, self.block_h)
 
 
 _lib = None
@@ -104,6 +107,22 @@ def cost(p: Params, cl: np.ndarray, cr: np.ndarray) -> np.ndarray:
     cr = np.ascontiguousarray(cr, np.uint64)
     out = np.empty((p.height, p.width, p.num_disp), np.uint8)
     lib().oracle_cost(ctypes.byref(p.c()), _p(cl), _p(cr), _p(out))
+    return out
+
+
+def block_cost(p: Params, C: np.ndarray) -> np.ndarray:
+    """O2b -- SGBM block cost (reading c19).  C u8[H][W][D] -> u32[H][W][D]."""
+    C = np.ascontiguousarray(C, np.uint8)
+    out = np.empty((p.height, p.width, p.num_disp), np.uint32)
+    lib().oracle_block_cost(ctypes.byref(p.c()), _p(C), _p(out))
+    return out
+
+
+def sgm32(p: Params, C: np.ndarray) -> np.ndarray:
+    """O3 on a u32 cost volume (SGBM block costs).  -> u32[H][W][D]."""
+    C = np.ascontiguousarray(C, np.uint32)
+    out = np.empty((p.height, p.width, p.num_disp), np.uint32)
+    lib().oracle_sgm32(ctypes.byref(p.c()), _p(C), _p(out))
     return out
 
 

@@ -15,6 +15,8 @@
  *
  *   O1 census      CSCT bit i = I(p + o_i) > I(p - o_i)
  *   O2 cost        C = popcount(cl(x,y) XOR cr(x-delta,y)) or nb
+ *   O2b SGBM cost  CB(x,y,d) = sum over the bw x bh block of C(x+u,y+v,d),
+ *                  nb for block positions outside the image
  *   O3 SGM         L_r(p,d) = C + min(L_r(p-r,d), L_r(p-r,d+-1)+P1,
  *                                     min_k L_r(p-r,k)+P2) - min_k L_r(p-r,k)
  *                  S = sum_r L_r
@@ -48,6 +50,7 @@ typedef struct {
     float   lr_max_diff;       /* px; < 0 disables */
     int32_t subpixel;          /* 0/1 */
     float   focal_px, baseline_m;
+    int32_t block_w, block_h;  /* SGBM block (odd); 1 x 1 = plain SGM */
 } oracle_params;
 
 /* mask bits */
@@ -110,6 +113,35 @@ void oracle_cost(const oracle_params* p, const uint64_t* cl, const uint64_t* cr,
             }
 }
 
+/* ---------------------------------------------------------- O2b SGBM cost
+ * SGBM ("SGBM computes the cost by the hamming distance between the
+ * local regions of the two pixels"; "for SGBM, sum of hamming over the
+ * block around both pixels"): the same offset (u,v) is applied to both pixels,
+ *   CB(x,y,d) = sum_{|u| <= bw/2, |v| <= bh/2} C~(x+u, y+v, d),
+ * C~ = C (O2, nb for invalid / out of range) inside the image and nb outside
+ * (reading c19: a block position off the image is an invalid match, c3).
+ * bw = bh = 1 gives CB = C.  Layout [H][W][D], u32.
+ */
+void oracle_block_cost(const oracle_params* p, const uint8_t* C, uint32_t* CB)
+{
+    int W = p->width, H = p->height, D = p->num_disp, nb = nbits(p);
+    int bu = p->block_w / 2, bv = p->block_h / 2;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int d = 0; d < D; ++d) {
+                uint32_t sum = 0;
+                for (int v = -bv; v <= bv; ++v)
+                    for (int u = -bu; u <= bu; ++u) {
+                        int xx = x + u, yy = y + v;
+                        if (xx >= 0 && xx < W && yy >= 0 && yy < H)
+                            sum += C[((size_t)yy * W + xx) * D + d];
+                        else
+                            sum += (uint32_t)nb;
+                    }
+                CB[((size_t)y * W + x) * D + d] = sum;
+            }
+}
+
 /* ------------------------------------------------------------- O3 one line
  * The SGM recursion along one line of n pixels ("four-path semi-global
  * matching (SGM) [Hirschmuller]"):
@@ -158,7 +190,7 @@ static int inside(const oracle_params* p, int x, int y) {
 /* L_r for one direction over the whole image: every line of direction r starts
  * at a pixel whose predecessor p - r is outside the image ("first pixel of each
  * path: L_r = C") and is walked forward with oracle_chain. */
-void oracle_sgm_path(const oracle_params* p, const uint8_t* C, int rx, int ry, uint32_t* L)
+void oracle_sgm_path32(const oracle_params* p, const uint32_t* C, int rx, int ry, uint32_t* L)
 {
     int W = p->width, H = p->height, D = p->num_disp;
     int nmax = W > H ? W : H;
@@ -184,17 +216,39 @@ void oracle_sgm_path(const oracle_params* p, const uint8_t* C, int rx, int ry, u
     free(cbuf); free(lbuf); free(xs); free(ys);
 }
 
-/* S = sum_r L_r over the configured path set. */
-void oracle_sgm(const oracle_params* p, const uint8_t* C, uint32_t* S)
+/* S = sum_r L_r over the configured path set, on a u32 cost volume
+ * (the per-pixel Hamming cost O2 or the SGBM block cost O2b). */
+void oracle_sgm32(const oracle_params* p, const uint32_t* C, uint32_t* S)
 {
     size_t n = (size_t)p->width * p->height * p->num_disp;
     uint32_t* L = (uint32_t*)malloc(sizeof(uint32_t) * n);
     memset(S, 0, sizeof(uint32_t) * n);
     for (int r = 0; r < p->paths; ++r) {
-        oracle_sgm_path(p, C, DIRS[r][0], DIRS[r][1], L);
+        oracle_sgm_path32(p, C, DIRS[r][0], DIRS[r][1], L);
         for (size_t i = 0; i < n; ++i) S[i] += L[i];
     }
     free(L);
+}
+
+/* The same on the u8 Hamming cost volume of O2 (values widened, unchanged). */
+static uint32_t* widen(const oracle_params* p, const uint8_t* C)
+{
+    size_t n = (size_t)p->width * p->height * p->num_disp;
+    uint32_t* C32 = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    for (size_t i = 0; i < n; ++i) C32[i] = C[i];
+    return C32;
+}
+void oracle_sgm_path(const oracle_params* p, const uint8_t* C, int rx, int ry, uint32_t* L)
+{
+    uint32_t* C32 = widen(p, C);
+    oracle_sgm_path32(p, C32, rx, ry, L);
+    free(C32);
+}
+void oracle_sgm(const oracle_params* p, const uint8_t* C, uint32_t* S)
+{
+    uint32_t* C32 = widen(p, C);
+    oracle_sgm32(p, C32, S);
+    free(C32);
 }
 
 /* S(x,y,.) for ONE pixel, computed from the raw cost volume by walking, for
@@ -212,14 +266,21 @@ void oracle_sgm_pixel_from_census(const oracle_params* p, const uint64_t* cl, co
         int rx = DIRS[r][0], ry = DIRS[r][1];
         int sx = x, sy = y, n = 1;                 /* back up to the start of the line */
         while (inside(p, sx - rx, sy - ry)) { sx -= rx; sy -= ry; ++n; }
+        int bu = p->block_w / 2, bv = p->block_h / 2;
         for (int i = 0; i < n; ++i) {
             int px = sx + i * rx, py = sy + i * ry;
-            for (int d = 0; d < D; ++d) {          /* O2 restated for this pixel */
-                int xr = px - (p->min_disp + d);
-                int c = nb;
-                if (valid_c(p, px, py) && xr >= 0 && valid_c(p, xr, py))
-                    c = popcount64(cl[py * W + px] ^ cr[py * W + xr]);
-                cbuf[(size_t)i * D + d] = (uint32_t)c;
+            for (int d = 0; d < D; ++d) {          /* O2 / O2b restated for this pixel */
+                uint32_t sum = 0;
+                for (int v = -bv; v <= bv; ++v)
+                    for (int u = -bu; u <= bu; ++u) {
+                        int qx = px + u, qy = py + v, xr = qx - (p->min_disp + d);
+                        int c = nb;
+                        if (qx >= 0 && qx < W && qy >= 0 && qy < H &&
+                            valid_c(p, qx, qy) && xr >= 0 && valid_c(p, xr, qy))
+                            c = popcount64(cl[qy * W + qx] ^ cr[qy * W + xr]);
+                        sum += (uint32_t)c;
+                    }
+                cbuf[(size_t)i * D + d] = sum;
             }
         }
         oracle_chain(n, D, p->p1, p->p2, cbuf, lbuf);
@@ -380,6 +441,7 @@ int oracle_compute(const oracle_params* p, const uint8_t* left, const uint8_t* r
     uint64_t* cl = (uint64_t*)malloc(sizeof(uint64_t) * npx);
     uint64_t* cr = (uint64_t*)malloc(sizeof(uint64_t) * npx);
     uint8_t* C = (uint8_t*)malloc(ncell);
+    uint32_t* CB = (uint32_t*)malloc(sizeof(uint32_t) * ncell);
     uint32_t* S = (uint32_t*)malloc(sizeof(uint32_t) * ncell);
     int16_t* dsl = (int16_t*)malloc(sizeof(int16_t) * npx);
     int16_t* dsr = (int16_t*)malloc(sizeof(int16_t) * npx);
@@ -390,11 +452,12 @@ int oracle_compute(const oracle_params* p, const uint8_t* left, const uint8_t* r
     float* disp = (float*)malloc(sizeof(float) * npx);
     double* z = (double*)malloc(sizeof(double) * npx);
     int rc = -1;
-    if (!cl || !cr || !C || !S || !dsl || !dsr || !ml || !mr || !dl || !dr || !disp || !z) goto done;
+    if (!cl || !cr || !C || !CB || !S || !dsl || !dsr || !ml || !mr || !dl || !dr || !disp || !z) goto done;
     oracle_census(p, left, cl);                 /* O1 */
     oracle_census(p, right, cr);
     oracle_cost(p, cl, cr, C);                  /* O2 */
-    oracle_sgm(p, C, S);                        /* O3 */
+    oracle_block_cost(p, C, CB);                /* O2b (1 x 1: CB = C) */
+    oracle_sgm32(p, CB, S);                     /* O3 */
     oracle_wta_left(p, S, dsl, ml, dl);         /* O4, O5 */
     oracle_wta_right(p, S, dsr, mr, dr);        /* O6 */
     oracle_lr_depth(p, dl, dr, mr, ml, disp, z);/* O7, O8 */
@@ -412,7 +475,7 @@ int oracle_compute(const oracle_params* p, const uint8_t* left, const uint8_t* r
     if (mask_r_out) memcpy(mask_r_out, mr, npx);
     rc = 0;
 done:
-    free(cl); free(cr); free(C); free(S); free(dsl); free(dsr); free(ml); free(mr);
+    free(cl); free(cr); free(C); free(CB); free(S); free(dsl); free(dsr); free(ml); free(mr);
     free(dl); free(dr); free(disp); free(z);
     return rc;
 }
