@@ -42,7 +42,8 @@ KERNEL_NAMES = {"census": "census_kernel (K1)", "dir": "sgm_dir_kernel (D1, one 
                 "wta": "WTA kernel (K4: D1 wta_kernel / D3 wta2_kernel)", "lr": "lr_depth_kernel (K5)",
                 "down": "vsweep_kernel<down> (D3, 3 downward paths)",
                 "up": "vsweep_kernel<up> (D3, 3 upward paths)",
-                "row": "hrow_kernel (D3, horizontal paths)"}
+                "row": "hrow_kernel (D3, horizontal paths)",
+                "block": "block_cost_kernel (SGBM block cost volume)"}
 
 
 def peaks():

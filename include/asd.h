@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define ASD_VERSION 1
+#define ASD_VERSION 2
 
 #define ASD_OK              0
 #define ASD_E_INVALID_ARG  (-1)  /* bad parameter, NULL required pointer, n out of range */
@@ -62,7 +62,8 @@ extern "C" {
  *       (SPEC allows up to 112 bits; nb > 64 -> ASD_E_UNSUPPORTED)
  *   min_disp >= 0; num_disp % 16 == 0 and 16 <= num_disp <= 256
  *   0 <= p1 <= p2 and nb + p2 <= 255  (each path's L_r <= C + P2 fits 8 bits;
- *       else ASD_E_UNSUPPORTED)
+ *       else ASD_E_UNSUPPORTED); with an SGBM block instead
+ *       paths * (block_w*block_h*nb + p2) <= 65535 (S fits 16 bits)
  *   paths in {4, 8} (4 = horizontal + vertical, 8 adds the diagonals, reading c6)
  *   uniqueness: percent, < 0 disables the test; <= 100000
  *   lr_max_diff: px, < 0 disables the LR check; not NaN
@@ -70,7 +71,13 @@ extern "C" {
  *   focal_px, baseline_m: finite, > 0; depth = fb / disparity with
  *       fb = (float)((double)focal_px * (double)baseline_m)
  *   engine: ASD_ENGINE_AUTO / _D1 / _D3; D3 outside its envelope ->
- *       ASD_E_UNSUPPORTED.  Results are bit-identical across engines. */
+ *       ASD_E_UNSUPPORTED.  Results are bit-identical across engines.
+ *   block_w, block_h: SGBM block ("SGBM computes the cost by
+ *       the hamming distance between the local regions of the two pixels";
+ *       SPEC S:258; reading c19): odd, 1..15; 0 is read as 1.
+ *       1 x 1 = plain SGM.  The cost becomes CB(x,y,d) = sum over the block
+ *       of C(x+u, y+v, d), nb for block positions off the image.  A block
+ *       larger than 1 x 1 runs on engine D1 (the D3 packing holds 8-bit costs). */
 /* Aggregation designs:
  *   ASD_ENGINE_D1  one warp-per-line kernel per path direction, u16 S volume
  *                  read-modify-written in HBM (any configuration above)
@@ -96,6 +103,7 @@ typedef struct asd_params {
     int32_t subpixel;
     float   focal_px, baseline_m;
     int32_t engine;      /* ASD_ENGINE_* (0 = auto) */
+    int32_t block_w, block_h;   /* SGBM block, 1 x 1 (or 0) = SGM */
 } asd_params;
 
 /* Per-frame statistics; exact integers except depth_sum.
@@ -215,7 +223,8 @@ int asd_plan_info(const asd_ctx* ctx, char* buf, int n);
 #define ASD_STAGE_DOWN   4   /* D3: downward sweep (3 paths, or 1 at 4-path) */
 #define ASD_STAGE_UP     5   /* D3: upward sweep */
 #define ASD_STAGE_ROW    6   /* D3: horizontal paths, S written over the partial */
-#define ASD_STAGE_COUNT  7
+#define ASD_STAGE_BLOCK  7   /* SGBM block cost volume (D1 with block > 1 x 1) */
+#define ASD_STAGE_COUNT  8
 typedef struct asd_stage_times {
     double ms[ASD_STAGE_COUNT];
     double alg_bytes[ASD_STAGE_COUNT];

@@ -35,7 +35,8 @@ class asd_params(ctypes.Structure):
                 ("paths", ctypes.c_int32), ("uniqueness", ctypes.c_int32),
                 ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
                 ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
-                ("engine", ctypes.c_int32)]
+                ("engine", ctypes.c_int32),
+                ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32)]
 
 
 class asd_frame_stats(ctypes.Structure):
@@ -49,13 +50,13 @@ class asd_debug_out(ctypes.Structure):
                  "disp_l", "disp_r", "mask", "mask_r")]
 
 
-STAGES = ("census", "dir", "wta", "lr", "down", "up", "row")
+STAGES = ("census", "dir", "wta", "lr", "down", "up", "row", "block")
 
 
 class asd_stage_times(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 7), ("alg_bytes", ctypes.c_double * 7),
-                ("alg_ops", ctypes.c_double * 7),
-                ("launches", ctypes.c_int32 * 7), ("dropped", ctypes.c_int32),
+    _fields_ = [("ms", ctypes.c_double * 8), ("alg_bytes", ctypes.c_double * 8),
+                ("alg_ops", ctypes.c_double * 8),
+                ("launches", ctypes.c_int32 * 8), ("dropped", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
 
@@ -121,12 +122,14 @@ class Params:
     focal_px: float = 430.0
     baseline_m: float = 0.055
     engine: int = 0            # ASD_ENGINE_AUTO (0), _D1 (1), _D3 (3)
+    block_w: int = 1           # SGBM block (reading c19); 1 x 1 = SGM
+    block_h: int = 1
 
     def c(self) -> asd_params:
         return asd_params(self.width, self.height, self.min_disp, self.num_disp, self.census_w,
                           self.census_h, self.p1, self.p2, self.paths, self.uniqueness,
                           self.lr_max_diff, self.subpixel, self.focal_px, self.baseline_m,
-                          self.engine)
+                          self.engine, self.block_w, self.block_h)
 
     @property
     def nbits(self) -> int:

@@ -33,6 +33,7 @@ struct asd_ctx {
     void* census_l = nullptr;
     void* census_r = nullptr;
     uint16_t* S = nullptr;
+    uint16_t* cb = nullptr;       // SGBM block cost volume [B][H][W][D] u16 (D1, block > 1)
     float* dl = nullptr;
     float* dr = nullptr;
     int16_t* dstar_l = nullptr;
@@ -126,8 +127,17 @@ int validate(const asd_params* p, char* why, size_t n)
         snprintf(why, n, "need 0 <= p1 <= p2 (got p1=%d p2=%d)", p->p1, p->p2);
         return ASD_E_INVALID_ARG;
     }
-    if (nb + p->p2 > 255) {
+    const int bw = p->block_w == 0 ? 1 : p->block_w, bh = p->block_h == 0 ? 1 : p->block_h;
+    if (bw < 1 || bh < 1 || !(bw & 1) || !(bh & 1) || bw > 15 || bh > 15) {
+        snprintf(why, n, "block_w/block_h must be odd in [1, 15] (0 = 1); got %d x %d", p->block_w, p->block_h);
+        return ASD_E_INVALID_ARG;
+    }
+    if (bw * bh == 1 && nb + p->p2 > 255) {
         snprintf(why, n, "nb + p2 = %d > 255 (per-path cost must fit 8 bits)", nb + p->p2);
+        return ASD_E_UNSUPPORTED;
+    }
+    if (bw * bh > 1 && (long long)(p->paths == 8 ? 8 : 4) * ((long long)bw * bh * nb + p->p2) > 65535) {
+        snprintf(why, n, "paths * (block area * nb + p2) > 65535 (S must fit 16 bits)");
         return ASD_E_UNSUPPORTED;
     }
     if (p->paths != 4 && p->paths != 8) {
@@ -165,11 +175,13 @@ DevParams make_dev(const asd_params* p)
     d.fb = (float)((double)p->focal_px * (double)p->baseline_m);
     d.npx = (long long)p->width * p->height;
     d.ncell = d.npx * p->num_disp;
+    d.bw = p->block_w == 0 ? 1 : p->block_w;
+    d.bh = p->block_h == 0 ? 1 : p->block_h;
     return d;
 }
 
 struct Layout {
-    size_t sig, s, pa, pab, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
+    size_t sig, s, cb, pa, pab, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
 };
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
@@ -181,6 +193,7 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     const size_t B = (size_t)max_batch;
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
     L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
+    L.cb = (engine == ASD_ENGINE_D1 && d.bw * d.bh > 1) ? align_up(B * d.ncell * 2) : 0;
     L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.H * pa_cols * d.D * 2) : 0;   // P_A | C << 8, u16
     L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
     L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
@@ -190,7 +203,7 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     L.stage_in = align_up(B * d.npx * 2);
     L.stage_out = align_up(B * d.npx * 2 * 4);
     L.stats = align_up(B * sizeof(asd_frame_stats));
-    L.total = 2 * L.sig + L.s + L.pa + L.pab + L.stash + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
+    L.total = 2 * L.sig + L.s + L.cb + L.pa + L.pab + L.stash + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
               2 * (L.stage_in + L.stage_out + L.stats);
     return L;
 }
@@ -230,7 +243,12 @@ struct ProfScope {
 // dl, dr (f32), d* (i16) and masks (u8) for both views.  LR: read those per-
 // pixel maps once, write disp and depth (f32).
 static double alg_bytes_census(const DevParams& p, size_t sig) { return 2.0 * p.npx * (1 + sig); }
-static double alg_bytes_dir(const DevParams& p, bool first) { return (first ? 2.0 : 4.0) * p.ncell; }
+static double alg_bytes_dir(const DevParams& p, bool first)
+{   // + the u16 block-cost read in SGBM mode
+    return ((first ? 2.0 : 4.0) + (p.bw * p.bh > 1 ? 2.0 : 0.0)) * p.ncell;
+}
+// SGBM block cost: write CB (u16); census reads are L2-resident.
+static double alg_bytes_block(const DevParams& p) { return 2.0 * p.ncell; }
 static double alg_bytes_wta(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * (4 + 2 + 1); }
 static double alg_bytes_lr(const DevParams& p) { return p.npx * (2 * (4 + 1) + 2 + 2 * 4.0); }
 // Design D3: down sweep writes P_A | C << 8 (u16, 2 B/cell); up sweep reads it
@@ -434,10 +452,14 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         launch_census(p, n, left, right, npx, c->census_l, c->census_r, npx, s);
     }
     FrameScratch fs = frame_scratch(c);
+    if (c->engine == ASD_ENGINE_D1 && c->cb) {      // SGBM: block cost volume first
+        ProfScope ps(c, s, ASD_STAGE_BLOCK, n * alg_bytes_block(p));
+        launch_block_cost(p, n, c->census_l, c->census_r, npx, c->cb, p.ncell, s);
+    }
     for (int r = 0; c->engine == ASD_ENGINE_D1 && r < p.paths; ++r) {
         ProfScope ps(c, s, ASD_STAGE_DIR, n * alg_bytes_dir(p, r == 0));
         if (!launch_sgm_dir(p, n, kDirs[r][0], kDirs[r][1], r == 0, c->census_l, c->census_r, npx,
-                            c->S, p.ncell, s)) {
+                            c->S, p.ncell, s, c->cb)) {
             set_err(c, "no SGM kernel instance for num_disp=%d", p.D);
             return ASD_E_UNSUPPORTED;
         }
@@ -465,7 +487,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
 void free_ctx(asd_ctx* c)
 {
     if (!c) return;
-    void* ptrs[] = {c->census_l, c->census_r, c->S, c->dl, c->dr, c->dstar_l, c->dstar_r,
+    void* ptrs[] = {c->census_l, c->census_r, c->S, c->cb, c->dl, c->dr, c->dstar_l, c->dstar_r,
                     c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
@@ -558,6 +580,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     };
     alloc(&c->census_l, L.sig); alloc(&c->census_r, L.sig);
     if (L.s) alloc((void**)&c->S, L.s);
+    if (L.cb) alloc((void**)&c->cb, L.cb);
     if (L.pa) alloc((void**)&c->pa, L.pa);
     if (L.pab) alloc((void**)&c->pab, L.pab);
     if (L.stash) alloc((void**)&c->stash, L.stash);
@@ -614,7 +637,7 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 {
     if (!ctx || n <= 0) return 0;
     const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
-    if (ctx->engine != ASD_ENGINE_D3) return chunks * (3 + ctx->dp.paths);
+    if (ctx->engine != ASD_ENGINE_D3) return chunks * (3 + ctx->dp.paths + (ctx->cb ? 1 : 0));
     return 6 * ((n + ctx->group - 1) / ctx->group);   // per group: census, down, up, row, WTA, LR
 }
 

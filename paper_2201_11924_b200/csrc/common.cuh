@@ -21,6 +21,7 @@ struct DevParams {
     float fb;          // focal_px * baseline_m rounded once to fp32
     long long npx;     // W*H
     long long ncell;   // W*H*D
+    int bw, bh;        // SGBM block (1 x 1 = SGM)
 };
 
 constexpr uint8_t MASK_BORDER = 1, MASK_UNIQUE = 2, MASK_LR = 4, MASK_NONPOS = 8;

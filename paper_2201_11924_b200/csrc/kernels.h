@@ -14,9 +14,16 @@ void launch_census(const DevParams& p, int nframes, const uint8_t* left, const u
 
 // K2/K3 one SGM direction (design D1); first = write S instead of accumulate.
 int num_chains(const DevParams& p, int rx, int ry);
+// cv != nullptr: read the matching cost from that u16 [H][W][D] volume (SGBM)
+// instead of recomputing it from the census images.
 bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
                     const void* cl, const void* cr, long long sig_stride,
-                    uint16_t* S, long long s_stride, cudaStream_t s);
+                    uint16_t* S, long long s_stride, cudaStream_t s,
+                    const uint16_t* cv = nullptr);
+
+// SGBM block cost volume CB (u16 [H][W][D] per frame), sgbm.cu.
+void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
+                       long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s);
 
 // K4 WTA/uniqueness/sub-pixel, left + right view.
 bool launch_wta(const DevParams& p, int nframes, const uint16_t* S, long long s_stride,

@@ -15,6 +15,8 @@
 // SPEC S:300, reading c3) is recomputed from the census images on the fly:
 //   C = popc(cl(x,y) ^ cr(x-delta,y)) if both windows are valid, else nb.
 // The next pixel's census word and S vector are prefetched one step ahead.
+// SGBM (CV = true): the cost is read from the block-cost volume CB (sgbm.cu,
+// PAPER.md P:291, reading c19) instead of the census images.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -72,11 +74,11 @@ template <> __device__ __forceinline__ void store_s<8>(uint16_t* dst, const int 
                                                 v[4] | (v[5] << 16), v[6] | (v[7] << 16));
 }
 
-template <int DPL, typename SigT, bool FIRST>
+template <int DPL, typename SigT, bool FIRST, bool CV>
 __global__ void __launch_bounds__(128)
 sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
                const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base, long long sig_stride,
-               uint16_t* __restrict__ S_base, long long s_stride)
+               uint16_t* __restrict__ S_base, long long s_stride, const uint16_t* __restrict__ cv_base)
 {
     const int chain = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -85,6 +87,7 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
     const SigT* cl = cl_base + frame * sig_stride;
     const SigT* cr = cr_base + frame * sig_stride;
     uint16_t* S = S_base + frame * s_stride;
+    const uint16_t* CVf = CV ? cv_base + frame * s_stride : nullptr;
     const bool active = lane < act;
     const int d0 = lane * DPL;
 
@@ -95,42 +98,47 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
     int M = 0;
     bool first = true;
     // prefetch state for the current pixel
-    SigT nl = cl[(long long)y * p.W + x];
+    SigT nl = CV ? (SigT)0 : cl[(long long)y * p.W + x];
     SigT nr[DPL];
-    int ns[DPL];
+    int ns[DPL], nc[DPL];
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
         const int xr = x - p.min_disp - d0 - j;
-        nr[j] = (active && xr >= 0) ? cr[(long long)y * p.W + xr] : (SigT)0;
+        nr[j] = (!CV && active && xr >= 0) ? cr[(long long)y * p.W + xr] : (SigT)0;
         ns[j] = 0;
+        nc[j] = 0;
     }
     if (!FIRST && active) load_s<DPL>(S + ((long long)y * p.W + x) * p.D + d0, ns);
+    if (CV && active) load_s<DPL>(CVf + ((long long)y * p.W + x) * p.D + d0, nc);
 
     while (true) {
         const SigT sl = nl;
         SigT sr[DPL];
-        int sv[DPL];
+        int sv[DPL], sc[DPL];
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) { sr[j] = nr[j]; sv[j] = ns[j]; }
+        for (int j = 0; j < DPL; ++j) { sr[j] = nr[j]; sv[j] = ns[j]; sc[j] = nc[j]; }
         const int cx = x, cy = y;
         const bool vl = census_valid(p, cx, cy);
         x += rx; y += ry;
         const bool more = x >= 0 && x < p.W && y >= 0 && y < p.H;
         if (more) {                       // prefetch the next pixel of the line
-            nl = cl[(long long)y * p.W + x];
+            if (!CV) {
+                nl = cl[(long long)y * p.W + x];
 #pragma unroll
-            for (int j = 0; j < DPL; ++j) {
-                const int xr = x - p.min_disp - d0 - j;
-                nr[j] = (active && xr >= 0) ? cr[(long long)y * p.W + xr] : (SigT)0;
+                for (int j = 0; j < DPL; ++j) {
+                    const int xr = x - p.min_disp - d0 - j;
+                    nr[j] = (active && xr >= 0) ? cr[(long long)y * p.W + xr] : (SigT)0;
+                }
             }
             if (!FIRST && active) load_s<DPL>(S + ((long long)y * p.W + x) * p.D + d0, ns);
+            if (CV && active) load_s<DPL>(CVf + ((long long)y * p.W + x) * p.D + d0, nc);
         }
         // matching cost of the current pixel
         int c[DPL];
 #pragma unroll
         for (int j = 0; j < DPL; ++j) {
             const int xr = cx - p.min_disp - d0 - j;
-            c[j] = (vl && xr >= p.R) ? popc_sig(sl ^ sr[j]) : p.nb;
+            c[j] = CV ? sc[j] : ((vl && xr >= p.R) ? popc_sig(sl ^ sr[j]) : p.nb);
         }
         int Ln[DPL];
         if (first) {
@@ -173,27 +181,30 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
 template <int DPL, typename SigT>
 static void launch_dir_t(const DevParams& p, int nframes, int rx, int ry, bool first, int act,
                          const void* cl, const void* cr, long long sig_stride,
-                         uint16_t* S, long long s_stride, cudaStream_t s)
+                         uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv)
 {
     const int n = num_chains(p, rx, ry);
     dim3 grid((n + 3) / 4, nframes), block(128);
-    if (first)
-        sgm_dir_kernel<DPL, SigT, true><<<grid, block, 0, s>>>(p, rx, ry, n, act,
-            (const SigT*)cl, (const SigT*)cr, sig_stride, S, s_stride);
-    else
-        sgm_dir_kernel<DPL, SigT, false><<<grid, block, 0, s>>>(p, rx, ry, n, act,
-            (const SigT*)cl, (const SigT*)cr, sig_stride, S, s_stride);
+    const SigT* l = (const SigT*)cl;
+    const SigT* r = (const SigT*)cr;
+    if (cv) {
+        if (first) sgm_dir_kernel<DPL, SigT, true, true><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
+        else sgm_dir_kernel<DPL, SigT, false, true><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
+    } else {
+        if (first) sgm_dir_kernel<DPL, SigT, true, false><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
+        else sgm_dir_kernel<DPL, SigT, false, false><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
+    }
 }
 
 template <typename SigT>
 static bool launch_dir_sig(const DevParams& p, int nframes, int rx, int ry, bool first,
                            const void* cl, const void* cr, long long sig_stride,
-                           uint16_t* S, long long s_stride, cudaStream_t s)
+                           uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv)
 {
     // D = DPL * act with act = 32 (D % 32 == 0) or 16 (D % 32 == 16)
     const int act = (p.D % 32 == 0) ? 32 : 16;
     const int dpl = p.D / act;
-#define ASD_DIR_CASE(K) case K: launch_dir_t<K, SigT>(p, nframes, rx, ry, first, act, cl, cr, sig_stride, S, s_stride, s); return true;
+#define ASD_DIR_CASE(K) case K: launch_dir_t<K, SigT>(p, nframes, rx, ry, first, act, cl, cr, sig_stride, S, s_stride, s, cv); return true;
     switch (dpl) {
         ASD_DIR_CASE(1) ASD_DIR_CASE(2) ASD_DIR_CASE(3) ASD_DIR_CASE(4) ASD_DIR_CASE(5)
         ASD_DIR_CASE(6) ASD_DIR_CASE(7) ASD_DIR_CASE(8) ASD_DIR_CASE(9) ASD_DIR_CASE(11)
@@ -205,11 +216,11 @@ static bool launch_dir_sig(const DevParams& p, int nframes, int rx, int ry, bool
 
 bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
                     const void* cl, const void* cr, long long sig_stride,
-                    uint16_t* S, long long s_stride, cudaStream_t s)
+                    uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv)
 {
     if (p.nb <= 32)
-        return launch_dir_sig<uint32_t>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s);
-    return launch_dir_sig<unsigned long long>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s);
+        return launch_dir_sig<uint32_t>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s, cv);
+    return launch_dir_sig<unsigned long long>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s, cv);
 }
 
 }  // namespace asd

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_version_and_strerror(lib):
-    assert lib.asd_version() == 1
+    assert lib.asd_version() == 2
     assert lib.asd_strerror(0) == b"ok"
     assert lib.asd_strerror(-2) == b"unsupported configuration"
 
@@ -60,6 +60,9 @@ def test_sm100a_only_cubin():
     (dict(focal_px=0.0), asd.ASD_E_INVALID_ARG),
     (dict(lr_max_diff=float("nan")), asd.ASD_E_INVALID_ARG),
     (dict(width=3), asd.ASD_E_INVALID_ARG),
+    (dict(block_w=2), asd.ASD_E_INVALID_ARG),                    # SGBM block must be odd
+    (dict(block_h=17), asd.ASD_E_INVALID_ARG),                   # <= 15
+    (dict(block_w=15, block_h=15, p2=6000), asd.ASD_E_UNSUPPORTED),  # 8*(225*12+p2) > 65535
 ])
 def test_validation(lib, kw, code):
     d = dict(width=64, height=48, num_disp=16, census_w=5, census_h=5)
