@@ -115,6 +115,23 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def run_params(cfg, block: int) -> dict:
+    """Config parameters; block > 1 = SGBM with P1 = 8*area, P2 = 32*area."""
+    d = cfg.params_dict()
+    if block > 1:
+        d.update(block_w=block, block_h=block, p1=8 * block * block, p2=32 * block * block)
+    return d
+
+
+def workload(block: int) -> str:
+    if block > 1:
+        a = block * block
+        return (f"C-SGBM{block}x{block}: 1280x720, D=128, census 9x7, {block}x{block} block, "
+                f"P1={8 * a} P2={32 * a}, 8-path SGM, uniqueness 10%, LR 1 px, sub-pixel, depth")
+    return ("C: 1280x720, D=128, census 9x7, P1=8 P2=32, 8-path SGM, uniqueness 10%, LR 1 px, "
+            "sub-pixel, depth")
+
+
 # ----------------------------------------------------------------- oracle (CPU)
 def oracle_workers():
     cores = len(os.sched_getaffinity(0))
@@ -126,11 +143,11 @@ def oracle_workers():
     return max(1, min(cores, mem_frames, 32)), cores
 
 
-def oracle_frames_parallel(cfg, Ls, Rs, nworkers):
+def oracle_frames_parallel(params, Ls, Rs, nworkers):
     """The oracle as it stands: one full frame per worker thread (ctypes releases
     the GIL, so the C oracle runs on nworkers host cores)."""
     import oracle
-    p = oracle.Params(**cfg.params_dict())
+    p = oracle.Params(**params)
     oracle.lib()
     out = [None] * nworkers
 
@@ -146,12 +163,13 @@ def oracle_frames_parallel(cfg, Ls, Rs, nworkers):
     return time.perf_counter() - t0, out
 
 
-def cpu_baseline(cfg, Ls, Rs):
+def cpu_baseline(params, Ls, Rs):
     nworkers, cores = oracle_workers()
-    wall, _ = oracle_frames_parallel(cfg, Ls, Rs, nworkers)
+    wall, _ = oracle_frames_parallel(params, Ls, Rs, nworkers)
     return {"value": round(nworkers / wall, 4), "unit": "frames/s", "cores": nworkers,
             "kind": "oracle",
-            "sample": f"{nworkers} full config-C frames (1280x720 D128 8-path), one per host thread "
+            "sample": f"{nworkers} full config-C frames (1280x720 D128 8-path"
+                      f"{', SGBM block' if params.get('block_w', 1) > 1 else ''}), one per host thread "
                       f"on {nworkers} of {cores} cores, plain-C oracle (gcc -O2), wall {wall:.1f} s"}
 
 
@@ -162,13 +180,14 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = synth.CONFIGS[CONFIG]
+    params = run_params(cfg, args.block)
     Ls, Rs = synth.frame_pool(cfg, min(POOL, 4))
     nworkers, cores = oracle_workers()
     for _ in range(args.warmup):
-        oracle_frames_parallel(cfg, Ls, Rs, nworkers)
+        oracle_frames_parallel(params, Ls, Rs, nworkers)
     tot = 0.0
     for _ in range(args.steps):
-        w, _ = oracle_frames_parallel(cfg, Ls, Rs, nworkers)
+        w, _ = oracle_frames_parallel(params, Ls, Rs, nworkers)
         tot += w
     frames = nworkers * args.steps
     value = frames / tot
@@ -177,7 +196,7 @@ def run_reference(args):
             "ms_per_step": round(1000 * tot / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 6),
-            "config": {"workload": "C: 1280x720, D=128, census 9x7, 8-path SGM, LR + sub-pixel + depth",
+            "config": {"workload": workload(args.block),
                        "frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "frames/s", "cores": nworkers,
                              "kind": "oracle",
@@ -200,6 +219,8 @@ def main():
                     help="frames per asd_depth_batch chunk (0: a whole number of cluster waves, ~32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--block", type=int, default=1,
+                    help="SGBM block size (odd; 1 = SGM, the headline line)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -222,6 +243,7 @@ def main():
     torch.cuda.set_device(dev)
 
     cfg = synth.CONFIGS[CONFIG]
+    params = run_params(cfg, args.block)
     B = args.frames
     H, W = cfg.height, cfg.width
     pool_L, pool_R = synth.frame_pool(cfg, POOL)
@@ -233,11 +255,11 @@ def main():
     depth = torch.empty(B, H, W, device=dev)
     stats = torch.zeros(B, 4, dtype=torch.int32, device=dev)
     if args.max_batch <= 0:
-        probe = asd.Stereo(asd.Params(**cfg.params_dict()), local, 1)
+        probe = asd.Stereo(asd.Params(**params), local, 1)
         fpw = probe.frames_per_wave
         probe.close()
         args.max_batch = max(1, (MAX_BATCH // fpw) * fpw) if fpw > 0 else MAX_BATCH
-    st = asd.Stereo(asd.Params(**cfg.params_dict()), local, args.max_batch)
+    st = asd.Stereo(asd.Params(**params), local, args.max_batch)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -364,15 +386,14 @@ def main():
                         "note": "stage_ms are per-kernel event sums; row/wta/lr overlap the sweeps"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cfg, pool_L, pool_R)
+            cpu = cpu_baseline(params, pool_L, pool_R)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
             "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 3),
-            "config": {"workload": "C: 1280x720, D=128, census 9x7, P1=8 P2=32, 8-path SGM, "
-                                   "uniqueness 10%, LR 1 px, sub-pixel, depth",
+            "config": {"workload": workload(args.block),
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
                        "l2": "inputs larger than L2 (236 MB/step/GPU) + per-frame scratch > L2",
