@@ -42,7 +42,8 @@ class OracleParams(ctypes.Structure):
                 ("paths", ctypes.c_int32), ("uniqueness", ctypes.c_int32),
                 ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
                 ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
-                ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32)]
+                ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32),
+                ("median_ksize", ctypes.c_int32)]
 
 
 @dataclass
@@ -64,6 +65,7 @@ class Params:
     baseline_m: float = 0.055
     block_w: int = 1          # SGBM block; 1 x 1 = plain SGM
     block_h: int = 1
+    median_ksize: int = 0     # 0 (off), 3, 5
 
     @property
     def nbits(self) -> int:
@@ -73,7 +75,8 @@ class Params:
         return OracleParams(self.width, self.height, self.min_disp, self.num_disp,
                             self.census_w, self.census_h, self.p1, self.p2, self.paths,
                             self.uniqueness, self.lr_max_diff, self.subpixel,
-                            self.focal_px, self.baseline_m, self.block_w, self.block_h)
+                            self.focal_px, self.baseline_m, self.block_w, self.block_h,
+                            self.median_ksize)
 
 
 _lib = None
@@ -199,6 +202,34 @@ def lr_depth(p: Params, dl, dr, mask_r, mask):
     z = np.empty((p.height, p.width), np.float64)
     lib().oracle_lr_depth(ctypes.byref(p.c()), _p(dl), _p(dr), _p(mask_r), _p(m), _p(disp), _p(z))
     return m, disp, z
+
+
+def median(p: Params, dl: np.ndarray, mask: np.ndarray) -> np.ndarray:
+    """O9 -- lower median over the valid k x k neighbours (reading c20)."""
+    dl = np.ascontiguousarray(dl, np.float32)
+    mask = np.ascontiguousarray(mask, np.uint8)
+    out = np.empty_like(dl)
+    lib().oracle_median(ctypes.byref(p.c()), _p(dl), _p(mask), _p(out))
+    return out
+
+
+class OracleCamera(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("fx", ctypes.c_float), ("fy", ctypes.c_float),
+                ("cx", ctypes.c_float), ("cy", ctypes.c_float)]
+
+
+def register(ir: tuple, rgb: tuple, R, t, z: np.ndarray) -> np.ndarray:
+    """O10 -- depth registration into the RGB frame (reading c21).
+    ir / rgb = (width, height, fx, fy, cx, cy); R 3x3, t 3; z f32[H_ir][W_ir]
+    (NaN = invalid) -> f32[H_rgb][W_rgb] (NaN = no sample)."""
+    z = np.ascontiguousarray(z, np.float32)
+    R = np.ascontiguousarray(np.asarray(R, np.float32).reshape(9))
+    t = np.ascontiguousarray(np.asarray(t, np.float32).reshape(3))
+    ci, cr = OracleCamera(*ir), OracleCamera(*rgb)
+    out = np.empty((rgb[1], rgb[0]), np.float32)
+    lib().oracle_register(ctypes.byref(ci), ctypes.byref(cr), _p(R), _p(t), _p(z), _p(out))
+    return out
 
 
 def checksum(dstar: np.ndarray, mask: np.ndarray) -> int:

@@ -24,7 +24,9 @@
  *   O5 sub-pixel   parabola through (d*-1, d*, d*+1)
  *   O6 right view  same WTA/sub-pixel on S_R(x,d) = S(x+delta,d)  (reading c10)
  *   O7 LR check    |dl - dr(x - round(dl))| <= lr
+ *   O9 median      lower median of the valid k x k neighbours
  *   O8 depth       z = f*b/d
+ *   O10 register   unproject, transform, reproject, z-buffer
  *
  * Every function follows the definition in that order, with no blocking,
  * fusion or reordering.  SGM is organised exactly as its definition reads:
@@ -51,6 +53,7 @@ typedef struct {
     int32_t subpixel;          /* 0/1 */
     float   focal_px, baseline_m;
     int32_t block_w, block_h;  /* SGBM block (odd); 1 x 1 = plain SGM */
+    int32_t median_ksize;      /* 0 (off), 3 or 5 */
 } oracle_params;
 
 /* mask bits */
@@ -382,11 +385,44 @@ void oracle_wta_right(const oracle_params* p, const uint32_t* S,
     free(sr); free(defined);
 }
 
-/* O7 + O8.  LR ("left-right consistency check", readings c11,
- * c12): evaluated iff lr >= 0 and (mask & 3) == 0; xr = x - (int)floorf(dl +
- * 0.5f); invalid if xr outside [0,W), mask_r(xr) != 0 or |dl - dr(xr)| > lr.
- * Depth (reading c14): OM_NONPOS iff dl <= 0 (always evaluated);
- * if mask == 0: disp = dl, depth = f*b/dl in fp64; else both NaN. */
+/* O9 median ("median filtering"; S:342-347 [OP] median, reading c20):
+ * for a pixel valid after the LR check ((mask & 7) == 0), the lower median
+ * (element (n-1)/2 of the ascending order) of dl over the pixels of the
+ * k x k window inside the image that are valid too (n >= 1: the pixel itself);
+ * invalid pixels keep dl.  ksize 0 = identity. */
+static int cmp_float(const void* a, const void* b)
+{
+    float x = *(const float*)a, y = *(const float*)b;
+    return (x > y) - (x < y);
+}
+void oracle_median(const oracle_params* p, const float* dl, const uint8_t* mask, float* out)
+{
+    int W = p->width, H = p->height, k = p->median_ksize / 2;
+    float v[64];
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t i = (size_t)y * W + x;
+            out[i] = dl[i];
+            if (p->median_ksize <= 0 || (mask[i] & 7u) != 0) continue;
+            int n = 0;
+            for (int yy = y - k; yy <= y + k; ++yy)
+                for (int xx = x - k; xx <= x + k; ++xx) {
+                    if (xx < 0 || xx >= W || yy < 0 || yy >= H) continue;
+                    size_t j = (size_t)yy * W + xx;
+                    if ((mask[j] & 7u) == 0) v[n++] = dl[j];
+                }
+            qsort(v, (size_t)n, sizeof(float), cmp_float);
+            out[i] = v[(n - 1) / 2];
+        }
+}
+
+/* O7 + O9 + O8.  LR ("left-right consistency check", readings
+ * c11, c12): evaluated iff lr >= 0 and (mask & 3) == 0; xr = x - (int)floorf(dl
+ * + 0.5f); invalid if xr outside [0,W), mask_r(xr) != 0 or |dl - dr(xr)| > lr.
+ * Then the median (O9) of the LR-checked map when median_ksize > 0 (S:368
+ * order: lr_check -> median -> disp_to_depth).  Depth (reading
+ * c14) on that value d: OM_NONPOS iff d <= 0 (always evaluated); if mask == 0:
+ * disp = d, depth = f*b/d in fp64; else both NaN. */
 void oracle_lr_depth(const oracle_params* p, const float* dl, const float* dr,
                      const uint8_t* mask_r, uint8_t* mask, float* disp, double* depth)
 {
@@ -404,6 +440,15 @@ void oracle_lr_depth(const oracle_params* p, const float* dl, const float* dr,
                     if (mask_r[j] != 0 || fabsf(d - dr[j]) > p->lr_max_diff) m |= OM_LR;
                 }
             }
+            mask[i] = m;
+        }
+    float* dm = (float*)malloc(sizeof(float) * (size_t)W * H);
+    oracle_median(p, dl, mask, dm);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t i = (size_t)y * W + x;
+            uint8_t m = mask[i];
+            float d = dm[i];
             if (d <= 0.0f) m |= OM_NONPOS;
             mask[i] = m;
             if (m == 0) {
@@ -414,6 +459,52 @@ void oracle_lr_depth(const oracle_params* p, const float* dl, const float* dr,
                 depth[i] = NAN;
             }
         }
+    free(dm);
+}
+
+/* O10 depth registration ("an optional depth registration that aligns
+ * the depth map to the RGB camera frame"; S:357-365 [OP] register_depth,
+ * reading c21).  Pinhole cameras without distortion; pixel (x, y) sits at
+ * image coordinate (x, y).  Each source pixel with finite z > 0 is unprojected
+ * with the IR intrinsics, moved into the RGB frame (P' = R P + t, R row-major),
+ * reprojected with the RGB intrinsics; the target pixel is
+ * (floor(u + 0.5), floor(v + 0.5)) and the z-buffer keeps the smallest Z'.
+ * Targets never hit are NaN.  The coordinate arithmetic decides integers (the
+ * target pixel), so it is done in fp32, one IEEE operation at a time in the
+ * order written (the kernel does the same, reading c21):
+ *   a = ((float)x - cx) * z / fx,  b = ((float)y - cy) * z / fy
+ *   X' = ((R00 a + R01 b) + R02 z) + t0   (likewise Y', Z')
+ *   u = (X' / Z') * fx' + cx',  v = (Y' / Z') * fy' + cy'                  */
+typedef struct { int32_t width, height; float fx, fy, cx, cy; } oracle_camera;
+
+void oracle_register(const oracle_camera* ir, const oracle_camera* rgb, const float* R, const float* t,
+                     const float* z_in, float* z_out)
+{
+    size_t nt = (size_t)rgb->width * rgb->height;
+    for (size_t i = 0; i < nt; ++i) z_out[i] = INFINITY;
+    for (int y = 0; y < ir->height; ++y)
+        for (int x = 0; x < ir->width; ++x) {
+            float z = z_in[(size_t)y * ir->width + x];
+            if (!(z > 0.0f) || isinf(z)) continue;        /* NaN (invalid) or non-positive */
+            float a = (float)x - ir->cx; a = a * z; a = a / ir->fx;
+            float b = (float)y - ir->cy; b = b * z; b = b / ir->fy;
+            float P[3];
+            for (int r = 0; r < 3; ++r) {
+                float s = R[3 * r] * a;
+                s = s + R[3 * r + 1] * b;
+                s = s + R[3 * r + 2] * z;
+                P[r] = s + t[r];
+            }
+            if (!(P[2] > 0.0f)) continue;
+            float u = P[0] / P[2]; u = u * rgb->fx; u = u + rgb->cx;
+            float v = P[1] / P[2]; v = v * rgb->fy; v = v + rgb->cy;
+            float uu = u + 0.5f, vv = v + 0.5f;
+            if (!(uu >= 0.0f && uu < (float)rgb->width && vv >= 0.0f && vv < (float)rgb->height)) continue;
+            int iu = (int)floorf(uu), iv = (int)floorf(vv);
+            size_t j = (size_t)iv * rgb->width + iu;
+            if (P[2] < z_out[j]) z_out[j] = P[2];
+        }
+    for (size_t i = 0; i < nt; ++i) if (isinf(z_out[i])) z_out[i] = NAN;
 }
 
 /* murmur3 fmix32 -- per-frame checksum of the bit-exact outputs. */
