@@ -77,7 +77,11 @@ extern "C" {
  *       SPEC S:258; reading c19): odd, 1..15; 0 is read as 1.
  *       1 x 1 = plain SGM.  The cost becomes CB(x,y,d) = sum over the block
  *       of C(x+u, y+v, d), nb for block positions off the image.  A block
- *       larger than 1 x 1 runs on engine D1 (the D3 packing holds 8-bit costs). */
+ *       larger than 1 x 1 runs on engine D1 (the D3 packing holds 8-bit costs).
+ *   median_ksize: 0, 3 or 5 ("median filtering"; SPEC S:342-347;
+ *       reading c20): after the LR check, a pixel with no BORDER/UNIQUE/LR bit
+ *       takes the lower median of dl over the valid k x k neighbours (itself
+ *       included); the non-positive test and the depth use that value. */
 /* Aggregation designs:
  *   ASD_ENGINE_D1  one warp-per-line kernel per path direction, u16 S volume
  *                  read-modify-written in HBM (any configuration above)
@@ -104,6 +108,7 @@ typedef struct asd_params {
     float   focal_px, baseline_m;
     int32_t engine;      /* ASD_ENGINE_* (0 = auto) */
     int32_t block_w, block_h;   /* SGBM block, 1 x 1 (or 0) = SGM */
+    int32_t median_ksize;       /* median filter after the LR check: 0 (off), 3, 5 */
 } asd_params;
 
 /* Per-frame statistics; exact integers except depth_sum.
@@ -205,6 +210,28 @@ int asd_group(const asd_ctx* ctx);
 /* Human-readable description of the chosen kernel geometry (cluster size,
  * CTA shape, residency), NUL-terminated into buf[0..n).  Returns its length. */
 int asd_plan_info(const asd_ctx* ctx, char* buf, int n);
+
+/* ---- depth registration into the RGB frame ----
+ * PAPER.md P:289 "an optional depth registration that aligns the depth map to
+ * the RGB camera frame"; reading c21.
+ * Pinhole cameras without distortion; pixel (x, y) is at image coordinate
+ * (x, y).  A source pixel with finite depth z > 0 is unprojected with `ir`,
+ * moved by P' = R P + t (R 3x3 row-major, t 3: host arrays, IR-camera to
+ * RGB-camera coordinates, metres), reprojected with `rgb` to the target pixel
+ * (floor(u + 0.5), floor(v + 0.5)); the z-buffer keeps the smallest Z'.
+ * depth: device [n][ir.height][ir.width] f32 (NaN = invalid, e.g. the
+ * asd_depth output); out: device [n][rgb.height][rgb.width] f32, NaN where no
+ * sample lands.  Both owned by the caller; enqueued on cuda_stream (NULL =
+ * default stream), no host synchronisation.  Returns ASD_OK,
+ * ASD_E_INVALID_ARG (NULL pointer, n < 0, non-positive sizes or focal lengths,
+ * non-finite R/t/intrinsics) or ASD_E_CUDA. */
+typedef struct asd_camera {
+    int32_t width, height;
+    float   fx, fy, cx, cy;
+} asd_camera;
+
+int asd_register_depth(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
+                       int n, const float* depth, float* out, void* cuda_stream);
 
 /* ---- live stage timing (CUDA events on the launching stream) ----
  * asd_profile_begin(ctx, max_launches) pre-creates events for up to

@@ -36,7 +36,8 @@ class asd_params(ctypes.Structure):
                 ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
                 ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
                 ("engine", ctypes.c_int32),
-                ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32)]
+                ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32),
+                ("median_ksize", ctypes.c_int32)]
 
 
 class asd_frame_stats(ctypes.Structure):
@@ -81,6 +82,8 @@ SYMBOLS = [
     ("asd_profile_end", _I, [_VP, ctypes.POINTER(asd_stage_times)]),
     ("asd_profile_timeline", _I, [_VP, _I, ctypes.POINTER(ctypes.c_int32),
                                   ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
+    ("asd_register_depth", _I, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                _I, _VP, _VP, _VP]),
     ("asd_strerror", ctypes.c_char_p, [_I]),
     ("asd_last_error", ctypes.c_char_p, [_VP]),
 ]
@@ -124,12 +127,13 @@ class Params:
     engine: int = 0            # ASD_ENGINE_AUTO (0), _D1 (1), _D3 (3)
     block_w: int = 1           # SGBM block (reading c19); 1 x 1 = SGM
     block_h: int = 1
+    median_ksize: int = 0      # 0 / 3 / 5 (reading c20)
 
     def c(self) -> asd_params:
         return asd_params(self.width, self.height, self.min_disp, self.num_disp, self.census_w,
                           self.census_h, self.p1, self.p2, self.paths, self.uniqueness,
                           self.lr_max_diff, self.subpixel, self.focal_px, self.baseline_m,
-                          self.engine, self.block_w, self.block_h)
+                          self.engine, self.block_w, self.block_h, self.median_ksize)
 
     @property
     def nbits(self) -> int:
@@ -152,6 +156,31 @@ def _stream(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+class asd_camera(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("fx", ctypes.c_float), ("fy", ctypes.c_float),
+                ("cx", ctypes.c_float), ("cy", ctypes.c_float)]
+
+
+def register_depth(ir: tuple, rgb: tuple, R, t, depth, out=None, stream=None):
+    """asd_register_depth: depth maps (torch f32 CUDA, [n][H][W] or [H][W], NaN =
+    invalid) into the RGB frame.  ir / rgb = (width, height, fx, fy, cx, cy);
+    R 3x3, t 3 (IR -> RGB coordinates).  Returns out [n][H_rgb][W_rgb]."""
+    import torch
+    squeeze = depth.dim() == 2
+    d = depth.unsqueeze(0) if squeeze else depth
+    assert d.is_cuda and d.dtype == torch.float32 and d.is_contiguous()
+    n = d.shape[0]
+    if out is None:
+        out = torch.empty(n, rgb[1], rgb[0], device=d.device, dtype=torch.float32)
+    Rc = (ctypes.c_float * 9)(*[float(v) for v in list(__import__("numpy").asarray(R, "float32").reshape(9))])
+    tc = (ctypes.c_float * 3)(*[float(v) for v in list(__import__("numpy").asarray(t, "float32").reshape(3))])
+    ci, cr = asd_camera(*ir), asd_camera(*rgb)
+    _check(load().asd_register_depth(ctypes.byref(ci), ctypes.byref(cr), Rc, tc, n, _ptr(d), _ptr(out),
+                                     _stream(stream)))
+    return out[0] if squeeze else out
 
 
 def scratch_bytes(params: Params, max_batch: int = 1) -> int:

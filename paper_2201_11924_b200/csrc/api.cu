@@ -132,6 +132,10 @@ int validate(const asd_params* p, char* why, size_t n)
         snprintf(why, n, "block_w/block_h must be odd in [1, 15] (0 = 1); got %d x %d", p->block_w, p->block_h);
         return ASD_E_INVALID_ARG;
     }
+    if (p->median_ksize != 0 && p->median_ksize != 3 && p->median_ksize != 5) {
+        snprintf(why, n, "median_ksize must be 0, 3 or 5 (got %d)", p->median_ksize);
+        return ASD_E_INVALID_ARG;
+    }
     if (bw * bh == 1 && nb + p->p2 > 255) {
         snprintf(why, n, "nb + p2 = %d > 255 (per-path cost must fit 8 bits)", nb + p->p2);
         return ASD_E_UNSUPPORTED;
@@ -177,6 +181,7 @@ DevParams make_dev(const asd_params* p)
     d.ncell = d.npx * p->num_disp;
     d.bw = p->block_w == 0 ? 1 : p->block_w;
     d.bh = p->block_h == 0 ? 1 : p->block_h;
+    d.median = p->median_ksize;
     return d;
 }
 
@@ -799,6 +804,32 @@ int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
     if (o.mask_r) cudaMemcpyAsync(o.mask_r, ctx->mask_r, npx, cudaMemcpyDeviceToDevice, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_err(ctx, "debug extraction failed: %s", cudaGetErrorString(e)); return ASD_E_CUDA; }
+    return ASD_OK;
+}
+
+int asd_register_depth(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
+                       int n, const float* depth, float* out, void* cuda_stream)
+{
+    if (!ir || !rgb || !R || !t || n < 0 || (n > 0 && (!depth || !out))) {
+        set_err(nullptr, "asd_register_depth: NULL argument or n < 0");
+        return ASD_E_INVALID_ARG;
+    }
+    auto cam_ok = [](const asd_camera* c) {
+        return c->width > 0 && c->height > 0 && (long long)c->width * c->height <= (1ll << 26) &&
+               std::isfinite(c->fx) && std::isfinite(c->fy) && c->fx > 0.0f && c->fy > 0.0f &&
+               std::isfinite(c->cx) && std::isfinite(c->cy);
+    };
+    if (!cam_ok(ir) || !cam_ok(rgb)) {
+        set_err(nullptr, "asd_register_depth: camera sizes / intrinsics out of range");
+        return ASD_E_INVALID_ARG;
+    }
+    for (int i = 0; i < 9; ++i) if (!std::isfinite(R[i])) { set_err(nullptr, "R not finite"); return ASD_E_INVALID_ARG; }
+    for (int i = 0; i < 3; ++i) if (!std::isfinite(t[i])) { set_err(nullptr, "t not finite"); return ASD_E_INVALID_ARG; }
+    if (n == 0) return ASD_OK;
+    if (launch_register(ir, rgb, R, t, n, depth, out, (cudaStream_t)cuda_stream) != 0) {
+        set_err(nullptr, "asd_register_depth: %s", cudaGetErrorString(cudaGetLastError()));
+        return ASD_E_CUDA;
+    }
     return ASD_OK;
 }
 

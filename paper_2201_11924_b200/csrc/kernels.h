@@ -21,6 +21,10 @@ bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
                     uint16_t* S, long long s_stride, cudaStream_t s,
                     const uint16_t* cv = nullptr);
 
+// Depth registration (register.cu): fill, scatter with an atomicMin z-buffer, finish.
+int launch_register(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
+                    int n, const float* depth, float* out, cudaStream_t s);
+
 // SGBM block cost volume CB (u16 [H][W][D] per frame), sgbm.cu.
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
                        long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s);

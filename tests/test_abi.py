@@ -63,6 +63,7 @@ def test_sm100a_only_cubin():
     (dict(block_w=2), asd.ASD_E_INVALID_ARG),                    # SGBM block must be odd
     (dict(block_h=17), asd.ASD_E_INVALID_ARG),                   # <= 15
     (dict(block_w=15, block_h=15, p2=6000), asd.ASD_E_UNSUPPORTED),  # 8*(225*12+p2) > 65535
+    (dict(median_ksize=4), asd.ASD_E_INVALID_ARG),               # 0, 3 or 5
 ])
 def test_validation(lib, kw, code):
     d = dict(width=64, height=48, num_disp=16, census_w=5, census_h=5)
@@ -86,3 +87,18 @@ def test_scratch_bytes(lib):
 def test_null_ctx_rejected(lib):
     assert lib.asd_depth(None, None, None, None, None, None) == asd.ASD_E_INVALID_ARG
     assert lib.asd_depth_batch(None, 1, None, None, None, None, None, None) == asd.ASD_E_INVALID_ARG
+
+
+def test_register_depth_validation(lib):
+    """asd_register_depth rejects NULL / out-of-range arguments before touching the GPU."""
+    ir = abi.asd_camera(40, 30, 100.0, 100.0, 19.5, 14.5)
+    bad = abi.asd_camera(0, 30, 100.0, 100.0, 19.5, 14.5)
+    R = (ctypes.c_float * 9)(1, 0, 0, 0, 1, 0, 0, 0, 1)
+    t = (ctypes.c_float * 3)(0, 0, 0)
+    reg = lib.asd_register_depth
+    assert reg(None, ctypes.byref(ir), R, t, 1, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert reg(ctypes.byref(ir), ctypes.byref(ir), R, t, -1, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert reg(ctypes.byref(ir), ctypes.byref(bad), R, t, 0, None, None, None) == asd.ASD_E_INVALID_ARG
+    Rn = (ctypes.c_float * 9)(float("nan"), 0, 0, 0, 1, 0, 0, 0, 1)
+    assert reg(ctypes.byref(ir), ctypes.byref(ir), Rn, t, 0, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert reg(ctypes.byref(ir), ctypes.byref(ir), R, t, 0, None, None, None) == asd.ASD_OK
