@@ -258,3 +258,47 @@ def compute(p: Params, left: np.ndarray, right: np.ndarray, debug: bool = False)
     if rc != 0:
         raise MemoryError("oracle_compute: allocation failed")
     return out
+
+
+# ------------------------------------------------------------------ O0 noise
+class OracleNoise(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_double), ("theta", ctypes.c_double), ("mu", ctypes.c_double),
+                ("sigma", ctypes.c_double), ("scale", ctypes.c_double)]
+
+
+D415_NOISE = dict(k=3.98, theta=0.254, mu=-0.231, sigma=0.83, scale=1.0)
+
+
+def philox(ctr, key):
+    """Philox4x32-10 of one 128-bit counter under a 64-bit key (4 x u32 out)."""
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32_10(c, k, o)
+    return list(o)
+
+
+def sensor_noise(clean: np.ndarray, seed: int, frame0: int = 0, view: int = 0, f64: bool = False, **noise):
+    """O0 -- gamma*I + n, quantised to u8 (readings c17, c22).
+    clean [n][H][W] or [H][W] (DN units) -> u8 of the same shape (and the
+    unrounded values when f64)."""
+    q = dict(D415_NOISE); q.update(noise)
+    c = np.ascontiguousarray(clean, np.float64)
+    shp = c.shape
+    c3 = c.reshape((-1,) + shp[-2:])
+    out = np.empty(c3.shape, np.uint8)
+    val = np.empty(c3.shape, np.float64) if f64 else None
+    lib().oracle_sensor_noise(ctypes.byref(OracleNoise(**q)), ctypes.c_uint64(seed), c3.shape[0],
+                              shp[-1], shp[-2], ctypes.c_uint32(frame0), ctypes.c_uint32(view),
+                              _p(c3), _p(out), _p(val) if f64 else None)
+    return (out.reshape(shp), val.reshape(shp)) if f64 else out.reshape(shp)
+
+
+def noise_samples(n: int, seed: int, frame: int = 0, view: int = 0, **noise):
+    """(gamma, n) samples of pixels 0..n-1 of one stream (before the scale blend)."""
+    q = dict(D415_NOISE); q.update(noise)
+    g = np.empty(n, np.float64)
+    a = np.empty(n, np.float64)
+    lib().oracle_noise_samples(ctypes.byref(OracleNoise(**q)), ctypes.c_uint64(seed), n,
+                               ctypes.c_uint32(frame), ctypes.c_uint32(view), _p(g), _p(a))
+    return g, a

@@ -27,6 +27,8 @@
  *   O9 median      lower median of the valid k x k neighbours
  *   O8 depth       z = f*b/d
  *   O10 register   unproject, transform, reproject, z-buffer
+ *   O0 noise       I_noisy = gamma * I_clean + n, gamma ~ Gamma(k, theta),
+ *                  n ~ N(mu, sigma^2), quantised to u8           (c17, c22)
  *
  * Every function follows the definition in that order, with no blocking,
  * fusion or reordering.  SGM is organised exactly as its definition reads:
@@ -569,4 +571,111 @@ done:
     free(cl); free(cr); free(C); free(CB); free(S); free(dsl); free(dsr); free(ml); free(mr);
     free(dl); free(dr); free(disp); free(z);
     return rc;
+}
+
+
+/* ------------------------------------------------------------- O0 noise
+ * Sensor noise front end ("a multiplicative term gamma
+ * modeling the laser speckle and an additive term n modeling camera thermal
+ * noise", I_noisy = gamma * I_clean + n, gamma ~ Gamma(k, theta), n ~ N(mu,
+ * sigma^2); D415 values P:350; readings c17, c22 in DESIGN.md §3).
+ *
+ * Random numbers: Philox4x32-10 (Salmon et al., SC'11: a 10-round Feistel-like
+ * bijection of a 128-bit counter under a 64-bit key; round multipliers
+ * 0xD2511F53 / 0xCD9E8D57, Weyl key increments 0x9E3779B9 / 0xBB67AE85),
+ * key = (seed low, seed high 32 bits), counter = (pixel, attempt, frame, view).
+ * A 32-bit output x maps to the open interval: U(x) = ((x >> 8) + 0.5) / 2^24.
+ * Normal: Box-Muller, z = sqrt(-2 ln U(x0)) cos(2 pi U(x1)).
+ * n: the block with attempt = 0xFFFFFFFF; n = mu + sigma z.
+ * Gamma (Marsaglia & Tsang 2000): k' = k (k >= 1) or k + 1 (k < 1 boost),
+ * d = k' - 1/3, c = 1 / sqrt(9 d); attempt j = 0..15: z from block j, v =
+ * (1 + c z)^3, accept iff v > 0 and ln U(x2) < z^2 / 2 + d - d v + d ln v,
+ * g = d v; for k < 1, g *= U(x3 of block 0)^(1/k); no acceptance in 16
+ * attempts (probability < 1e-25 at k = 3.98) -> g = d.  gamma = g * theta.
+ * Noise scale s: gamma' = k theta + s (gamma - k theta), n' = s n.
+ * Output: clamp(floor(gamma' I + n' + 0.5), 0, 255) as u8 (c17).
+ * All arithmetic in double (the kernel also computes in double).           */
+static void philox_round(uint32_t c[4], const uint32_t k[2])
+{
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0], n2 = hi0 ^ c[3] ^ k[1];
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+}
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    uint32_t k[2] = {key[0], key[1]};
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u; }
+        philox_round(c, k);
+    }
+    for (int i = 0; i < 4; ++i) out[i] = c[i];
+}
+static double unif(uint32_t x) { return ((double)(x >> 8) + 0.5) / 16777216.0; }
+static const double PI_D = 3.14159265358979323846;
+
+typedef struct {
+    double k, theta, mu, sigma, scale;
+} oracle_noise;
+
+static double bm_normal(const uint32_t x[4])
+{
+    return sqrt(-2.0 * log(unif(x[0]))) * cos(2.0 * PI_D * unif(x[1]));
+}
+
+/* gamma and n for one pixel (both before the scale blend) */
+static void noise_pixel(const oracle_noise* q, uint64_t seed, uint32_t pix, uint32_t frame, uint32_t view,
+                        double* gamma, double* n)
+{
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {pix, 0xFFFFFFFFu, frame, view}, x[4];
+    oracle_philox4x32_10(ctr, key, x);
+    *n = q->mu + q->sigma * bm_normal(x);
+    double kk = q->k >= 1.0 ? q->k : q->k + 1.0;
+    double d = kk - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * d);
+    double g = d, boost = 1.0;
+    for (uint32_t j = 0; j < 16; ++j) {
+        ctr[1] = j;
+        oracle_philox4x32_10(ctr, key, x);
+        if (j == 0 && q->k < 1.0) boost = pow(unif(x[3]), 1.0 / q->k);
+        double z = bm_normal(x);
+        double t = 1.0 + c * z;
+        double v = t * t * t;
+        if (v <= 0.0) continue;
+        if (log(unif(x[2])) < 0.5 * z * z + d - d * v + d * log(v)) { g = d * v; break; }
+    }
+    *gamma = g * boost * q->theta;
+}
+
+/* n_images clean images [n][H][W] (double) -> u8 [n][H][W]; image i is frame
+ * frame0 + i of view `view`.  noisy_f64 (may be NULL) gets gamma' I + n' before
+ * rounding. */
+void oracle_sensor_noise(const oracle_noise* q, uint64_t seed, int n_images, int W, int H,
+                         uint32_t frame0, uint32_t view, const double* clean, uint8_t* out, double* noisy_f64)
+{
+    for (int i = 0; i < n_images; ++i)
+        for (int pix = 0; pix < W * H; ++pix) {
+            double g, n;
+            noise_pixel(q, seed, (uint32_t)pix, frame0 + (uint32_t)i, view, &g, &n);
+            double kt = q->k * q->theta;
+            double gs = kt + q->scale * (g - kt), ns = q->scale * n;
+            size_t o = (size_t)i * W * H + pix;
+            double val = gs * clean[o] + ns;
+            if (noisy_f64) noisy_f64[o] = val;
+            double r = floor(val + 0.5);
+            if (r < 0.0) r = 0.0;
+            if (r > 255.0) r = 255.0;
+            out[o] = (uint8_t)r;
+        }
+}
+
+/* The gamma and n samples of pixels 0..n-1 of one (frame, view) stream, for
+ * distribution tests. */
+void oracle_noise_samples(const oracle_noise* q, uint64_t seed, int n, uint32_t frame, uint32_t view,
+                          double* gamma, double* add)
+{
+    for (int i = 0; i < n; ++i) noise_pixel(q, seed, (uint32_t)i, frame, view, gamma + i, add + i);
 }
