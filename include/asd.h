@@ -233,6 +233,28 @@ typedef struct asd_camera {
 int asd_register_depth(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
                        int n, const float* depth, float* out, void* cuda_stream);
 
+/* ---- sensor noise front end ----
+ * I_noisy = gamma * I_clean + n with gamma ~ Gamma(k, theta)
+ * (laser speckle) and n ~ N(mu, sigma^2) (thermal noise); D415 parameters
+ * k = 3.98, theta = 0.254, mu = -0.231, sigma = 0.83.  Readings c17
+ * (DN units, round half up, clamp to u8) and c22 (sampling, random streams,
+ * noise scale) in DESIGN.md §3.  clean: device [n][height][width] f32 clean IR
+ * intensities in DN units; out: device [n][height][width] u8 (the input of
+ * asd_depth*).  Image i draws from the Philox4x32-10 stream keyed by seed with
+ * counter (pixel, attempt, frame0 + i, view), so left (view 0) and right
+ * (view 1) images of a frame and consecutive frames are independent and any
+ * tiling of the work reproduces the same values.  Enqueued on cuda_stream.
+ * Returns ASD_OK, ASD_E_INVALID_ARG (NULL pointer, n < 0, sizes, k/theta <= 0,
+ * sigma < 0, non-finite parameters) or ASD_E_CUDA. */
+typedef struct asd_noise {
+    double k, theta;      /* gamma shape and scale */
+    double mu, sigma;     /* additive Gaussian mean and standard deviation (DN) */
+    double scale;         /* noise strength s: gamma' = k theta + s (gamma - k theta), n' = s n */
+} asd_noise;
+
+int asd_sensor_noise(const asd_noise* q, uint64_t seed, int n, int width, int height,
+                     uint32_t frame0, uint32_t view, const float* clean, uint8_t* out, void* cuda_stream);
+
 /* ---- live stage timing (CUDA events on the launching stream) ----
  * asd_profile_begin(ctx, max_launches) pre-creates events for up to
  * max_launches kernel launches; from then on every launch the context enqueues

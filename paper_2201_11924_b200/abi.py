@@ -84,6 +84,8 @@ SYMBOLS = [
                                   ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     ("asd_register_depth", _I, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 _I, _VP, _VP, _VP]),
+    ("asd_sensor_noise", _I, [ctypes.c_void_p, ctypes.c_uint64, _I, _I, _I, ctypes.c_uint32,
+                              ctypes.c_uint32, _VP, _VP, _VP]),
     ("asd_strerror", ctypes.c_char_p, [_I]),
     ("asd_last_error", ctypes.c_char_p, [_VP]),
 ]
@@ -180,6 +182,31 @@ def register_depth(ir: tuple, rgb: tuple, R, t, depth, out=None, stream=None):
     ci, cr = asd_camera(*ir), asd_camera(*rgb)
     _check(load().asd_register_depth(ctypes.byref(ci), ctypes.byref(cr), Rc, tc, n, _ptr(d), _ptr(out),
                                      _stream(stream)))
+    return out[0] if squeeze else out
+
+
+class asd_noise(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_double), ("theta", ctypes.c_double), ("mu", ctypes.c_double),
+                ("sigma", ctypes.c_double), ("scale", ctypes.c_double)]
+
+
+D415_NOISE = dict(k=3.98, theta=0.254, mu=-0.231, sigma=0.83, scale=1.0)
+
+
+def sensor_noise(clean, seed: int, frame0: int = 0, view: int = 0, out=None, stream=None, **noise):
+    """asd_sensor_noise: clean IR intensities (torch f32 CUDA, [n][H][W] or
+    [H][W], DN units) -> u8 noisy images (readings c17, c22)."""
+    import torch
+    q = dict(D415_NOISE); q.update(noise)
+    squeeze = clean.dim() == 2
+    c = clean.unsqueeze(0) if squeeze else clean
+    assert c.is_cuda and c.dtype == torch.float32 and c.is_contiguous()
+    n, H, W = c.shape
+    if out is None:
+        out = torch.empty(n, H, W, device=c.device, dtype=torch.uint8)
+    _check(load().asd_sensor_noise(ctypes.byref(asd_noise(**q)), ctypes.c_uint64(seed), n, W, H,
+                                   ctypes.c_uint32(frame0), ctypes.c_uint32(view), _ptr(c), _ptr(out),
+                                   _stream(stream)))
     return out[0] if squeeze else out
 
 

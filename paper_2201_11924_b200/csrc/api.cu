@@ -807,6 +807,27 @@ int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
     return ASD_OK;
 }
 
+int asd_sensor_noise(const asd_noise* q, uint64_t seed, int n, int width, int height,
+                     uint32_t frame0, uint32_t view, const float* clean, uint8_t* out, void* cuda_stream)
+{
+    if (!q || n < 0 || (n > 0 && (!clean || !out)) || width < 1 || height < 1 ||
+        (long long)width * height > (1ll << 26) || n > 65535) {
+        set_err(nullptr, "asd_sensor_noise: NULL argument or size out of range");
+        return ASD_E_INVALID_ARG;
+    }
+    if (!(std::isfinite(q->k) && q->k > 0.0 && std::isfinite(q->theta) && q->theta > 0.0 &&
+          std::isfinite(q->mu) && std::isfinite(q->sigma) && q->sigma >= 0.0 && std::isfinite(q->scale))) {
+        set_err(nullptr, "asd_sensor_noise: need finite k, theta > 0, sigma >= 0, mu, scale");
+        return ASD_E_INVALID_ARG;
+    }
+    if (n == 0) return ASD_OK;
+    if (launch_noise(q, seed, n, width, height, frame0, view, clean, out, (cudaStream_t)cuda_stream) != 0) {
+        set_err(nullptr, "asd_sensor_noise: %s", cudaGetErrorString(cudaGetLastError()));
+        return ASD_E_CUDA;
+    }
+    return ASD_OK;
+}
+
 int asd_register_depth(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
                        int n, const float* depth, float* out, void* cuda_stream)
 {

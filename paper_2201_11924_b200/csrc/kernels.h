@@ -25,6 +25,10 @@ bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
 int launch_register(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
                     int n, const float* depth, float* out, cudaStream_t s);
 
+// Sensor noise front end (noise.cu).
+int launch_noise(const asd_noise* q, uint64_t seed, int n, int width, int height, uint32_t frame0,
+                 uint32_t view, const float* clean, uint8_t* out, cudaStream_t s);
+
 // SGBM block cost volume CB (u16 [H][W][D] per frame), sgbm.cu.
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
                        long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s);

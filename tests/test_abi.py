@@ -102,3 +102,14 @@ def test_register_depth_validation(lib):
     Rn = (ctypes.c_float * 9)(float("nan"), 0, 0, 0, 1, 0, 0, 0, 1)
     assert reg(ctypes.byref(ir), ctypes.byref(ir), Rn, t, 0, None, None, None) == asd.ASD_E_INVALID_ARG
     assert reg(ctypes.byref(ir), ctypes.byref(ir), R, t, 0, None, None, None) == asd.ASD_OK
+
+
+def test_sensor_noise_validation(lib):
+    q = abi.asd_noise(3.98, 0.254, -0.231, 0.83, 1.0)
+    bad = abi.asd_noise(-1.0, 0.254, -0.231, 0.83, 1.0)
+    f = lib.asd_sensor_noise
+    assert f(None, 1, 1, 8, 8, 0, 0, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert f(ctypes.byref(q), 1, -1, 8, 8, 0, 0, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert f(ctypes.byref(q), 1, 1, 0, 8, 0, 0, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert f(ctypes.byref(bad), 1, 0, 8, 8, 0, 0, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert f(ctypes.byref(q), 1, 0, 8, 8, 0, 0, None, None, None) == asd.ASD_OK
