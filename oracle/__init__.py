@@ -302,3 +302,15 @@ def noise_samples(n: int, seed: int, frame: int = 0, view: int = 0, **noise):
     lib().oracle_noise_samples(ctypes.byref(OracleNoise(**q)), ctypes.c_uint64(seed), n,
                                ctypes.c_uint32(frame), ctypes.c_uint32(view), _p(g), _p(a))
     return g, a
+
+
+def rectify(Hm, img: np.ndarray) -> np.ndarray:
+    """O00 -- homography warp with bilinear sampling (reading c23).
+    Hm maps output pixel coordinates to input coordinates."""
+    img = np.ascontiguousarray(img, np.uint8)
+    Hd = np.ascontiguousarray(np.asarray(Hm, np.float64).reshape(9))
+    out = np.empty_like(img)
+    rc = lib().oracle_rectify(_p(Hd), img.shape[1], img.shape[0], _p(img), _p(out))
+    if rc != 0:
+        raise ValueError("singular homography")
+    return out

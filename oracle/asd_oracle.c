@@ -27,6 +27,7 @@
  *   O9 median      lower median of the valid k x k neighbours
  *   O8 depth       z = f*b/d
  *   O10 register   unproject, transform, reproject, z-buffer
+ *   O00 rectify    homography warp, bilinear sampling              (c23)
  *   O0 noise       I_noisy = gamma * I_clean + n, gamma ~ Gamma(k, theta),
  *                  n ~ N(mu, sigma^2), quantised to u8           (c17, c22)
  *
@@ -678,4 +679,47 @@ void oracle_noise_samples(const oracle_noise* q, uint64_t seed, int n, uint32_t 
                           double* gamma, double* add)
 {
     for (int i = 0; i < n; ++i) noise_pixel(q, seed, (uint32_t)i, frame, view, gamma + i, add + i);
+}
+
+
+/* ------------------------------------------------------------ O00 rectify
+ * Stereo rectification ("performs a stereo rectification to project the
+ * images onto a common image plane"; S:279-287 [OP] rectify: "warp by
+ * supplied 3x3 homographies with bilinear sampling"; reading c23): H maps
+ * OUTPUT pixel coordinates to INPUT coordinates (row-major, homogeneous):
+ *   w = H20 x + H21 y + H22,  u = (H00 x + H01 y + H02) / w,  v = (...) / w;
+ *   x0 = floor(u), y0 = floor(v), a = u - x0, b = v - y0;
+ *   out = (1-a)(1-b) I(x0,y0) + a(1-b) I(x0+1,y0) + (1-a) b I(x0,y0+1) + a b I(x0+1,y0+1),
+ *   I = 0 outside the image (and w <= 0 gives 0); u8 = clamp(floor(out + 0.5), 0, 255).
+ * fp64, in this order (the kernel does the same).  Returns -1 for a singular H. */
+int oracle_rectify(const double* Hm, int W, int H, const uint8_t* in, uint8_t* out)
+{
+    double det = Hm[0] * (Hm[4] * Hm[8] - Hm[5] * Hm[7]) - Hm[1] * (Hm[3] * Hm[8] - Hm[5] * Hm[6]) +
+                 Hm[2] * (Hm[3] * Hm[7] - Hm[4] * Hm[6]);
+    if (!(fabs(det) > 0.0) || isnan(det)) return -1;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            double w = Hm[6] * x + Hm[7] * y + Hm[8];
+            double val = 0.0;
+            if (w > 0.0) {
+                double u = (Hm[0] * x + Hm[1] * y + Hm[2]) / w;
+                double v = (Hm[3] * x + Hm[4] * y + Hm[5]) / w;
+                if (u > -2.0 && u < W + 1.0 && v > -2.0 && v < H + 1.0) {
+                    double fx0 = floor(u), fy0 = floor(v);
+                    int x0 = (int)fx0, y0 = (int)fy0;
+                    double a = u - fx0, b = v - fy0;
+                    double I00 = 0, I10 = 0, I01 = 0, I11 = 0;
+                    if (x0 >= 0 && x0 < W && y0 >= 0 && y0 < H) I00 = in[y0 * W + x0];
+                    if (x0 + 1 >= 0 && x0 + 1 < W && y0 >= 0 && y0 < H) I10 = in[y0 * W + x0 + 1];
+                    if (x0 >= 0 && x0 < W && y0 + 1 >= 0 && y0 + 1 < H) I01 = in[(y0 + 1) * W + x0];
+                    if (x0 + 1 >= 0 && x0 + 1 < W && y0 + 1 >= 0 && y0 + 1 < H) I11 = in[(y0 + 1) * W + x0 + 1];
+                    val = (1.0 - a) * (1.0 - b) * I00 + a * (1.0 - b) * I10 + (1.0 - a) * b * I01 + a * b * I11;
+                }
+            }
+            double r = floor(val + 0.5);
+            if (r < 0.0) r = 0.0;
+            if (r > 255.0) r = 255.0;
+            out[y * W + x] = (uint8_t)r;
+        }
+    return 0;
 }
