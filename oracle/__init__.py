@@ -43,7 +43,7 @@ class OracleParams(ctypes.Structure):
                 ("lr_max_diff", ctypes.c_float), ("subpixel", ctypes.c_int32),
                 ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
                 ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32),
-                ("median_ksize", ctypes.c_int32)]
+                ("median_ksize", ctypes.c_int32), ("lr_mode", ctypes.c_int32)]
 
 
 @dataclass
@@ -66,6 +66,7 @@ class Params:
     block_w: int = 1          # SGBM block; 1 x 1 = plain SGM
     block_h: int = 1
     median_ksize: int = 0     # 0 (off), 3, 5
+    lr_mode: int = 0          # right view: 0 = R1 (re-index, c10), 1 = R2 (own SGM, c24)
 
     @property
     def nbits(self) -> int:
@@ -76,7 +77,7 @@ class Params:
                             self.census_w, self.census_h, self.p1, self.p2, self.paths,
                             self.uniqueness, self.lr_max_diff, self.subpixel,
                             self.focal_px, self.baseline_m, self.block_w, self.block_h,
-                            self.median_ksize)
+                            self.median_ksize, self.lr_mode)
 
 
 _lib = None
@@ -110,6 +111,15 @@ def cost(p: Params, cl: np.ndarray, cr: np.ndarray) -> np.ndarray:
     cr = np.ascontiguousarray(cr, np.uint64)
     out = np.empty((p.height, p.width, p.num_disp), np.uint8)
     lib().oracle_cost(ctypes.byref(p.c()), _p(cl), _p(cr), _p(out))
+    return out
+
+
+def cost_right(p: Params, cl: np.ndarray, cr: np.ndarray) -> np.ndarray:
+    """O2 with the right view as reference (reading c24).  -> u8[H][W][D]."""
+    cl = np.ascontiguousarray(cl, np.uint64)
+    cr = np.ascontiguousarray(cr, np.uint64)
+    out = np.empty((p.height, p.width, p.num_disp), np.uint8)
+    lib().oracle_cost_right(ctypes.byref(p.c()), _p(cl), _p(cr), _p(out))
     return out
 
 

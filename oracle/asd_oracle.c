@@ -23,6 +23,8 @@
  *   O4 WTA         smallest argmin + uniqueness test
  *   O5 sub-pixel   parabola through (d*-1, d*, d*+1)
  *   O6 right view  same WTA/sub-pixel on S_R(x,d) = S(x+delta,d)  (reading c10)
+ *   O6b right view R2: SGM of the right-referenced cost
+ *                  C_R(x,y,d) = hamming(cr(x,y), cl(x+delta,y))   (reading c24)
  *   O7 LR check    |dl - dr(x - round(dl))| <= lr
  *   O9 median      lower median of the valid k x k neighbours
  *   O8 depth       z = f*b/d
@@ -57,6 +59,7 @@ typedef struct {
     float   focal_px, baseline_m;
     int32_t block_w, block_h;  /* SGBM block (odd); 1 x 1 = plain SGM */
     int32_t median_ksize;      /* 0 (off), 3 or 5 */
+    int32_t lr_mode;           /* right view: 0 = R1 re-index S (c10), 1 = R2 full right-view SGM (c24) */
 } oracle_params;
 
 /* mask bits */
@@ -115,6 +118,23 @@ void oracle_cost(const oracle_params* p, const uint64_t* cl, const uint64_t* cr,
                 int c = nb;
                 if (valid_c(p, x, y) && xr >= 0 && valid_c(p, xr, y))
                     c = popcount64(cl[y * W + x] ^ cr[y * W + xr]);
+                C[((size_t)y * W + x) * D + d] = (uint8_t)c;
+            }
+}
+
+/* O2 for the right view as reference (reading c24, "run the pipeline
+ * with roles swapped"): C_R(x,y,d) = hamming(cr(x,y), cl(x+delta,y)), nb when
+ * x + delta >= W or either census window is invalid.  Layout [H][W][D]. */
+void oracle_cost_right(const oracle_params* p, const uint64_t* cl, const uint64_t* cr, uint8_t* C)
+{
+    int W = p->width, H = p->height, D = p->num_disp, nb = nbits(p);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int d = 0; d < D; ++d) {
+                int xl = x + (p->min_disp + d);
+                int c = nb;
+                if (valid_c(p, x, y) && xl < W && valid_c(p, xl, y))
+                    c = popcount64(cr[y * W + x] ^ cl[y * W + xl]);
                 C[((size_t)y * W + x) * D + d] = (uint8_t)c;
             }
 }
@@ -419,6 +439,29 @@ void oracle_median(const oracle_params* p, const float* dl, const uint8_t* mask,
         }
 }
 
+/* O6b right view R2 (reading c24): WTA + uniqueness + sub-pixel over every d
+ * of the right-referenced aggregate S_R (as the left view); mask_r gets
+ * OM_BORDER when the right pixel's census window leaves the image. */
+void oracle_wta_right_r2(const oracle_params* p, const uint32_t* SR,
+                         int16_t* dstar_r, uint8_t* mask_r, float* dr)
+{
+    int W = p->width, H = p->height, D = p->num_disp;
+    uint8_t* defined = (uint8_t*)malloc((size_t)D);
+    for (int d = 0; d < D; ++d) defined[d] = 1;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            int uf; float disp;
+            int b = wta_subpix(p, SR + ((size_t)y * W + x) * D, defined, &uf, &disp);
+            uint8_t m = 0;
+            if (!valid_c(p, x, y)) m |= OM_BORDER;
+            if (uf) m |= OM_UNIQUE;
+            dstar_r[y * W + x] = (int16_t)b;
+            mask_r[y * W + x] = m;
+            dr[y * W + x] = disp;
+        }
+    free(defined);
+}
+
 /* O7 + O9 + O8.  LR ("left-right consistency check", readings
  * c11, c12): evaluated iff lr >= 0 and (mask & 3) == 0; xr = x - (int)floorf(dl
  * + 0.5f); invalid if xr outside [0,W), mask_r(xr) != 0 or |dl - dr(xr)| > lr.
@@ -553,7 +596,19 @@ int oracle_compute(const oracle_params* p, const uint8_t* left, const uint8_t* r
     oracle_block_cost(p, C, CB);                /* O2b (1 x 1: CB = C) */
     oracle_sgm32(p, CB, S);                     /* O3 */
     oracle_wta_left(p, S, dsl, ml, dl);         /* O4, O5 */
-    oracle_wta_right(p, S, dsr, mr, dr);        /* O6 */
+    if (p->lr_mode == 1) {                      /* O6b: R2, the right view's own SGM */
+        oracle_cost_right(p, cl, cr, C);
+        oracle_block_cost(p, C, CB);
+        oracle_sgm32(p, CB, S);
+        oracle_wta_right_r2(p, S, dsr, mr, dr);
+        if (cost || agg) {                      /* debug outputs stay the left view's */
+            oracle_cost(p, cl, cr, C);
+            oracle_block_cost(p, C, CB);
+            oracle_sgm32(p, CB, S);
+        }
+    } else {
+        oracle_wta_right(p, S, dsr, mr, dr);    /* O6 (R1) */
+    }
     oracle_lr_depth(p, dl, dr, mr, ml, disp, z);/* O7, O8 */
     if (out_disp) memcpy(out_disp, disp, sizeof(float) * npx);
     if (out_depth) memcpy(out_depth, z, sizeof(double) * npx);
