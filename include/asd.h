@@ -81,7 +81,12 @@ extern "C" {
  *   median_ksize: 0, 3 or 5 ("median filtering"; SPEC S:342-347;
  *       reading c20): after the LR check, a pixel with no BORDER/UNIQUE/LR bit
  *       takes the lower median of dl over the valid k x k neighbours (itself
- *       included); the non-positive test and the depth use that value. */
+ *       included); the non-positive test and the depth use that value.
+ *   lr_mode: right-view disparity for the LR check.  0 = R1 (reading c10,
+ *       S:389): WTA on the re-indexed left aggregate S(x + delta, d).  1 = R2
+ *       (reading c24): the right view runs its own SGM on
+ *       C_R = hamming(cr(x), cl(x + delta)) (twice the aggregation work; engine
+ *       D1). */
 /* Aggregation designs:
  *   ASD_ENGINE_D1  one warp-per-line kernel per path direction, u16 S volume
  *                  read-modify-written in HBM (any configuration above)
@@ -109,6 +114,7 @@ typedef struct asd_params {
     int32_t engine;      /* ASD_ENGINE_* (0 = auto) */
     int32_t block_w, block_h;   /* SGBM block, 1 x 1 (or 0) = SGM */
     int32_t median_ksize;       /* median filter after the LR check: 0 (off), 3, 5 */
+    int32_t lr_mode;            /* right view: 0 = R1 re-index S (default), 1 = R2 own SGM */
 } asd_params;
 
 /* Per-frame statistics; exact integers except depth_sum.
@@ -232,6 +238,19 @@ typedef struct asd_camera {
 
 int asd_register_depth(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
                        int n, const float* depth, float* out, void* cuda_stream);
+
+/* ---- stereo rectification ----
+ * PAPER.md P:289 "performs a stereo rectification to project the images onto
+ * a common image plane"; reading c23.  Warps n
+ * u8 images [n][height][width] (device) by one 3x3 homography Hm (host, 9
+ * doubles, row-major) that maps OUTPUT pixel coordinates to INPUT coordinates,
+ * bilinear sampling of the zero-padded input, round half up to u8; call once
+ * per view with that view's homography.  in and out must not overlap.  A
+ * born-rectified rig needs no call (identity).  Returns ASD_OK,
+ * ASD_E_INVALID_ARG (NULL pointer, n < 0, sizes, non-finite or singular Hm)
+ * or ASD_E_CUDA. */
+int asd_rectify(const double* Hm, int n, int width, int height, const uint8_t* in, uint8_t* out,
+                void* cuda_stream);
 
 /* ---- sensor noise front end ----
  * I_noisy = gamma * I_clean + n with gamma ~ Gamma(k, theta)

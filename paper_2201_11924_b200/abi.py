@@ -37,7 +37,7 @@ class asd_params(ctypes.Structure):
                 ("focal_px", ctypes.c_float), ("baseline_m", ctypes.c_float),
                 ("engine", ctypes.c_int32),
                 ("block_w", ctypes.c_int32), ("block_h", ctypes.c_int32),
-                ("median_ksize", ctypes.c_int32)]
+                ("median_ksize", ctypes.c_int32), ("lr_mode", ctypes.c_int32)]
 
 
 class asd_frame_stats(ctypes.Structure):
@@ -86,6 +86,7 @@ SYMBOLS = [
                                 _I, _VP, _VP, _VP]),
     ("asd_sensor_noise", _I, [ctypes.c_void_p, ctypes.c_uint64, _I, _I, _I, ctypes.c_uint32,
                               ctypes.c_uint32, _VP, _VP, _VP]),
+    ("asd_rectify", _I, [ctypes.c_void_p, _I, _I, _I, _VP, _VP, _VP]),
     ("asd_strerror", ctypes.c_char_p, [_I]),
     ("asd_last_error", ctypes.c_char_p, [_VP]),
 ]
@@ -130,12 +131,13 @@ class Params:
     block_w: int = 1           # SGBM block (reading c19); 1 x 1 = SGM
     block_h: int = 1
     median_ksize: int = 0      # 0 / 3 / 5 (reading c20)
+    lr_mode: int = 0           # right view: 0 = R1 re-index (c10), 1 = R2 own SGM (c24)
 
     def c(self) -> asd_params:
         return asd_params(self.width, self.height, self.min_disp, self.num_disp, self.census_w,
                           self.census_h, self.p1, self.p2, self.paths, self.uniqueness,
                           self.lr_max_diff, self.subpixel, self.focal_px, self.baseline_m,
-                          self.engine, self.block_w, self.block_h, self.median_ksize)
+                          self.engine, self.block_w, self.block_h, self.median_ksize, self.lr_mode)
 
     @property
     def nbits(self) -> int:
@@ -207,6 +209,21 @@ def sensor_noise(clean, seed: int, frame0: int = 0, view: int = 0, out=None, str
     _check(load().asd_sensor_noise(ctypes.byref(asd_noise(**q)), ctypes.c_uint64(seed), n, W, H,
                                    ctypes.c_uint32(frame0), ctypes.c_uint32(view), _ptr(c), _ptr(out),
                                    _stream(stream)))
+    return out[0] if squeeze else out
+
+
+def rectify(Hm, images, out=None, stream=None):
+    """asd_rectify: warp u8 images (torch CUDA, [n][H][W] or [H][W]) by the
+    homography Hm (output -> input pixel coordinates; reading c23)."""
+    import torch
+    squeeze = images.dim() == 2
+    im = images.unsqueeze(0) if squeeze else images
+    assert im.is_cuda and im.dtype == torch.uint8 and im.is_contiguous()
+    n, H, W = im.shape
+    if out is None:
+        out = torch.empty_like(im)
+    Hd = (ctypes.c_double * 9)(*[float(v) for v in __import__("numpy").asarray(Hm, "float64").reshape(9)])
+    _check(load().asd_rectify(Hd, n, W, H, _ptr(im), _ptr(out), _stream(stream)))
     return out[0] if squeeze else out
 
 

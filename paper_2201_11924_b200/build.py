@@ -23,7 +23,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "lib", "libasd.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NO_FMA = {"post.cu", "sgm_v2.cu", "register.cu", "noise.cu"}
+NO_FMA = {"post.cu", "sgm_v2.cu", "register.cu", "noise.cu", "rectify.cu"}
 
 
 def nvcc() -> str:

@@ -34,6 +34,7 @@ struct asd_ctx {
     void* census_r = nullptr;
     uint16_t* S = nullptr;
     uint16_t* cb = nullptr;       // SGBM block cost volume [B][H][W][D] u16 (D1, block > 1)
+    uint16_t* SR = nullptr;       // right view's own aggregate [B][H][W][D] u16 (D1, lr_mode R2)
     float* dl = nullptr;
     float* dr = nullptr;
     int16_t* dstar_l = nullptr;
@@ -136,6 +137,10 @@ int validate(const asd_params* p, char* why, size_t n)
         snprintf(why, n, "median_ksize must be 0, 3 or 5 (got %d)", p->median_ksize);
         return ASD_E_INVALID_ARG;
     }
+    if (p->lr_mode != 0 && p->lr_mode != 1) {
+        snprintf(why, n, "lr_mode must be 0 (R1) or 1 (R2) (got %d)", p->lr_mode);
+        return ASD_E_INVALID_ARG;
+    }
     if (bw * bh == 1 && nb + p->p2 > 255) {
         snprintf(why, n, "nb + p2 = %d > 255 (per-path cost must fit 8 bits)", nb + p->p2);
         return ASD_E_UNSUPPORTED;
@@ -182,11 +187,12 @@ DevParams make_dev(const asd_params* p)
     d.bw = p->block_w == 0 ? 1 : p->block_w;
     d.bh = p->block_h == 0 ? 1 : p->block_h;
     d.median = p->median_ksize;
+    d.lr_mode = p->lr_mode;
     return d;
 }
 
 struct Layout {
-    size_t sig, s, cb, pa, pab, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
+    size_t sig, s, sr, cb, pa, pab, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
 };
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
@@ -199,6 +205,7 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
     L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
     L.cb = (engine == ASD_ENGINE_D1 && d.bw * d.bh > 1) ? align_up(B * d.ncell * 2) : 0;
+    L.sr = (engine == ASD_ENGINE_D1 && d.lr_mode == 1) ? align_up(B * d.ncell * 2) : 0;
     L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.H * pa_cols * d.D * 2) : 0;   // P_A | C << 8, u16
     L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
     L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
@@ -208,7 +215,7 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     L.stage_in = align_up(B * d.npx * 2);
     L.stage_out = align_up(B * d.npx * 2 * 4);
     L.stats = align_up(B * sizeof(asd_frame_stats));
-    L.total = 2 * L.sig + L.s + L.cb + L.pa + L.pab + L.stash + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
+    L.total = 2 * L.sig + L.s + L.sr + L.cb + L.pa + L.pab + L.stash + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
               2 * (L.stage_in + L.stage_out + L.stats);
     return L;
 }
@@ -469,9 +476,23 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             return ASD_E_UNSUPPORTED;
         }
     }
+    if (c->engine == ASD_ENGINE_D1 && c->SR) {      // R2: the right view's own SGM (c24)
+        if (c->cb) {
+            ProfScope ps(c, s, ASD_STAGE_BLOCK, n * alg_bytes_block(p));
+            launch_block_cost(p, n, c->census_l, c->census_r, npx, c->cb, p.ncell, s, true);
+        }
+        for (int r = 0; r < p.paths; ++r) {
+            ProfScope ps(c, s, ASD_STAGE_DIR, n * alg_bytes_dir(p, r == 0));
+            if (!launch_sgm_dir(p, n, kDirs[r][0], kDirs[r][1], r == 0, c->census_l, c->census_r, npx,
+                                c->SR, p.ncell, s, c->cb, true)) {
+                set_err(c, "no SGM kernel instance for num_disp=%d", p.D);
+                return ASD_E_UNSUPPORTED;
+            }
+        }
+    }
     if (c->engine == ASD_ENGINE_D1) {
-        ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta(p));
-        if (!launch_wta(p, n, c->S, p.ncell, fs, npx, s)) {
+        ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta(p) * (c->SR ? 1.5 : 1.0));
+        if (!launch_wta(p, n, c->S, p.ncell, fs, npx, s, c->SR)) {
             set_err(c, "no WTA kernel instance for num_disp=%d", p.D);
             return ASD_E_UNSUPPORTED;
         }
@@ -492,7 +513,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
 void free_ctx(asd_ctx* c)
 {
     if (!c) return;
-    void* ptrs[] = {c->census_l, c->census_r, c->S, c->cb, c->dl, c->dr, c->dstar_l, c->dstar_r,
+    void* ptrs[] = {c->census_l, c->census_r, c->S, c->SR, c->cb, c->dl, c->dr, c->dstar_l, c->dstar_r,
                     c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
@@ -586,6 +607,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     alloc(&c->census_l, L.sig); alloc(&c->census_r, L.sig);
     if (L.s) alloc((void**)&c->S, L.s);
     if (L.cb) alloc((void**)&c->cb, L.cb);
+    if (L.sr) alloc((void**)&c->SR, L.sr);
     if (L.pa) alloc((void**)&c->pa, L.pa);
     if (L.pab) alloc((void**)&c->pab, L.pab);
     if (L.stash) alloc((void**)&c->stash, L.stash);
@@ -642,7 +664,8 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
 {
     if (!ctx || n <= 0) return 0;
     const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
-    if (ctx->engine != ASD_ENGINE_D3) return chunks * (3 + ctx->dp.paths + (ctx->cb ? 1 : 0));
+    if (ctx->engine != ASD_ENGINE_D3)
+        return chunks * (3 + (ctx->dp.paths + (ctx->cb ? 1 : 0)) * (ctx->SR ? 2 : 1));
     return 6 * ((n + ctx->group - 1) / ctx->group);   // per group: census, down, up, row, WTA, LR
 }
 
@@ -804,6 +827,27 @@ int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
     if (o.mask_r) cudaMemcpyAsync(o.mask_r, ctx->mask_r, npx, cudaMemcpyDeviceToDevice, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_err(ctx, "debug extraction failed: %s", cudaGetErrorString(e)); return ASD_E_CUDA; }
+    return ASD_OK;
+}
+
+int asd_rectify(const double* Hm, int n, int width, int height, const uint8_t* in, uint8_t* out,
+                void* cuda_stream)
+{
+    if (!Hm || n < 0 || n > 65535 || (n > 0 && (!in || !out)) || width < 1 || height < 1 ||
+        (long long)width * height > (1ll << 26)) {
+        set_err(nullptr, "asd_rectify: NULL argument or size out of range");
+        return ASD_E_INVALID_ARG;
+    }
+    for (int i = 0; i < 9; ++i)
+        if (!std::isfinite(Hm[i])) { set_err(nullptr, "asd_rectify: non-finite homography"); return ASD_E_INVALID_ARG; }
+    const double det = Hm[0] * (Hm[4] * Hm[8] - Hm[5] * Hm[7]) - Hm[1] * (Hm[3] * Hm[8] - Hm[5] * Hm[6]) +
+                       Hm[2] * (Hm[3] * Hm[7] - Hm[4] * Hm[6]);
+    if (!(std::fabs(det) > 0.0)) { set_err(nullptr, "asd_rectify: singular homography"); return ASD_E_INVALID_ARG; }
+    if (n == 0) return ASD_OK;
+    if (launch_rectify(Hm, n, width, height, in, out, (cudaStream_t)cuda_stream) != 0) {
+        set_err(nullptr, "asd_rectify: %s", cudaGetErrorString(cudaGetLastError()));
+        return ASD_E_CUDA;
+    }
     return ASD_OK;
 }
 

@@ -23,6 +23,7 @@ struct DevParams {
     long long ncell;   // W*H*D
     int bw, bh;        // SGBM block (1 x 1 = SGM)
     int median;        // median ksize: 0 (off), 3, 5
+    int lr_mode;       // right view: 0 = R1 re-index (c10), 1 = R2 own SGM (c24)
 };
 
 constexpr uint8_t MASK_BORDER = 1, MASK_UNIQUE = 2, MASK_LR = 4, MASK_NONPOS = 8;

@@ -16,14 +16,18 @@ void launch_census(const DevParams& p, int nframes, const uint8_t* left, const u
 int num_chains(const DevParams& p, int rx, int ry);
 // cv != nullptr: read the matching cost from that u16 [H][W][D] volume (SGBM)
 // instead of recomputing it from the census images.
+// right_ref: the right view is the reference (R2, reading c24).
 bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
                     const void* cl, const void* cr, long long sig_stride,
                     uint16_t* S, long long s_stride, cudaStream_t s,
-                    const uint16_t* cv = nullptr);
+                    const uint16_t* cv = nullptr, bool right_ref = false);
 
 // Depth registration (register.cu): fill, scatter with an atomicMin z-buffer, finish.
 int launch_register(const asd_camera* ir, const asd_camera* rgb, const float* R, const float* t,
                     int n, const float* depth, float* out, cudaStream_t s);
+
+// Homography rectification (rectify.cu).
+int launch_rectify(const double* Hm, int n, int W, int H, const uint8_t* in, uint8_t* out, cudaStream_t s);
 
 // Sensor noise front end (noise.cu).
 int launch_noise(const asd_noise* q, uint64_t seed, int n, int width, int height, uint32_t frame0,
@@ -31,11 +35,13 @@ int launch_noise(const asd_noise* q, uint64_t seed, int n, int width, int height
 
 // SGBM block cost volume CB (u16 [H][W][D] per frame), sgbm.cu.
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
-                       long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s);
+                       long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s,
+                       bool right_ref = false);
 
 // K4 WTA/uniqueness/sub-pixel, left + right view.
+// SR != nullptr: the right view is the WTA of its own aggregate SR (R2, c24).
 bool launch_wta(const DevParams& p, int nframes, const uint16_t* S, long long s_stride,
-                const FrameScratch& fs, long long px_stride, cudaStream_t s);
+                const FrameScratch& fs, long long px_stride, cudaStream_t s, const uint16_t* SR = nullptr);
 
 // K5 LR check + depth + per-frame stats.
 void launch_lr_depth(const DevParams& p, int nframes, const FrameScratch& fs, long long px_stride,

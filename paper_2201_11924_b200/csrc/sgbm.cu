@@ -25,7 +25,9 @@ namespace asd {
 constexpr int SB_TX = 32;            // pixels per CTA
 constexpr int SB_MAXB = 15;          // block dims bound (asd_create validates)
 
-template <typename SigT>
+// RR: the right view is the reference (R2, reading c24): cl_base / cr_base are
+// then the reference and matched census and the matched column is x' + delta.
+template <typename SigT, bool RR>
 __global__ void __launch_bounds__(256)
 block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base,
                   long long sig_stride, uint16_t* __restrict__ cb_base, long long cell_stride)
@@ -35,8 +37,9 @@ block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __r
     const int bu = p.bw / 2, bv = p.bh / 2;
     const int frame = blockIdx.z, y = blockIdx.y, x0 = blockIdx.x * SB_TX;
     const int NC = SB_TX + p.bw - 1;                 // block columns x0-bu .. x0+TX-1+bu
-    const int NRW = NC + D - 1;                      // right span: xr = x' - min - d
-    const int xr0 = x0 - bu - p.min_disp - (D - 1);  // first right column
+    const int NRW = NC + D - 1;                      // matched span: x' -/+ (min + d)
+    const int xr0 = RR ? x0 - bu + p.min_disp                 // first matched column
+                       : x0 - bu - p.min_disp - (D - 1);
     const SigT* cl = cl_base + frame * sig_stride;
     const SigT* cr = cr_base + frame * sig_stride;
 
@@ -68,8 +71,8 @@ block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __r
         uint32_t run = 0;
         Pfx[d] = 0;
         for (int c = 0; c < NC; ++c) {
-            // right column of block column c at disparity d: x' - min - d
-            const int rc = c + (D - 1) - d;
+            // matched column of block column c at disparity d: x' - min - d (x' + min + d for RR)
+            const int rc = RR ? c + d : c + (D - 1) - d;
             uint32_t vs = 0;
             for (int v = 0; v < p.bh; ++v) {
                 const int li = v * NC + c, ri = v * NRW + rc;
@@ -90,23 +93,30 @@ static size_t block_cost_smem(const DevParams& p, size_t sig)
     return (b + 15) & ~size_t(15);
 }
 
+template <typename SigT, bool RR>
+static void launch_bc(const DevParams& p, dim3 grid, int threads, const void* ref, const void* mat,
+                      long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s)
+{
+    const size_t sm = block_cost_smem(p, sizeof(SigT));
+    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    block_cost_kernel<SigT, RR><<<grid, threads, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat, sig_stride, cb,
+                                                         cell_stride);
+}
+
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
-                       long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s)
+                       long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s,
+                       bool right_ref)
 {
     dim3 grid((p.W + SB_TX - 1) / SB_TX, p.H, nframes);
     const int threads = p.D < 256 ? p.D : 256;
+    const void* ref = right_ref ? cr : cl;
+    const void* mat = right_ref ? cl : cr;
     if (p.nb <= 32) {
-        const size_t sm = block_cost_smem(p, 4);
-        cudaFuncSetAttribute((const void*)block_cost_kernel<uint32_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        block_cost_kernel<uint32_t><<<grid, threads, sm, s>>>(p, (const uint32_t*)cl, (const uint32_t*)cr,
-                                                              sig_stride, cb, cell_stride);
+        if (right_ref) launch_bc<uint32_t, true>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
+        else launch_bc<uint32_t, false>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
     } else {
-        const size_t sm = block_cost_smem(p, 8);
-        cudaFuncSetAttribute((const void*)block_cost_kernel<unsigned long long>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        block_cost_kernel<unsigned long long><<<grid, threads, sm, s>>>(
-            p, (const unsigned long long*)cl, (const unsigned long long*)cr, sig_stride, cb, cell_stride);
+        if (right_ref) launch_bc<unsigned long long, true>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
+        else launch_bc<unsigned long long, false>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
     }
 }
 

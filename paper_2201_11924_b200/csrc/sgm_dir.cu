@@ -74,7 +74,10 @@ template <> __device__ __forceinline__ void store_s<8>(uint16_t* dst, const int 
                                                 v[4] | (v[5] << 16), v[6] | (v[7] << 16));
 }
 
-template <int DPL, typename SigT, bool FIRST, bool CV>
+// MODE 0: cost from census, left view as reference (C = popc(cl(x) ^ cr(x - delta)));
+// MODE 1: right view as reference (R2, reading c24: popc(cr(x) ^ cl(x + delta)));
+// MODE 2: cost read from a u16 volume (SGBM block cost, either reference).
+template <int DPL, typename SigT, bool FIRST, int MODE>
 __global__ void __launch_bounds__(128)
 sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
                const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base, long long sig_stride,
@@ -84,8 +87,10 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
     const int lane = threadIdx.x & 31;
     if (chain >= nchains) return;
     const int frame = blockIdx.y;
-    const SigT* cl = cl_base + frame * sig_stride;
-    const SigT* cr = cr_base + frame * sig_stride;
+    constexpr bool CV = MODE == 2, RR = MODE == 1;
+    // reference / matched census (swapped for the right-view reference)
+    const SigT* cl = (RR ? cr_base : cl_base) + frame * sig_stride;
+    const SigT* cr = (RR ? cl_base : cr_base) + frame * sig_stride;
     uint16_t* S = S_base + frame * s_stride;
     const uint16_t* CVf = CV ? cv_base + frame * s_stride : nullptr;
     const bool active = lane < act;
@@ -103,8 +108,8 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
     int ns[DPL], nc[DPL];
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
-        const int xr = x - p.min_disp - d0 - j;
-        nr[j] = (!CV && active && xr >= 0) ? cr[(long long)y * p.W + xr] : (SigT)0;
+        const int xr = RR ? x + p.min_disp + d0 + j : x - p.min_disp - d0 - j;
+        nr[j] = (!CV && active && xr >= 0 && xr < p.W) ? cr[(long long)y * p.W + xr] : (SigT)0;
         ns[j] = 0;
         nc[j] = 0;
     }
@@ -126,8 +131,8 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
                 nl = cl[(long long)y * p.W + x];
 #pragma unroll
                 for (int j = 0; j < DPL; ++j) {
-                    const int xr = x - p.min_disp - d0 - j;
-                    nr[j] = (active && xr >= 0) ? cr[(long long)y * p.W + xr] : (SigT)0;
+                    const int xr = RR ? x + p.min_disp + d0 + j : x - p.min_disp - d0 - j;
+                    nr[j] = (active && xr >= 0 && xr < p.W) ? cr[(long long)y * p.W + xr] : (SigT)0;
                 }
             }
             if (!FIRST && active) load_s<DPL>(S + ((long long)y * p.W + x) * p.D + d0, ns);
@@ -137,8 +142,9 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
         int c[DPL];
 #pragma unroll
         for (int j = 0; j < DPL; ++j) {
-            const int xr = cx - p.min_disp - d0 - j;
-            c[j] = CV ? sc[j] : ((vl && xr >= p.R) ? popc_sig(sl ^ sr[j]) : p.nb);
+            const int xr = RR ? cx + p.min_disp + d0 + j : cx - p.min_disp - d0 - j;
+            const bool vm = RR ? xr < p.W - p.R : xr >= p.R;    // matched census window valid
+            c[j] = CV ? sc[j] : ((vl && vm) ? popc_sig(sl ^ sr[j]) : p.nb);
         }
         int Ln[DPL];
         if (first) {
@@ -181,30 +187,30 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
 template <int DPL, typename SigT>
 static void launch_dir_t(const DevParams& p, int nframes, int rx, int ry, bool first, int act,
                          const void* cl, const void* cr, long long sig_stride,
-                         uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv)
+                         uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv, bool right_ref)
 {
     const int n = num_chains(p, rx, ry);
     dim3 grid((n + 3) / 4, nframes), block(128);
     const SigT* l = (const SigT*)cl;
     const SigT* r = (const SigT*)cr;
-    if (cv) {
-        if (first) sgm_dir_kernel<DPL, SigT, true, true><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
-        else sgm_dir_kernel<DPL, SigT, false, true><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
-    } else {
-        if (first) sgm_dir_kernel<DPL, SigT, true, false><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
-        else sgm_dir_kernel<DPL, SigT, false, false><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
-    }
+#define ASD_DIR_LAUNCH(M) \
+    if (first) sgm_dir_kernel<DPL, SigT, true, M><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv); \
+    else sgm_dir_kernel<DPL, SigT, false, M><<<grid, block, 0, s>>>(p, rx, ry, n, act, l, r, sig_stride, S, s_stride, cv);
+    if (cv) { ASD_DIR_LAUNCH(2) }
+    else if (right_ref) { ASD_DIR_LAUNCH(1) }
+    else { ASD_DIR_LAUNCH(0) }
+#undef ASD_DIR_LAUNCH
 }
 
 template <typename SigT>
 static bool launch_dir_sig(const DevParams& p, int nframes, int rx, int ry, bool first,
                            const void* cl, const void* cr, long long sig_stride,
-                           uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv)
+                           uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv, bool right_ref)
 {
     // D = DPL * act with act = 32 (D % 32 == 0) or 16 (D % 32 == 16)
     const int act = (p.D % 32 == 0) ? 32 : 16;
     const int dpl = p.D / act;
-#define ASD_DIR_CASE(K) case K: launch_dir_t<K, SigT>(p, nframes, rx, ry, first, act, cl, cr, sig_stride, S, s_stride, s, cv); return true;
+#define ASD_DIR_CASE(K) case K: launch_dir_t<K, SigT>(p, nframes, rx, ry, first, act, cl, cr, sig_stride, S, s_stride, s, cv, right_ref); return true;
     switch (dpl) {
         ASD_DIR_CASE(1) ASD_DIR_CASE(2) ASD_DIR_CASE(3) ASD_DIR_CASE(4) ASD_DIR_CASE(5)
         ASD_DIR_CASE(6) ASD_DIR_CASE(7) ASD_DIR_CASE(8) ASD_DIR_CASE(9) ASD_DIR_CASE(11)
@@ -216,11 +222,11 @@ static bool launch_dir_sig(const DevParams& p, int nframes, int rx, int ry, bool
 
 bool launch_sgm_dir(const DevParams& p, int nframes, int rx, int ry, bool first,
                     const void* cl, const void* cr, long long sig_stride,
-                    uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv)
+                    uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv, bool right_ref)
 {
     if (p.nb <= 32)
-        return launch_dir_sig<uint32_t>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s, cv);
-    return launch_dir_sig<unsigned long long>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s, cv);
+        return launch_dir_sig<uint32_t>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s, cv, right_ref);
+    return launch_dir_sig<unsigned long long>(p, nframes, rx, ry, first, cl, cr, sig_stride, S, s_stride, s, cv, right_ref);
 }
 
 }  // namespace asd

@@ -1114,6 +1114,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     auto no = [&](const char* why) { snprintf(pl.why, sizeof pl.why, "%s", why); pl.ok = false; return false; };
     if (p.nb > 32) return no("nb > 32 (u64 census)");
     if (p.bw * p.bh > 1) return no("SGBM block cost (> 8 bits per path) runs on engine D1");
+    if (p.lr_mode != 0) return no("the R2 right view (its own SGM) runs on engine D1");
     if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 128) return no("num_disp not in {16,32,64,128}");
     const int np = p.paths == 8 ? 3 : 1;
     if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");

@@ -113,3 +113,12 @@ def test_sensor_noise_validation(lib):
     assert f(ctypes.byref(q), 1, 1, 0, 8, 0, 0, None, None, None) == asd.ASD_E_INVALID_ARG
     assert f(ctypes.byref(bad), 1, 0, 8, 8, 0, 0, None, None, None) == asd.ASD_E_INVALID_ARG
     assert f(ctypes.byref(q), 1, 0, 8, 8, 0, 0, None, None, None) == asd.ASD_OK
+
+
+def test_rectify_validation(lib):
+    eye = (ctypes.c_double * 9)(1, 0, 0, 0, 1, 0, 0, 0, 1)
+    sing = (ctypes.c_double * 9)(1, 2, 0, 2, 4, 0, 0, 0, 1)
+    assert lib.asd_rectify(None, 0, 8, 8, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert lib.asd_rectify(sing, 0, 8, 8, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert lib.asd_rectify(eye, -1, 8, 8, None, None, None) == asd.ASD_E_INVALID_ARG
+    assert lib.asd_rectify(eye, 0, 8, 8, None, None, None) == asd.ASD_OK
