@@ -530,7 +530,8 @@ struct RArgs {
     FrameScratch fs;          // WTA outputs for K5
     long long px_stride;
     int nbuf;                 // rows of the WTA kernel's S window
-    int bstride;              // u16 per window row (D + 4)
+    int bstride;              // u16 per window row (D + 2)
+    uint32_t p1x2, p2x2;      // P1, P2 in both u16 halves
 };
 
 constexpr uint32_t NONE16 = 0xFFFFu;
@@ -756,19 +757,22 @@ __device__ __forceinline__ void row_cost(const DevParams& p, int lane, uint32_t 
 }
 
 // row_rec: L_r(x) from the predecessor state Lp (zero at the line start) and
-// its min M (0 at the start); returns the new min.
+// its min M packed in both halves (M | M << 16; 0 at the start); returns the
+// new packed min.  The warp reduction runs on the (min, min) word of each
+// lane: the u32 minimum over lanes of (m << 16 | m) is the packed minimum, so
+// no unpack/repack is needed, and P1 / P2 come packed from the kernel
+// arguments (constant-bank operands).
 template <int D>
-__device__ __forceinline__ uint32_t row_rec(const DevParams& p, int lane, const uint32_t (&C)[RowGeom<D>::NRR],
-                                            const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t M,
+__device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int lane,
+                                            const uint32_t (&C)[RowGeom<D>::NRR],
+                                            const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t Mpk,
                                             uint32_t (&Ln)[RowGeom<D>::NRR])
 {
     constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
-    const uint32_t P1P1 = (uint32_t)p.p1 * 0x10001u;
-    const uint32_t MP2 = (M + (uint32_t)p.p2) * 0x10001u;
-    const uint32_t negMM = 0u - M * 0x10001u;
-    uint32_t lmin;
+    const uint32_t MP2 = Mpk + p2x2;
+    uint32_t mm;
     if constexpr (DPL == 4) {
-        const uint32_t QA = Lp[0] + P1P1, QB = Lp[NRR - 1] + P1P1;
+        const uint32_t QA = Lp[0] + p1x2, QB = Lp[NRR - 1] + p1x2;
         uint32_t prevB = __shfl_up_sync(FULL, QB, 1);
         uint32_t nextA = __shfl_down_sync(FULL, QA, 1);
         if (lane == 0) prevB = INF2;
@@ -779,12 +783,11 @@ __device__ __forceinline__ uint32_t row_rec(const DevParams& p, int lane, const 
         uint32_t tB = vmin2(vmin2(QA, dp1B), Lp[NRR - 1]);
         tA = vmin2(tA, MP2);
         tB = vmin2(tB, MP2);
-        Ln[0] = tA + C[0] + negMM;
-        Ln[NRR - 1] = tB + C[NRR - 1] + negMM;
-        const uint32_t mm = vmin2(Ln[0], Ln[NRR - 1]);
-        lmin = min(mm & 0xFFFFu, mm >> 16);
+        Ln[0] = tA + C[0] - Mpk;
+        Ln[NRR - 1] = tB + C[NRR - 1] - Mpk;
+        mm = vmin2(Ln[0], Ln[NRR - 1]);
     } else {
-        const uint32_t Q = Lp[0] + P1P1;
+        const uint32_t Q = Lp[0] + p1x2;
         uint32_t prev = __shfl_up_sync(FULL, Q, 1);
         uint32_t next = __shfl_down_sync(FULL, Q, 1);
         if (lane == 0) prev = INF2;
@@ -793,11 +796,12 @@ __device__ __forceinline__ uint32_t row_rec(const DevParams& p, int lane, const 
         const uint32_t dp1 = __byte_perm(Q, next, 0x5432);
         uint32_t t = vmin2(vmin2(dm1, dp1), Lp[0]);
         t = vmin2(t, MP2);
-        Ln[0] = t + C[0] + negMM;
-        lmin = min(Ln[0] & 0xFFFFu, Ln[0] >> 16);
+        Ln[0] = t + C[0] - Mpk;
+        mm = Ln[0];
     }
-    if (ACT < 32 && lane >= ACT) lmin = 0xFFFFFFFFu;
-    return __reduce_min_sync(FULL, lmin);
+    uint32_t m2 = vmin2(mm, __byte_perm(mm, mm, 0x1032));          // (min, min)
+    if (ACT < 32 && lane >= ACT) m2 = 0xFFFFFFFFu;
+    return __reduce_min_sync(FULL, m2);
 }
 
 // ---------------------------------------------------------------- K_row
@@ -864,7 +868,7 @@ hrow_kernel(RArgs a)
                             const bool vx = F || (vrow && x >= p.R && x < W - p.R);
                             uint32_t Cc[NRR], Ln[NRR];
                             row_cost<D, F>(p, lane, clv, vx, x + lim0, wnd, Cc);
-                            M = row_rec<D>(p, lane, Cc, L, M, Ln);
+                            M = row_rec<D>(a.p1x2, a.p2x2, lane, Cc, L, M, Ln);
 #pragma unroll
                             for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                             if (active) {
@@ -916,41 +920,44 @@ hrow_kernel(RArgs a)
             }
         };
         const int xtop = ((W - 1) / SG) * SG;              // sub-groups aligned to SG
-        load_sg(xtop, P, Sx);
-        for (int xs = xtop; xs >= 0; xs -= SG) {
-            load_sg(xs - SG, Pn, Sn);
+        // one sub-group of SG pixels from the buffers PP / SS (x = xs + SG-1 .. xs)
+        auto group = [&](int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG]) {
+            const bool whole = xs + SG <= W;
 #pragma unroll
             for (int k = SG - 1; k >= 0; --k) {
                 const int x = xs + k;
-                if (x < W) {
+                if (whole || x < W) {
                     uint32_t Cc[NRR], Pv[NRR], Ln[NRR];
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) {
-                        Pv[r] = P[k][r] & 0x01FF01FFu;
-                        Cc[r] = (P[k][r] >> 9) & 0x003F003Fu;
+                        Pv[r] = PP[k][r] & 0x01FF01FFu;
+                        Cc[r] = (PP[k][r] >> 9) & 0x003F003Fu;
                     }
-                    M = row_rec<D>(p, lane, Cc, L, M, Ln);
+                    M = row_rec<D>(a.p1x2, a.p2x2, lane, Cc, L, M, Ln);
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                     if (active) {
                         if constexpr (DPL == 4) {
-                            const uint32_t s0 = Pv[0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
-                            const uint32_t s1 = Pv[NRR - 1] + __byte_perm(Sx[k], 0u, 0x4342) + Ln[NRR - 1];
+                            const uint32_t s0 = Pv[0] + __byte_perm(SS[k], 0u, 0x4140) + Ln[0];
+                            const uint32_t s1 = Pv[NRR - 1] + __byte_perm(SS[k], 0u, 0x4342) + Ln[NRR - 1];
                             *reinterpret_cast<uint2*>(pab + (long long)x * D) =
                                 make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
                         } else {
                             *reinterpret_cast<uint32_t*>(pab + (long long)x * D) =
-                                Pv[0] + __byte_perm(Sx[k], 0u, 0x4140) + Ln[0];
+                                Pv[0] + __byte_perm(SS[k], 0u, 0x4140) + Ln[0];
                         }
                     }
                 }
             }
-#pragma unroll
-            for (int k = 0; k < SG; ++k) {
-#pragma unroll
-                for (int r = 0; r < NRR; ++r) P[k][r] = Pn[k][r];
-                Sx[k] = Sn[k];
-            }
+        };
+        // ping-pong between the two buffer sets (no register copies)
+        load_sg(xtop, P, Sx);
+        for (int xs = xtop; xs >= 0; xs -= 2 * SG) {
+            load_sg(xs - SG, Pn, Sn);
+            group(xs, P, Sx);
+            if (xs - SG < 0) break;
+            load_sg(xs - 2 * SG, P, Sx);
+            group(xs - SG, Pn, Sn);
         }
     }
 }
@@ -1247,6 +1254,8 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.p = p; r.cl = (const uint32_t*)cl; r.cr = (const uint32_t*)cr; r.sig_stride = sig_stride;
     r.pab = pab; r.stash = stash; r.cell_stride = cell_stride; r.fs = fs; r.px_stride = px_stride;
     r.nbuf = pl.nbuf; r.bstride = pl.bstride;
+    r.p1x2 = (uint32_t)p.p1 * 0x10001u;
+    r.p2x2 = (uint32_t)p.p2 * 0x10001u;
     if (stage == 2) {
         RKernel k = pick_rkernel(p.D);
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
