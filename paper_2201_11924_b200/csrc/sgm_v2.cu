@@ -574,7 +574,7 @@ __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, i
     constexpr int KS = RowGeom<D>::KS;
     uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
     const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);     // rows are 4-byte aligned
-#pragma unroll 4
+#pragma unroll
     for (int q = 0; q < D; q += 4) {
         const uint32_t v0 = r32[q / 2], v1 = r32[q / 2 + 1];
         ka = vmin2(ka, v0 * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
@@ -590,7 +590,7 @@ __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, i
     r[dstar] = (uint16_t)NONE16;
     if (dstar + 1 < D) r[dstar + 1] = (uint16_t)NONE16;
     uint32_t vm = 0xFFFFFFFFu, vm2 = 0xFFFFFFFFu;
-#pragma unroll 4
+#pragma unroll
     for (int q = 0; q < D; q += 4) {
         vm = vmin2(vm, r32[q / 2]);
         vm2 = vmin2(vm2, r32[q / 2 + 1]);
@@ -722,6 +722,46 @@ __device__ __forceinline__ void wta_right_fast(const DevParams& p, uint16_t* sb,
     if (dstar >= 1) *at(dstar - 1) = (uint16_t)cm;
     *at(dstar) = (uint16_t)s0;
     if (dstar + 1 < D) *at(dstar + 1) = (uint16_t)cp;
+    finish_wta(p, dstar, s0, min(vm & 0xFFFFu, vm >> 16), cm, cp, uf, disp);
+}
+
+// Right view on the linear stage window: the lane's diagonal S(xr + delta(d), d)
+// is b0[d * (BS + 1)] for every d (no wrap), all D defined; fully unrolled
+// (immediate offsets), packed u16 keys as in the left view, second pass over
+// the same diagonal with d*-1..d*+1 poisoned and then restored.
+template <int D>
+__device__ __forceinline__ void wta_right_lin(const DevParams& p, uint16_t* b0, int& dstar, bool& uf, float& disp)
+{
+    constexpr int BS = RowGeom<D>::BS, KS = RowGeom<D>::KS, STEP = BS + 1;
+    auto pair = [&](int d) -> uint32_t {
+        return __byte_perm((uint32_t)b0[d * STEP], (uint32_t)b0[(d + 1) * STEP], 0x5410);
+    };
+    uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
+#pragma unroll
+    for (int d = 0; d < D; d += 4) {
+        k0 = vmin2(k0, pair(d) * (1u << KS) + ((uint32_t)d | ((uint32_t)(d + 1) << 16)));
+        k1 = vmin2(k1, pair(d + 2) * (1u << KS) + ((uint32_t)(d + 2) | ((uint32_t)(d + 3) << 16)));
+    }
+    const uint32_t km = vmin2(k0, k1);
+    const uint32_t kb = min(km & 0xFFFFu, km >> 16);
+    dstar = (int)(kb & ((1u << KS) - 1u));
+    const uint32_t s0 = kb >> KS;
+    uint16_t* c0 = b0 + dstar * STEP;
+    const uint32_t cm = dstar >= 1 ? c0[-STEP] : NONE16;
+    const uint32_t cp = dstar + 1 < D ? c0[STEP] : NONE16;
+    if (dstar >= 1) c0[-STEP] = (uint16_t)NONE16;
+    c0[0] = (uint16_t)NONE16;
+    if (dstar + 1 < D) c0[STEP] = (uint16_t)NONE16;
+    uint32_t v0 = 0xFFFFFFFFu, v1 = 0xFFFFFFFFu;
+#pragma unroll
+    for (int d = 0; d < D; d += 4) {
+        v0 = vmin2(v0, pair(d));
+        v1 = vmin2(v1, pair(d + 2));
+    }
+    const uint32_t vm = vmin2(v0, v1);
+    if (dstar >= 1) c0[-STEP] = (uint16_t)cm;
+    c0[0] = (uint16_t)s0;
+    if (dstar + 1 < D) c0[STEP] = (uint16_t)cp;
     finish_wta(p, dstar, s0, min(vm & 0xFFFFu, vm >> 16), cm, cp, uf, disp);
 }
 
@@ -964,11 +1004,14 @@ hrow_kernel(RArgs a)
 
 // ---------------------------------------------------------------- K_wta
 // WTA / uniqueness / sub-pixel for the left view and the re-indexed right view
-// (K4 semantics, post.cu) from S rows staged in a shared-memory ring.  One CTA
-// (8 warps, two resident per SM) per image row walks stages of 256 pixels;
-// stage t needs S rows [256t, 256t + 255 + min + D - 1], each loaded once with
-// 4-byte cp.async (ring rows are D + 2 u16: an odd word stride keeps the
-// diagonal right-view reads free of bank conflicts).
+// (K4 semantics, post.cu) from S rows staged in shared memory.  One CTA (8
+// warps, two resident per SM) per image row walks stages of 256 pixels; stage
+// t loads S rows [256t, 256t + 255 + min + D - 1] with 4-byte cp.async into a
+// linear window (row x at slot x - 256t: the rows past the stage are loaded
+// again by the next stage, from L2), so every diagonal is wrap-free and both
+// views run fully unrolled with immediate offsets.  Window rows are D + 2 u16:
+// an odd word stride keeps the diagonal right-view reads free of bank
+// conflicts.
 constexpr int WTA_WARPS = 8;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 
@@ -998,36 +1041,31 @@ wta2_kernel(RArgs a)
         a.fs.mask_r[o] = MASK_BORDER;
         a.fs.dr[o] = 0.0f;
     }
-    constexpr int CH = D * 2 / 4;                     // 4-byte words per S row (ring rows are 4-byte aligned)
-    int loaded = 0;                                   // rows [0, loaded) issued
+    constexpr int CH = D * 2 / 4;                     // 4-byte words per S row (window rows are 4-byte aligned)
     const int nstage = (W + WTA_TX - 1) / WTA_TX;
     for (int t = 0; t < nstage; ++t) {
+        // linear window of this stage: row x at slot x - x0, rows [x0, hi)
         const int x0 = t * WTA_TX;
         const int hi = min(W, x0 + WTA_TX + p.min_disp + D - 1);
-        __syncthreads();                              // previous stage done with the ring
-        {   // thread t copies word t % CH of rows loaded + t / CH, + RSTEP, ...
+        __syncthreads();                              // previous stage done with the window
+        {   // thread t copies word t % CH of rows x0 + t / CH, + RSTEP, ...
             constexpr int RSTEP = 32 * WTA_WARPS / CH;
             const int c = threadIdx.x % CH;
-            int x = loaded + threadIdx.x / CH;
-            int slot = x % NB;
-            const uint16_t* src = S + (long long)x * D + c * 2;
-            for (; x < hi; x += RSTEP, src += RSTEP * D) {
+            int slot = threadIdx.x / CH;
+            const uint16_t* src = S + (long long)(x0 + slot) * D + c * 2;
+            for (; x0 + slot < hi; slot += RSTEP, src += RSTEP * D)
                 cp_async4(reinterpret_cast<uint32_t*>(sbuf + slot * BS + c * 2),
                           reinterpret_cast<const uint32_t*>(src), true);
-                slot += RSTEP;
-                if (slot >= NB) slot -= NB;
-            }
         }
         cp_async_commit();
         cp_async_wait<0>();
-        loaded = max(loaded, hi);
         __syncthreads();
         // left view
         {
             const int xp = x0 + warp * 32 + lane;
             if (xp < W) {
                 int ds; bool uf; float disp;
-                wta_left_lane<D>(p, sbuf + (xp % NB) * BS, ds, uf, disp);
+                wta_left_lane<D>(p, sbuf + (xp - x0) * BS, ds, uf, disp);
                 const long long o = frame * a.px_stride + (long long)y * W + xp;
                 uint8_t m = 0;
                 if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
@@ -1046,8 +1084,8 @@ wta2_kernel(RArgs a)
             const bool fast = xw + 31 + p.min_disp + D - 1 < W;   // warp-uniform: all d defined
             if (xr < W && nd > 0) {
                 int ds = -1; bool uf = false; float disp = 0.0f;
-                if (fast) wta_right_fast<D>(p, sbuf, NB, (xw + p.min_disp) % NB, lane, ds, uf, disp);
-                else wta_right_lane<D>(p, sbuf, NB, (xr + p.min_disp) % NB, nd, ds, uf, disp);
+                if (fast) wta_right_lin<D>(p, sbuf + (xr + p.min_disp - x0) * BS, ds, uf, disp);
+                else wta_right_lane<D>(p, sbuf, NB, xr + p.min_disp - x0, nd, ds, uf, disp);
                 const long long o = frame * a.px_stride + (long long)y * W + xr;
                 uint8_t m = 0;
                 if (!(vrow && xr >= p.R && xr < W - p.R)) m |= MASK_BORDER;
