@@ -2,15 +2,18 @@
 // volume never materialised and the path state packed two disparities per
 // 32-bit register (u16x2, VIMNMX/VIMNMX3 on sm_100a).
 //
-//   K_down  (cluster kernel)  rows top->bottom, paths  down, down-right, down-left
-//                             -> P_A  = sum of those L_r, u8 per cell
-//   K_up    (cluster kernel)  rows bottom->top, paths  up, up-left, up-right
-//                             -> P_AB = P_A + sum, u16 per cell
+//   K_down  (cluster kernel)  rows top->bottom, paths  down, down-right, down-left;
+//                             cost C by POPC from census rows in shared memory
+//                             -> P_A | C << 8 per cell (u16, warp-private order)
+//   K_up    (cluster kernel)  rows bottom->top (TMA ring of K_down rows),
+//                             paths up, up-left, up-right
+//                             -> P_AB | C << 9 per cell (u16, natural order)
 //   K_row   (warp per row)    left->right path (L stashed as u8), then
-//                             right->left path; S = P_AB + L_lr + L_rl, and
-//                             WTA/uniqueness/sub-pixel for the left view and
-//                             the re-indexed right view from a shared-memory
-//                             window of S rows (K4 semantics, post.cu).
+//                             right->left path; S = P_AB + L_lr + L_rl
+//                             written over the partial, natural d order
+//   K_wta   (CTA per row)     WTA / uniqueness / sub-pixel for the left view
+//                             and the re-indexed right view from shared-memory
+//                             windows of S rows (K4 semantics, post.cu)
 // 4-path: K_down/K_up carry only the vertical path.
 //
 // Recursion ("four-path semi-global matching", SPEC S:309,
@@ -652,79 +655,6 @@ __device__ __forceinline__ void wta_right_lane(const DevParams& p, uint16_t* sb,
     finish_wta(p, dstar, s0, vm, cm, cp, uf, disp);
 }
 
-// Right view, fast path: all 32 lanes of the warp hold consecutive right pixels
-// (r0 = (rb + lane) mod NB) and every d in [0, D) is defined.  The lanes wrap
-// around the ring at different d, but only inside one 32-wide band [A, B);
-// below it no lane has wrapped and above it each lane's base is fixed, so the
-// loops have warp-uniform bounds and read two disparities per key.
-template <int D>
-__device__ __forceinline__ void wta_right_fast(const DevParams& p, uint16_t* sb, int NB, int rb, int lane,
-                                               int& dstar, bool& uf, float& disp)
-{
-    constexpr int BS = RowGeom<D>::BS, KS = RowGeom<D>::KS, STEP = BS + 1;
-    const int r0 = rb + lane < NB ? rb + lane : rb + lane - NB;
-    const bool may_wrap = rb + lane < NB;
-    const int dw = NB - r0;                            // first wrapped d (>= D: none)
-    uint16_t* b0 = sb + r0 * BS;
-    uint16_t* b1 = b0 - NB * BS;
-    int A = NB - rb - 31;
-    A = A < 0 ? 0 : (A > D ? D : A);
-    A &= ~1;
-    int B = NB - rb + 1;
-    B = B > D ? D : B;
-    B = (B + 1) & ~1;
-    if (B > D) B = D;
-    if (B < A) B = A;
-    const uint16_t* bw = may_wrap ? b1 : b0;
-    auto pair = [](const uint16_t* q0, const uint16_t* q1, int d) -> uint32_t {
-        return __byte_perm((uint32_t)q0[d * STEP], (uint32_t)q1[(d + 1) * STEP], 0x5410);
-    };
-    auto dd = [](int d) -> uint32_t { return (uint32_t)d | ((uint32_t)(d + 1) << 16); };
-    uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
-    int d = 0;
-#pragma unroll 4
-    for (; d < A; d += 2) {
-        const uint32_t k = pair(b0, b0, d) * (1u << KS) + dd(d);
-        if (d & 2) k1 = vmin2(k1, k); else k0 = vmin2(k0, k);
-    }
-    for (; d < B; d += 2) {
-        const uint16_t* q0 = d < dw ? b0 : b1;
-        const uint16_t* q1 = d + 1 < dw ? b0 : b1;
-        k0 = vmin2(k0, pair(q0, q1, d) * (1u << KS) + dd(d));
-    }
-#pragma unroll 4
-    for (; d < D; d += 2) {
-        const uint32_t k = pair(bw, bw, d) * (1u << KS) + dd(d);
-        if (d & 2) k1 = vmin2(k1, k); else k0 = vmin2(k0, k);
-    }
-    const uint32_t km = vmin2(k0, k1);
-    const uint32_t kb = min(km & 0xFFFFu, km >> 16);
-    dstar = (int)(kb & ((1u << KS) - 1u));
-    const uint32_t s0 = kb >> KS;
-    auto at = [&](int e) -> uint16_t* { return (e < dw ? b0 : b1) + e * STEP; };
-    const uint32_t cm = dstar >= 1 ? *at(dstar - 1) : NONE16;
-    const uint32_t cp = dstar + 1 < D ? *at(dstar + 1) : NONE16;
-    if (dstar >= 1) *at(dstar - 1) = (uint16_t)NONE16;
-    *at(dstar) = (uint16_t)NONE16;
-    if (dstar + 1 < D) *at(dstar + 1) = (uint16_t)NONE16;
-    uint32_t v0 = 0xFFFFFFFFu, v1 = 0xFFFFFFFFu;
-    d = 0;
-#pragma unroll 4
-    for (; d < A; d += 2) {
-        if (d & 2) v1 = vmin2(v1, pair(b0, b0, d)); else v0 = vmin2(v0, pair(b0, b0, d));
-    }
-    for (; d < B; d += 2) v0 = vmin2(v0, pair(d < dw ? b0 : b1, d + 1 < dw ? b0 : b1, d));
-#pragma unroll 4
-    for (; d < D; d += 2) {
-        if (d & 2) v1 = vmin2(v1, pair(bw, bw, d)); else v0 = vmin2(v0, pair(bw, bw, d));
-    }
-    const uint32_t vm = vmin2(v0, v1);
-    if (dstar >= 1) *at(dstar - 1) = (uint16_t)cm;
-    *at(dstar) = (uint16_t)s0;
-    if (dstar + 1 < D) *at(dstar + 1) = (uint16_t)cp;
-    finish_wta(p, dstar, s0, min(vm & 0xFFFFu, vm >> 16), cm, cp, uf, disp);
-}
-
 // Right view on the linear stage window: the lane's diagonal S(xr + delta(d), d)
 // is b0[d * (BS + 1)] for every d (no wrap), all D defined; fully unrolled
 // (immediate offsets), packed u16 keys as in the left view, second pass over
@@ -765,10 +695,6 @@ __device__ __forceinline__ void wta_right_lin(const DevParams& p, uint16_t* b0, 
     finish_wta(p, dstar, s0, min(vm & 0xFFFFu, vm >> 16), cm, cp, uf, disp);
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* ptr)
-{
-    asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr));
-}
 
 // Horizontal-path step for one warp (lane = DPL disparities).  Register
 // layout: DPL == 4 -> A = (d0, d0+2), B = (d0+1, d0+3); DPL == 2 -> (d0, d0+1).
@@ -1015,11 +941,6 @@ hrow_kernel(RArgs a)
 constexpr int WTA_WARPS = 8;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc)
-{
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(gsrc) : "memory");
-}
 
 template <int D>
 __global__ void __launch_bounds__(32 * WTA_WARPS)
