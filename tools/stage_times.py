@@ -16,6 +16,7 @@ ap.add_argument("--max-batch", type=int, default=0)
 ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--timeline", action="store_true", help="print the per-launch timeline")
+ap.add_argument("--group", type=int, default=0, help="D3 pipeline group (frames); 0 = default")
 args = ap.parse_args()
 cfg = synth.CONFIGS[args.config]
 d = cfg.params_dict()
@@ -32,7 +33,9 @@ if args.max_batch <= 0:
     args.max_batch = max(1, (32 // fpw) * fpw) if fpw > 0 else 32
     print("frames per wave", fpw, "max_batch", args.max_batch)
 st = asd.Stereo(asd.Params(**d, engine=args.engine), 0, args.max_batch)
-print(st.plan_info)
+if args.group > 0 and st.engine == 3:
+    st.group = args.group
+print(st.plan_info, "group", st.group)
 st.asd_depth_batch(L, R, out, out)
 torch.cuda.synchronize()
 st.profile_begin(4096)
