@@ -35,6 +35,7 @@ struct asd_ctx {
     uint16_t* S = nullptr;
     uint16_t* cb = nullptr;       // SGBM block cost volume [B][H][W][D] u16 (D1, block > 1)
     uint16_t* SR = nullptr;       // right view's own aggregate [B][H][W][D] u16 (D1, lr_mode R2)
+    bool wta2 = false;            // D1: WTA by the ring-window kernel (plan.nbuf / rsmem / wide)
     float* dl = nullptr;
     float* dr = nullptr;
     int16_t* dstar_l = nullptr;
@@ -145,8 +146,8 @@ int validate(const asd_params* p, char* why, size_t n)
         snprintf(why, n, "nb + p2 = %d > 255 (per-path cost must fit 8 bits)", nb + p->p2);
         return ASD_E_UNSUPPORTED;
     }
-    if (bw * bh > 1 && (long long)(p->paths == 8 ? 8 : 4) * ((long long)bw * bh * nb + p->p2) > 65535) {
-        snprintf(why, n, "paths * (block area * nb + p2) > 65535 (S must fit 16 bits)");
+    if (bw * bh > 1 && (long long)(p->paths == 8 ? 8 : 4) * ((long long)bw * bh * nb + p->p2) > 65534) {
+        snprintf(why, n, "paths * (block area * nb + p2) > 65534 (S must fit 16 bits, 0xFFFF is a sentinel)");
         return ASD_E_UNSUPPORTED;
     }
     if (p->paths != 4 && p->paths != 8) {
@@ -492,7 +493,8 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
     }
     if (c->engine == ASD_ENGINE_D1) {
         ProfScope ps(c, s, ASD_STAGE_WTA, n * alg_bytes_wta(p) * (c->SR ? 1.5 : 1.0));
-        if (!launch_wta(p, n, c->S, p.ncell, fs, npx, s, c->SR)) {
+        if (c->wta2) launch_wta2(p, c->plan, n, c->S, p.ncell, fs, npx, s);
+        else if (!launch_wta(p, n, c->S, p.ncell, fs, npx, s, c->SR)) {
             set_err(c, "no WTA kernel instance for num_disp=%d", p.D);
             return ASD_E_UNSUPPORTED;
         }
@@ -597,6 +599,15 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
             delete c;
             return ASD_E_UNSUPPORTED;
         }
+    }
+    // Engine D1 with D in 16..128 and the R1 right view: the ring-window WTA
+    // kernel (wta2), with u32 keys when S can reach 2^(16 - log2 D).
+    c->wta2 = false;
+    if (c->engine == ASD_ENGINE_D1 && c->dp.lr_mode == 0 &&
+        (c->dp.D == 16 || c->dp.D == 32 || c->dp.D == 64 || c->dp.D == 128)) {
+        const int ks = c->dp.D <= 16 ? 4 : c->dp.D <= 32 ? 5 : c->dp.D <= 64 ? 6 : 7;
+        const long long smax = (long long)c->dp.paths * ((long long)c->dp.bw * c->dp.bh * c->dp.nb + c->dp.p2);
+        if (wta2_plan(c->dp, smax >= (1ll << (16 - ks)), c->plan)) c->wta2 = true;
     }
     Layout L = layout(c->dp, max_batch, c->engine,
                       c->engine == ASD_ENGINE_D3 ? c->plan.cs * c->plan.w : c->dp.W);

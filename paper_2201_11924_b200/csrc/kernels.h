@@ -56,9 +56,15 @@ struct V2Plan {
     size_t vsmem, vsmem_up;
     int DPL, nbuf, bstride;
     size_t rsmem;
+    bool wide;        // WTA keys in u32 (S may exceed 2^(16 - log2 D))
     char why[128];
 };
 bool v2_plan(const DevParams& p, int device, V2Plan& pl);
+// The ring-window WTA kernel alone (also used by engine D1 when D is 16..128):
+// fills nbuf / bstride / rsmem / wide; false if the window does not fit.
+bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl);
+void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16_t* S, long long cell_stride,
+                 const FrameScratch& fs, long long px_stride, cudaStream_t s);
 int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes,
                     const void* cl, const void* cr, long long sig_stride,
                     uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,

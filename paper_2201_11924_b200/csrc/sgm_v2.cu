@@ -571,20 +571,33 @@ template <int D> struct RowGeom {
 // Left view, one pixel per lane, from its window row r[0..D) (natural order).
 // Pass 1: packed u16 keys (S << KS) | d, u16x2 min.  Pass 2: min of S with
 // d*-1..d*+1 poisoned (the row belongs to this lane alone), then restored.
-template <int D>
+// WIDE: S may exceed 2^(16 - KS) (SGBM block costs, D1 volumes): u32 keys.
+template <int D, bool WIDE>
 __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, int& dstar, bool& uf, float& disp)
 {
     constexpr int KS = RowGeom<D>::KS;
-    uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
     const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);     // rows are 4-byte aligned
+    uint32_t kb;
+    if constexpr (WIDE) {
+        uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
 #pragma unroll
-    for (int q = 0; q < D; q += 4) {
-        const uint32_t v0 = r32[q / 2], v1 = r32[q / 2 + 1];
-        ka = vmin2(ka, v0 * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
-        kb2 = vmin2(kb2, v1 * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
+        for (int q = 0; q < D; q += 2) {
+            const uint32_t v = r32[q / 2];
+            ka = min(ka, ((v & 0xFFFFu) << KS) | (uint32_t)q);
+            kb2 = min(kb2, ((v >> 16) << KS) | (uint32_t)(q + 1));
+        }
+        kb = min(ka, kb2);
+    } else {
+        uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < D; q += 4) {
+            const uint32_t v0 = r32[q / 2], v1 = r32[q / 2 + 1];
+            ka = vmin2(ka, v0 * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
+            kb2 = vmin2(kb2, v1 * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
+        }
+        const uint32_t kmin = vmin2(ka, kb2);
+        kb = min(kmin & 0xFFFFu, kmin >> 16);
     }
-    const uint32_t kmin = vmin2(ka, kb2);
-    const uint32_t kb = min(kmin & 0xFFFFu, kmin >> 16);
     dstar = (int)(kb & ((1u << KS) - 1u));
     const uint32_t s0 = kb >> KS;
     const uint32_t cm = dstar >= 1 ? r[dstar - 1] : NONE16;
@@ -659,21 +672,32 @@ __device__ __forceinline__ void wta_right_lane(const DevParams& p, uint16_t* sb,
 // is b0[d * (BS + 1)] for every d (no wrap), all D defined; fully unrolled
 // (immediate offsets), packed u16 keys as in the left view, second pass over
 // the same diagonal with d*-1..d*+1 poisoned and then restored.
-template <int D>
+template <int D, bool WIDE>
 __device__ __forceinline__ void wta_right_lin(const DevParams& p, uint16_t* b0, int& dstar, bool& uf, float& disp)
 {
     constexpr int BS = RowGeom<D>::BS, KS = RowGeom<D>::KS, STEP = BS + 1;
     auto pair = [&](int d) -> uint32_t {
         return __byte_perm((uint32_t)b0[d * STEP], (uint32_t)b0[(d + 1) * STEP], 0x5410);
     };
-    uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
+    uint32_t kb;
+    if constexpr (WIDE) {
+        uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
 #pragma unroll
-    for (int d = 0; d < D; d += 4) {
-        k0 = vmin2(k0, pair(d) * (1u << KS) + ((uint32_t)d | ((uint32_t)(d + 1) << 16)));
-        k1 = vmin2(k1, pair(d + 2) * (1u << KS) + ((uint32_t)(d + 2) | ((uint32_t)(d + 3) << 16)));
+        for (int d = 0; d < D; d += 2) {
+            k0 = min(k0, ((uint32_t)b0[d * STEP] << KS) | (uint32_t)d);
+            k1 = min(k1, ((uint32_t)b0[(d + 1) * STEP] << KS) | (uint32_t)(d + 1));
+        }
+        kb = min(k0, k1);
+    } else {
+        uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
+#pragma unroll
+        for (int d = 0; d < D; d += 4) {
+            k0 = vmin2(k0, pair(d) * (1u << KS) + ((uint32_t)d | ((uint32_t)(d + 1) << 16)));
+            k1 = vmin2(k1, pair(d + 2) * (1u << KS) + ((uint32_t)(d + 2) | ((uint32_t)(d + 3) << 16)));
+        }
+        const uint32_t km = vmin2(k0, k1);
+        kb = min(km & 0xFFFFu, km >> 16);
     }
-    const uint32_t km = vmin2(k0, k1);
-    const uint32_t kb = min(km & 0xFFFFu, km >> 16);
     dstar = (int)(kb & ((1u << KS) - 1u));
     const uint32_t s0 = kb >> KS;
     uint16_t* c0 = b0 + dstar * STEP;
@@ -942,7 +966,7 @@ constexpr int WTA_WARPS = 8;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 
 
-template <int D>
+template <int D, bool WIDE>
 __global__ void __launch_bounds__(32 * WTA_WARPS)
 wta2_kernel(RArgs a)
 {
@@ -986,7 +1010,7 @@ wta2_kernel(RArgs a)
             const int xp = x0 + warp * 32 + lane;
             if (xp < W) {
                 int ds; bool uf; float disp;
-                wta_left_lane<D>(p, sbuf + (xp - x0) * BS, ds, uf, disp);
+                wta_left_lane<D, WIDE>(p, sbuf + (xp - x0) * BS, ds, uf, disp);
                 const long long o = frame * a.px_stride + (long long)y * W + xp;
                 uint8_t m = 0;
                 if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
@@ -1005,7 +1029,7 @@ wta2_kernel(RArgs a)
             const bool fast = xw + 31 + p.min_disp + D - 1 < W;   // warp-uniform: all d defined
             if (xr < W && nd > 0) {
                 int ds = -1; bool uf = false; float disp = 0.0f;
-                if (fast) wta_right_lin<D>(p, sbuf + (xr + p.min_disp - x0) * BS, ds, uf, disp);
+                if (fast) wta_right_lin<D, WIDE>(p, sbuf + (xr + p.min_disp - x0) * BS, ds, uf, disp);
                 else wta_right_lane<D>(p, sbuf, NB, xr + p.min_disp - x0, nd, ds, uf, disp);
                 const long long o = frame * a.px_stride + (long long)y * W + xr;
                 uint8_t m = 0;
@@ -1054,12 +1078,12 @@ static RKernel pick_rkernel(int D)
     return nullptr;
 }
 
-static RKernel pick_wkernel(int D)
+static RKernel pick_wkernel(int D, bool wide = false)
 {
-    if (D == 16) return v2::wta2_kernel<16>;
-    if (D == 32) return v2::wta2_kernel<32>;
-    if (D == 64) return v2::wta2_kernel<64>;
-    if (D == 128) return v2::wta2_kernel<128>;
+    if (D == 16) return wide ? v2::wta2_kernel<16, true> : v2::wta2_kernel<16, false>;
+    if (D == 32) return wide ? v2::wta2_kernel<32, true> : v2::wta2_kernel<32, false>;
+    if (D == 64) return wide ? v2::wta2_kernel<64, true> : v2::wta2_kernel<64, false>;
+    if (D == 128) return wide ? v2::wta2_kernel<128, true> : v2::wta2_kernel<128, false>;
     return nullptr;
 }
 
@@ -1163,17 +1187,34 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     }
-    // WTA kernel ring: rows [128t, 128t + 127 + min + D - 1] of stage t must
-    // fit beside nothing else; NB > 128 + min + D - 1
+    if (!wta2_plan(p, false, pl)) return no("min_disp + num_disp too large for the WTA window");
+    pl.ok = true;
+    return true;
+}
+
+// The WTA kernel's window: rows [256t, 256t + 255 + min + D - 1] of stage t.
+bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl)
+{
+    RKernel wk = pick_wkernel(p.D, wide);
+    if (!wk) return false;
     pl.nbuf = ((v2::WTA_TX + p.min_disp + p.D + 31) / 32) * 32;
     pl.bstride = p.D + 2;               // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
-    if (pl.rsmem > 200 * 1024) return no("min_disp + num_disp too large for the WTA ring");
-    RKernel wk = pick_wkernel(p.D);
+    if (pl.rsmem > 200 * 1024) return false;
     cudaFuncSetAttribute((const void*)wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.rsmem);
     cudaGetLastError();
-    pl.ok = true;
+    pl.wide = wide;
     return true;
+}
+
+void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16_t* S, long long cell_stride,
+                 const FrameScratch& fs, long long px_stride, cudaStream_t s)
+{
+    RArgs r{};
+    r.p = p; r.pab = const_cast<uint16_t*>(S); r.cell_stride = cell_stride; r.fs = fs; r.px_stride = px_stride;
+    r.nbuf = pl.nbuf; r.bstride = pl.bstride;
+    RKernel k = pick_wkernel(p.D, pl.wide);
+    k<<<dim3(p.H, nframes), 32 * v2::WTA_WARPS, pl.rsmem, s>>>(r);
 }
 
 static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const VArgs& a, bool up, cudaStream_t s)
@@ -1219,7 +1260,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         RKernel k = pick_rkernel(p.D);
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
     } else {
-        RKernel k = pick_wkernel(p.D);
+        RKernel k = pick_wkernel(p.D, pl.wide);
         k<<<dim3(p.H, nframes), 32 * v2::WTA_WARPS, pl.rsmem, s>>>(r);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
