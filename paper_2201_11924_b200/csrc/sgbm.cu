@@ -9,25 +9,27 @@
 // The volume (u16 [H][W][D]) feeds the D1 direction kernels (sgm_dir.cu, CV
 // mode) in place of the per-pixel Hamming cost.
 //
-// One CTA = TX consecutive pixels of one row of one frame, all D disparities;
-// thread = disparity (strided when D > blockDim).  The bh census rows of the
-// left block span and of the right span they are compared with are staged in
-// shared memory with validity flags.  Per disparity the thread forms the
-// vertical block sums V(c) of the TX + bw - 1 block columns, keeps their
-// prefix sums in shared memory ([c][d], conflict-free across the warp) and
-// writes CB(x0 + i, d) = P(i + bw) - P(i): (TX + bw - 1) * bh Hamming
-// evaluations per TX outputs, not TX * bw * bh.
+// Layout: thread = disparity, CTA = a TX x SB_RY pixel tile of one frame (see
+// block_cost_kernel): each Hamming distance once per CTA, horizontal window
+// sums per row, vertical sums slid down the tile's rows.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace asd {
 
-constexpr int SB_TX = 32;            // pixels per CTA
-constexpr int SB_MAXB = 15;          // block dims bound (asd_create validates)
+constexpr int SB_RY = 16;            // rows per CTA (the block sum slides down them)
 
 // RR: the right view is the reference (R2, reading c24): cl_base / cr_base are
 // then the reference and matched census and the matched column is x' + delta.
-template <typename SigT, bool RR>
+//
+// One CTA = TX pixels x SB_RY rows of one frame, thread = disparity
+// (blockDim = D).  The block sum slides down the rows: CB(y+1) = CB(y) +
+// H(y+1+bv) - H(y-bv), where H(y') are the horizontal block sums of row y'
+// for the TX pixels.  The last bh rows of H sit in a shared-memory ring
+// ([bh][TX][D] u16, each thread touching only its own d), CB in registers;
+// each new row's census spans are staged in shared memory, so each (column,
+// row, d) Hamming distance is evaluated once per CTA instead of bh times.
+template <typename SigT, bool RR, int TX>
 __global__ void __launch_bounds__(256)
 block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base,
                   long long sig_stride, uint16_t* __restrict__ cb_base, long long cell_stride)
@@ -35,88 +37,129 @@ block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __r
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = p.W, H = p.H, D = p.D;
     const int bu = p.bw / 2, bv = p.bh / 2;
-    const int frame = blockIdx.z, y = blockIdx.y, x0 = blockIdx.x * SB_TX;
-    const int NC = SB_TX + p.bw - 1;                 // block columns x0-bu .. x0+TX-1+bu
+    const int frame = blockIdx.z, y0 = blockIdx.y * SB_RY, x0 = blockIdx.x * TX;
+    const int y1 = min(H, y0 + SB_RY);
+    const int NC = TX + p.bw - 1;                    // block columns x0-bu .. x0+TX-1+bu
     const int NRW = NC + D - 1;                      // matched span: x' -/+ (min + d)
     const int xr0 = RR ? x0 - bu + p.min_disp                 // first matched column
                        : x0 - bu - p.min_disp - (D - 1);
     const SigT* cl = cl_base + frame * sig_stride;
     const SigT* cr = cr_base + frame * sig_stride;
+    const int d = threadIdx.x;                       // blockDim.x == D
 
-    SigT* Ls = reinterpret_cast<SigT*>(sm_raw);                  // [bh][NC]
-    SigT* Rs = Ls + p.bh * NC;                                    // [bh][NRW]
-    uint32_t* Pfx = reinterpret_cast<uint32_t*>(Rs + p.bh * NRW); // [NC + 1][D]
-    unsigned char* Lv = reinterpret_cast<unsigned char*>(Pfx + (NC + 1) * D);   // [bh][NC]
-    unsigned char* Rv = Lv + p.bh * NC;                                          // [bh][NRW]
-
-    for (int i = threadIdx.x; i < p.bh * NC; i += blockDim.x) {
-        const int v = i / NC, c = i - v * NC;
-        const int xx = x0 - bu + c, yy = y - bv + v;
-        const bool in = xx >= 0 && xx < W && yy >= 0 && yy < H;
-        const bool ok = in && census_valid(p, xx, yy);
+    const int NY = (y1 - y0) + p.bh - 1;             // census rows y0 - bv .. y1 - 1 + bv
+    SigT* Ls = reinterpret_cast<SigT*>(sm_raw);                            // [NY][NC]
+    SigT* Rs = Ls + (size_t)NY * NC;                                        // [NY][NRW]
+    uint16_t* Hr = reinterpret_cast<uint16_t*>(Rs + (size_t)NY * NRW);      // [bh][TX][D]
+    uint16_t* Cc = Hr + (size_t)p.bh * TX * D;                              // [NC][D]
+    unsigned char* Lv = reinterpret_cast<unsigned char*>(Cc + (size_t)NC * D);   // [NY][NC]
+    unsigned char* Rv = Lv + (size_t)NY * NC;                                     // [NY][NRW]
+    // stage every census row the tile needs once
+    for (int i = threadIdx.x; i < NY * NC; i += blockDim.x) {
+        const int r = i / NC, c = i - r * NC;
+        const int xx = x0 - bu + c, yy = y0 - bv + r;
+        const bool ok = yy >= 0 && yy < H && xx >= 0 && xx < W && census_valid(p, xx, yy);
         Ls[i] = ok ? cl[(long long)yy * W + xx] : (SigT)0;
         Lv[i] = ok;
     }
-    for (int i = threadIdx.x; i < p.bh * NRW; i += blockDim.x) {
-        const int v = i / NRW, c = i - v * NRW;
-        const int xr = xr0 + c, yy = y - bv + v;
+    for (int i = threadIdx.x; i < NY * NRW; i += blockDim.x) {
+        const int r = i / NRW, c = i - r * NRW;
+        const int xr = xr0 + c, yy = y0 - bv + r;
         const bool ok = yy >= 0 && yy < H && xr >= 0 && xr < W && census_valid(p, xr, yy);
         Rs[i] = ok ? cr[(long long)yy * W + xr] : (SigT)0;
         Rv[i] = ok;
     }
     __syncthreads();
 
-    uint16_t* cb = cb_base + frame * cell_stride + ((long long)y * W + x0) * D;
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    // H of image row yy into ring slot `slot` (this thread's d only: no syncs)
+    auto hrow = [&](int yy, int slot) {
+        const int r = yy - (y0 - bv);
+        const SigT* L = Ls + (size_t)r * NC;
+        const SigT* R = Rs + (size_t)r * NRW;
+        const unsigned char* lv = Lv + (size_t)r * NC;
+        const unsigned char* rv = Rv + (size_t)r * NRW;
         uint32_t run = 0;
-        Pfx[d] = 0;
-        for (int c = 0; c < NC; ++c) {
-            // matched column of block column c at disparity d: x' - min - d (x' + min + d for RR)
+        for (int c = 0; c < NC; ++c) {              // window sums over bw block columns
             const int rc = RR ? c + d : c + (D - 1) - d;
-            uint32_t vs = 0;
-            for (int v = 0; v < p.bh; ++v) {
-                const int li = v * NC + c, ri = v * NRW + rc;
-                vs += (Lv[li] && Rv[ri]) ? (uint32_t)popc_sig(Ls[li] ^ Rs[ri]) : (uint32_t)p.nb;
-            }
-            run += vs;
-            Pfx[(c + 1) * D + d] = run;
+            const uint32_t cv = (lv[c] && rv[rc]) ? (uint32_t)popc_sig(L[c] ^ R[rc]) : (uint32_t)p.nb;
+            Cc[(size_t)c * D + d] = (uint16_t)cv;
+            run += cv;
+            if (c >= p.bw) run -= Cc[(size_t)(c - p.bw) * D + d];
+            if (c + 1 >= p.bw) Hr[((size_t)slot * TX + (c + 1 - p.bw)) * D + d] = (uint16_t)run;
         }
-        for (int i = 0; i < SB_TX && x0 + i < W; ++i)
-            cb[(long long)i * D + d] = (uint16_t)(Pfx[(i + p.bw) * D + d] - Pfx[i * D + d]);
+    };
+    uint32_t cb[TX];
+#pragma unroll
+    for (int i = 0; i < TX; ++i) cb[i] = 0;
+    auto add_slot = [&](int slot, bool sub) {
+#pragma unroll
+        for (int i = 0; i < TX; ++i) {
+            const uint32_t v = Hr[((size_t)slot * TX + i) * D + d];
+            cb[i] = sub ? cb[i] - v : cb[i] + v;
+        }
+    };
+    auto write_row = [&](int y) {
+        uint16_t* out = cb_base + frame * cell_stride + ((long long)y * W + x0) * D + d;
+#pragma unroll
+        for (int i = 0; i < TX; ++i)
+            if (x0 + i < W) out[(long long)i * D] = (uint16_t)cb[i];
+    };
+    for (int v = 0; v < p.bh; ++v) {                 // rows y0 - bv .. y0 + bv -> slots 0 .. bh-1
+        hrow(y0 - bv + v, v);
+        add_slot(v, false);
+    }
+    write_row(y0);
+    for (int y = y0 + 1; y < y1; ++y) {
+        const int slot = (y - 1 - y0) % p.bh;        // holds row y - 1 - bv, leaving the window
+        add_slot(slot, true);
+        hrow(y + bv, slot);
+        add_slot(slot, false);
+        write_row(y);
     }
 }
 
+template <int TX>
 static size_t block_cost_smem(const DevParams& p, size_t sig)
 {
-    const size_t NC = SB_TX + p.bw - 1, NRW = NC + p.D - 1;
-    size_t b = (size_t)p.bh * (NC + NRW) * sig + (NC + 1) * p.D * 4 + (size_t)p.bh * (NC + NRW);
+    const size_t NC = TX + p.bw - 1, NRW = NC + p.D - 1, NY = SB_RY + p.bh - 1;
+    size_t b = NY * (NC + NRW) * (sig + 1) + (size_t)p.bh * TX * p.D * 2 + NC * p.D * 2;
     return (b + 15) & ~size_t(15);
 }
 
-template <typename SigT, bool RR>
-static void launch_bc(const DevParams& p, dim3 grid, int threads, const void* ref, const void* mat,
+template <typename SigT, bool RR, int TX>
+static bool launch_bc(const DevParams& p, int nframes, const void* ref, const void* mat,
                       long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s)
 {
-    const size_t sm = block_cost_smem(p, sizeof(SigT));
-    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    block_cost_kernel<SigT, RR><<<grid, threads, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat, sig_stride, cb,
-                                                         cell_stride);
+    const size_t sm = block_cost_smem<TX>(p, sizeof(SigT));
+    if (sm > 200 * 1024) return false;
+    dim3 grid((p.W + TX - 1) / TX, (p.H + SB_RY - 1) / SB_RY, nframes);
+    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    block_cost_kernel<SigT, RR, TX><<<grid, p.D, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat, sig_stride, cb,
+                                                          cell_stride);
+    return true;
+}
+
+template <typename SigT, bool RR>
+static void launch_bc_tx(const DevParams& p, int nframes, const void* ref, const void* mat,
+                         long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s)
+{
+    if (!launch_bc<SigT, RR, 32>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s))
+        launch_bc<SigT, RR, 8>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
 }
 
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
                        long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s,
                        bool right_ref)
 {
-    dim3 grid((p.W + SB_TX - 1) / SB_TX, p.H, nframes);
-    const int threads = p.D < 256 ? p.D : 256;
     const void* ref = right_ref ? cr : cl;
     const void* mat = right_ref ? cl : cr;
     if (p.nb <= 32) {
-        if (right_ref) launch_bc<uint32_t, true>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
-        else launch_bc<uint32_t, false>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
+        if (right_ref) launch_bc_tx<uint32_t, true>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
+        else launch_bc_tx<uint32_t, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
     } else {
-        if (right_ref) launch_bc<unsigned long long, true>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
-        else launch_bc<unsigned long long, false>(p, grid, threads, ref, mat, sig_stride, cb, cell_stride, s);
+        if (right_ref) launch_bc_tx<unsigned long long, true>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
+        else launch_bc_tx<unsigned long long, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
     }
 }
 
