@@ -115,21 +115,27 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def run_params(cfg, block: int) -> dict:
-    """Config parameters; block > 1 = SGBM with P1 = 8*area, P2 = 32*area."""
+def run_params(cfg, block: int, lr_mode: int = 0, median: int = 0) -> dict:
+    """Config parameters; block > 1 = SGBM with P1 = 8*area, P2 = 32*area (S:388);
+    lr_mode 1 = the R2 right view (reading c24); median = median ksize (c20)."""
     d = cfg.params_dict()
     if block > 1:
         d.update(block_w=block, block_h=block, p1=8 * block * block, p2=32 * block * block)
+    if lr_mode:
+        d.update(lr_mode=lr_mode)
+    if median:
+        d.update(median_ksize=median)
     return d
 
 
-def workload(block: int) -> str:
+def workload(block: int, lr_mode: int = 0, median: int = 0) -> str:
+    extra = (", R2 right view" if lr_mode else "") + (f", median {median}" if median else "")
     if block > 1:
         a = block * block
         return (f"C-SGBM{block}x{block}: 1280x720, D=128, census 9x7, {block}x{block} block, "
-                f"P1={8 * a} P2={32 * a}, 8-path SGM, uniqueness 10%, LR 1 px, sub-pixel, depth")
+                f"P1={8 * a} P2={32 * a}, 8-path SGM, uniqueness 10%, LR 1 px, sub-pixel, depth" + extra)
     return ("C: 1280x720, D=128, census 9x7, P1=8 P2=32, 8-path SGM, uniqueness 10%, LR 1 px, "
-            "sub-pixel, depth")
+            "sub-pixel, depth" + extra)
 
 
 # ----------------------------------------------------------------- oracle (CPU)
@@ -180,7 +186,7 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = synth.CONFIGS[CONFIG]
-    params = run_params(cfg, args.block)
+    params = run_params(cfg, args.block, args.lr_mode, args.median)
     Ls, Rs = synth.frame_pool(cfg, min(POOL, 4))
     nworkers, cores = oracle_workers()
     for _ in range(args.warmup):
@@ -196,7 +202,7 @@ def run_reference(args):
             "ms_per_step": round(1000 * tot / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 6),
-            "config": {"workload": workload(args.block),
+            "config": {"workload": workload(args.block, args.lr_mode, args.median),
                        "frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "frames/s", "cores": nworkers,
                              "kind": "oracle",
@@ -221,6 +227,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--block", type=int, default=1,
                     help="SGBM block size (odd; 1 = SGM, the headline line)")
+    ap.add_argument("--lr-mode", type=int, default=0, help="right view: 0 = R1 (headline), 1 = R2")
+    ap.add_argument("--median", type=int, default=0, help="median ksize 0 / 3 / 5")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -243,7 +251,7 @@ def main():
     torch.cuda.set_device(dev)
 
     cfg = synth.CONFIGS[CONFIG]
-    params = run_params(cfg, args.block)
+    params = run_params(cfg, args.block, args.lr_mode, args.median)
     B = args.frames
     H, W = cfg.height, cfg.width
     pool_L, pool_R = synth.frame_pool(cfg, POOL)
@@ -393,7 +401,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
             "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 3),
-            "config": {"workload": workload(args.block),
+            "config": {"workload": workload(args.block, args.lr_mode, args.median),
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
                        "l2": "inputs larger than L2 (236 MB/step/GPU) + per-frame scratch > L2",

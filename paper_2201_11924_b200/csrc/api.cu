@@ -48,6 +48,10 @@ struct asd_ctx {
     uint8_t* pa = nullptr;        // [B][H][W][D] u16 P_A | C << 8 (down sweep)
     uint16_t* pab = nullptr;      // [B][H][W][D] u16 partial (down + up)
     uint8_t* stash = nullptr;     // [B][H][W][D] u8 left->right path
+    // R2 on D3 (reading c24): the right-referenced pass's own partials
+    uint8_t* pa2 = nullptr;
+    uint16_t* pab2 = nullptr;
+    uint8_t* stash2 = nullptr;
     // host-path staging: two chunk buffers (inputs u8, outputs f32) + stats
     uint8_t* stage_in[2] = {nullptr, nullptr};     // [max_batch][2][H][W]
     float* stage_out[2] = {nullptr, nullptr};      // [max_batch][2][H][W]
@@ -60,7 +64,7 @@ struct asd_ctx {
     // while the row pass and WTA of group g run on s_lo on the SMs the sweep
     // clusters leave free; fork from / join back to the caller's stream.
     cudaStream_t s_hi = nullptr, s_lo = nullptr, s_cen = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_sw = nullptr, ev_hi = nullptr, ev_lo = nullptr, ev_cen = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_sw = nullptr, ev_sw2 = nullptr, ev_hi = nullptr, ev_lo = nullptr, ev_cen = nullptr;
     int group = 0;                // frames per overlap group (D3)
     std::vector<cudaEvent_t> ev_free;   // one per scratch slot (max_batch / group)
     // live stage timing (asd_profile_begin/end)
@@ -193,7 +197,7 @@ DevParams make_dev(const asd_params* p)
 }
 
 struct Layout {
-    size_t sig, s, sr, cb, pa, pab, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
+    size_t sig, s, sr, cb, pa, pab, r2, stash, px_f32, px_i16, px_u8, stage_in, stage_out, stats, total;
 };
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
@@ -210,13 +214,14 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.H * pa_cols * d.D * 2) : 0;   // P_A | C << 8, u16
     L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
     L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
+    L.r2 = (engine == ASD_ENGINE_D3 && d.lr_mode == 1) ? 1 : 0;   // doubles pa / pab / stash
     L.px_f32 = align_up(B * d.npx * 4);
     L.px_i16 = align_up(B * d.npx * 2);
     L.px_u8 = align_up(B * d.npx);
     L.stage_in = align_up(B * d.npx * 2);
     L.stage_out = align_up(B * d.npx * 2 * 4);
     L.stats = align_up(B * sizeof(asd_frame_stats));
-    L.total = 2 * L.sig + L.s + L.sr + L.cb + L.pa + L.pab + L.stash + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
+    L.total = 2 * L.sig + L.s + L.sr + L.cb + (L.pa + L.pab + L.stash) * (1 + L.r2) + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
               2 * (L.stage_in + L.stage_out + L.stats);
     return L;
 }
@@ -331,7 +336,9 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
     const int nslots = (int)c->ev_free.size();
     const int ngroups = (n + G - 1) / G;
     const long long pa_frame = (long long)p.H * c->plan.cs * c->plan.w * p.D;   // u16 elements
-    struct Slot { void* cl; void* cr; uint8_t* pa; uint16_t* pab; uint8_t* stash; FrameScratch g; };
+    struct Slot { void* cl; void* cr; uint8_t* pa; uint16_t* pab; uint8_t* stash;
+                  uint8_t* pa2; uint16_t* pab2; uint8_t* stash2; FrameScratch g; };
+    const bool r2 = c->pa2 != nullptr;             // R2: a right-referenced second pass (c24)
     auto slot_of = [&](int gi) {
         const long long b0 = (long long)(gi % nslots) * G;   // first scratch frame of the slot
         Slot q;
@@ -340,6 +347,9 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         q.pa = c->pa + b0 * pa_frame * 2;
         q.pab = c->pab + b0 * p.ncell;
         q.stash = c->stash + b0 * p.ncell;
+        q.pa2 = r2 ? c->pa2 + b0 * pa_frame * 2 : nullptr;
+        q.pab2 = r2 ? c->pab2 + b0 * p.ncell : nullptr;
+        q.stash2 = r2 ? c->stash2 + b0 * p.ncell : nullptr;
         q.g = fs;
         q.g.census_l = q.cl; q.g.census_r = q.cr;
         q.g.dl += b0 * npx; q.g.dr += b0 * npx; q.g.dstar_l += b0 * npx; q.g.dstar_r += b0 * npx;
@@ -396,6 +406,25 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             }
         }
         cudaEventRecord(c->ev_sw, c->s_hi);
+        if (r2) {                                    // the right view's own sweeps (R2)
+            {
+                ProfScope ps(c, c->s_hi, ASD_STAGE_DOWN, m * alg_bytes_down(p), m * alg_ops_sweep(p));
+                if (launch_v2_stage(0, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
+                                    nullptr, c->s_hi, 1) != 0) {
+                    set_err(c, "right-view down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                    return ASD_E_CUDA;
+                }
+            }
+            {
+                ProfScope ps(c, c->s_hi, ASD_STAGE_UP, m * alg_bytes_up(p), m * alg_ops_up(p));
+                if (launch_v2_stage(1, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
+                                    nullptr, c->s_hi) != 0) {
+                    set_err(c, "right-view up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                    return ASD_E_CUDA;
+                }
+            }
+            cudaEventRecord(c->ev_sw2, c->s_hi);
+        }
         cudaStreamWaitEvent(c->s_lo, c->ev_sw, 0);
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_ROW, m * alg_bytes_row(p), m * alg_ops_row(p));
@@ -407,9 +436,25 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_WTA, m * alg_bytes_wta3(p), m * alg_ops_wta3(p));
             if (launch_v2_stage(3, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
-                                nullptr, c->s_lo) != 0) {
+                                nullptr, c->s_lo, r2 ? 1 : 0) != 0) {
                 set_err(c, "WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                 return ASD_E_CUDA;
+            }
+        }
+        if (r2) {                                    // right view from its own aggregate
+            cudaStreamWaitEvent(c->s_lo, c->ev_sw2, 0);
+            {
+                ProfScope ps(c, c->s_lo, ASD_STAGE_ROW, m * alg_bytes_row(p), m * alg_ops_row(p));
+                launch_v2_stage(2, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
+                                nullptr, c->s_lo, 1);
+            }
+            {
+                ProfScope ps(c, c->s_lo, ASD_STAGE_WTA, m * alg_bytes_wta3(p), m * alg_ops_wta3(p));
+                if (launch_v2_stage(3, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
+                                    nullptr, c->s_lo, 2) != 0) {
+                    set_err(c, "right-view WTA launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+                    return ASD_E_CUDA;
+                }
             }
         }
         float* od = out_disp ? out_disp + f0 * npx : nullptr;
@@ -516,7 +561,7 @@ void free_ctx(asd_ctx* c)
 {
     if (!c) return;
     void* ptrs[] = {c->census_l, c->census_r, c->S, c->SR, c->cb, c->dl, c->dr, c->dstar_l, c->dstar_r,
-                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->stage_in[0], c->stage_in[1], c->stage_out[0],
+                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (int i = 0; i < 2; ++i) {
@@ -526,7 +571,7 @@ void free_ctx(asd_ctx* c)
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (cudaStream_t q : {c->s_hi, c->s_lo, c->s_cen}) if (q) cudaStreamDestroy(q);
-    for (cudaEvent_t e : {c->ev_fork, c->ev_sw, c->ev_hi, c->ev_lo, c->ev_cen}) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_sw, c->ev_sw2, c->ev_hi, c->ev_lo, c->ev_cen}) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_free) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     delete c;
@@ -622,6 +667,11 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     if (L.pa) alloc((void**)&c->pa, L.pa);
     if (L.pab) alloc((void**)&c->pab, L.pab);
     if (L.stash) alloc((void**)&c->stash, L.stash);
+    if (L.r2) {
+        alloc((void**)&c->pa2, L.pa);
+        alloc((void**)&c->pab2, L.pab);
+        alloc((void**)&c->stash2, L.stash);
+    }
     alloc((void**)&c->dl, L.px_f32); alloc((void**)&c->dr, L.px_f32);
     alloc((void**)&c->dstar_l, L.px_i16); alloc((void**)&c->dstar_r, L.px_i16);
     alloc((void**)&c->mask_l, L.px_u8); alloc((void**)&c->mask_r, L.px_u8);
@@ -644,7 +694,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
                    cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo) != cudaSuccess ||
                    cudaStreamCreateWithPriority(&c->s_cen, cudaStreamNonBlocking, hi) != cudaSuccess))
             ok = false;
-        for (cudaEvent_t* e : {&c->ev_fork, &c->ev_sw, &c->ev_hi, &c->ev_lo, &c->ev_cen})
+        for (cudaEvent_t* e : {&c->ev_fork, &c->ev_sw, &c->ev_sw2, &c->ev_hi, &c->ev_lo, &c->ev_cen})
             if (ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) ok = false;
         // overlap group: one wave of sweep clusters, at most max_batch
         const int wave = c->plan.cs > 0 ? c->plan.active_ctas / c->plan.cs : 1;
@@ -677,7 +727,8 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
     const int chunks = (n + ctx->max_batch - 1) / ctx->max_batch;
     if (ctx->engine != ASD_ENGINE_D3)
         return chunks * (3 + (ctx->dp.paths + (ctx->cb ? 1 : 0)) * (ctx->SR ? 2 : 1));
-    return 6 * ((n + ctx->group - 1) / ctx->group);   // per group: census, down, up, row, WTA, LR
+    // per group: census, down, up, row, WTA, LR (+ down, up, row, WTA of the R2 right view)
+    return (ctx->pa2 ? 10 : 6) * ((n + ctx->group - 1) / ctx->group);
 }
 
 int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }

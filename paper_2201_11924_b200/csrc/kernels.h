@@ -65,10 +65,14 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl);
 bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl);
 void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16_t* S, long long cell_stride,
                  const FrameScratch& fs, long long px_stride, cudaStream_t s);
+// variant: stage 0 -> 1 = right-referenced K_down (R2); stage 2 -> 1 = cost
+// from the P_AB | C words; stage 3 -> WTA mode (0 both views, 1 left only,
+// 2 left view written to the right-view maps).
 int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes,
                     const void* cl, const void* cr, long long sig_stride,
                     uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,
-                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s);
+                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s,
+                    int variant = 0);
 
 // Debug: materialise the raw cost volume C [H][W][D] u8 from the census images.
 void launch_cost_volume(const DevParams& p, const void* cl, const void* cr, uint8_t* cost,

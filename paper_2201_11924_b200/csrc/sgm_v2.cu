@@ -191,7 +191,10 @@ struct VGeom {
     __host__ __device__ static int slot_words(int w) { return w + T * cstride(w); }
 };
 
-template <int DC, int T, int NP, bool UP, int DPL_ROW>
+// RR (K_down only): the right view is the reference (R2, reading c24): a.cl is
+// then the right census, a.cr the left one, and the matched column of local
+// disparity j is x + delta instead of x - delta.
+template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false>
 __global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
 {
@@ -254,7 +257,7 @@ vsweep_kernel(VArgs a)
 #pragma unroll
         for (int k = 0; k < T; ++k) {
             uint32_t* dst = sl + w + k * cstr + G::coff(k);
-            const int g0 = x0 - p.min_disp - DC * k - (DC - 1);
+            const int g0 = RR ? x0 + p.min_disp + DC * k : x0 - p.min_disp - DC * k - (DC - 1);
             for (int ii = threadIdx.x; ii < n; ii += blockDim.x) {
                 const int gx = g0 + ii;
                 const bool ok = gx >= 0 && gx < W;
@@ -274,18 +277,21 @@ vsweep_kernel(VArgs a)
         }
         const uint32_t* sl = cens + slot * sw;
         const uint32_t clv = sl[xl];
-        // element for local disparity j (d = chunk*DC + j) at row[-j]
-        const uint32_t* row = sl + w + chunk * cstr + G::coff(chunk) + xl + (DC - 1);
-        const int lim = x - p.min_disp - p.R - chunk * DC;      // local j valid iff j <= lim
+        // element for local disparity j (d = chunk*DC + j) at row[-j] (RR: row[+j])
+        constexpr int SG = RR ? 1 : -1;
+        const uint32_t* row = sl + w + chunk * cstr + G::coff(chunk) + xl + (RR ? 0 : DC - 1);
+        // local j valid iff j <= lim (the matched census window lies inside the image)
+        const int lim = RR ? (W - p.R - 1) - (x + p.min_disp + chunk * DC)
+                           : x - p.min_disp - p.R - chunk * DC;
         if (lim >= DC - 1) {
 #pragma unroll
             for (int k = 0; k < NR; ++k)
-                C[k] = __byte_perm(__popc(clv ^ row[-k]), __popc(clv ^ row[-(NR + k)]), 0x5410);
+                C[k] = __byte_perm(__popc(clv ^ row[SG * k]), __popc(clv ^ row[SG * (NR + k)]), 0x5410);
         } else {
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
-                const uint32_t lo = k <= lim ? (uint32_t)__popc(clv ^ row[-k]) : (uint32_t)p.nb;
-                const uint32_t hi = NR + k <= lim ? (uint32_t)__popc(clv ^ row[-(NR + k)]) : (uint32_t)p.nb;
+                const uint32_t lo = k <= lim ? (uint32_t)__popc(clv ^ row[SG * k]) : (uint32_t)p.nb;
+                const uint32_t hi = NR + k <= lim ? (uint32_t)__popc(clv ^ row[SG * (NR + k)]) : (uint32_t)p.nb;
                 C[k] = __byte_perm(lo, hi, 0x5410);
             }
         }
@@ -800,7 +806,9 @@ __device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int la
 // L_rl written over P_AB in place, natural d order, for the WTA kernel.
 constexpr int HROW_WARPS = 4;
 
-template <int D>
+// CFROMP (R2's right-referenced pass, reading c24): the left->right path takes
+// its cost from the P_AB | C << 9 words instead of the census images.
+template <int D, bool CFROMP = false>
 __global__ void __launch_bounds__(32 * HROW_WARPS)
 hrow_kernel(RArgs a)
 {
@@ -831,7 +839,60 @@ hrow_kernel(RArgs a)
         return vrow && xb + 31 < W && xb >= p.R && xb + 31 < W - p.R && xb + lim0 >= D - 1;
     };
 
-    // ------------------------------------------------ left -> right
+    // ------------------------------------------------ left -> right, cost from P_AB | C
+    if constexpr (CFROMP) {
+        uint32_t L[NRR];
+#pragma unroll
+        for (int k = 0; k < NRR; ++k) L[k] = 0u;
+        uint32_t M = 0u;
+        uint32_t P[SG][NRR], Pn[SG][NRR];
+        auto load_c = [&](int xb, uint32_t (&PP)[SG][NRR]) {
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int x = xb + k;
+                if (x < W && active) {
+                    if constexpr (DPL == 4) {
+                        const uint2 u = *reinterpret_cast<const uint2*>(pab + (long long)x * D);
+                        PP[k][0] = u.x; PP[k][NRR - 1] = u.y;
+                    } else {
+                        PP[k][0] = *reinterpret_cast<const uint32_t*>(pab + (long long)x * D);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) PP[k][r] = 0u;
+                }
+            }
+        };
+        auto fwd = [&](int xs, const uint32_t (&PP)[SG][NRR]) {
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int x = xs + k;
+                if (x < W) {
+                    uint32_t Cc[NRR], Ln[NRR];
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) Cc[r] = (PP[k][r] >> 9) & 0x003F003Fu;
+                    M = row_rec<D>(a.p1x2, a.p2x2, lane, Cc, L, M, Ln);
+#pragma unroll
+                    for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
+                    if (active) {
+                        if constexpr (DPL == 4)
+                            *reinterpret_cast<uint32_t*>(stash + (long long)x * D) = __byte_perm(Ln[0], Ln[NRR - 1], 0x6420);
+                        else
+                            *reinterpret_cast<uint16_t*>(stash + (long long)x * D) = (uint16_t)__byte_perm(Ln[0], 0u, 0x4420);
+                    }
+                }
+            }
+        };
+        load_c(0, P);
+        for (int xs = 0; xs < W; xs += 2 * SG) {
+            load_c(xs + SG, Pn);
+            fwd(xs, P);
+            if (xs + SG >= W) break;
+            load_c(xs + 2 * SG, P);
+            fwd(xs + SG, Pn);
+        }
+    } else
+    // ------------------------------------------------ left -> right, cost from census
     {
         uint32_t L[NRR], wnd[DPL];
 #pragma unroll
@@ -966,7 +1027,10 @@ constexpr int WTA_WARPS = 8;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 
 
-template <int D, bool WIDE>
+// MODE 0: left view + re-indexed right view (R1).  MODE 1: left view only
+// (R2's left-referenced pass).  MODE 2: the "left view" of the right-referenced
+// aggregate, written to the right-view maps (R2's right view, reading c24).
+template <int D, bool WIDE, int MODE = 0>
 __global__ void __launch_bounds__(32 * WTA_WARPS)
 wta2_kernel(RArgs a)
 {
@@ -980,7 +1044,7 @@ wta2_kernel(RArgs a)
     const uint16_t* S = a.pab + frame * a.cell_stride + (long long)y * W * D;
     const bool vrow = y >= p.Q && y < p.H - p.Q;
     // right pixels with no defined disparity at all: xr + min_disp >= W
-    for (int xr = max(0, W - p.min_disp) + threadIdx.x; xr < W; xr += blockDim.x) {
+    for (int xr = max(0, W - p.min_disp) + threadIdx.x; MODE == 0 && xr < W; xr += blockDim.x) {
         const long long o = frame * a.px_stride + (long long)y * W + xr;
         a.fs.dstar_r[o] = -1;
         a.fs.mask_r[o] = MASK_BORDER;
@@ -1015,11 +1079,12 @@ wta2_kernel(RArgs a)
                 uint8_t m = 0;
                 if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
                 if (uf) m |= MASK_UNIQUE;
-                a.fs.dstar_l[o] = (int16_t)ds;
-                a.fs.mask_l[o] = m;
-                a.fs.dl[o] = disp;
+                (MODE == 2 ? a.fs.dstar_r : a.fs.dstar_l)[o] = (int16_t)ds;
+                (MODE == 2 ? a.fs.mask_r : a.fs.mask_l)[o] = m;
+                (MODE == 2 ? a.fs.dr : a.fs.dl)[o] = disp;
             }
         }
+        if constexpr (MODE != 0) continue;           // R2 passes: one view per launch
         __syncthreads();                              // left poisoning done before diagonal reads
         // right view
         {
@@ -1053,37 +1118,47 @@ typedef void (*VKernel)(VArgs);
 typedef void (*RKernel)(RArgs);
 
 template <int DC, int T, int DPL>
-static VKernel vk(int np, bool up)
+static VKernel vk(int np, bool up, bool rr)
 {
-    if (np == 3) return up ? v2::vsweep_kernel<DC, T, 3, true, DPL> : v2::vsweep_kernel<DC, T, 3, false, DPL>;
-    return up ? v2::vsweep_kernel<DC, T, 1, true, DPL> : v2::vsweep_kernel<DC, T, 1, false, DPL>;
+    if (up) return np == 3 ? v2::vsweep_kernel<DC, T, 3, true, DPL> : v2::vsweep_kernel<DC, T, 1, true, DPL>;
+    if (rr) return np == 3 ? v2::vsweep_kernel<DC, T, 3, false, DPL, true> : v2::vsweep_kernel<DC, T, 1, false, DPL, true>;
+    return np == 3 ? v2::vsweep_kernel<DC, T, 3, false, DPL> : v2::vsweep_kernel<DC, T, 1, false, DPL>;
 }
 
-static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up)
+// rr: the K_down instance with the right view as reference (R2)
+static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = false)
 {
-    if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up);
-    if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up);
-    if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up);
-    if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up);
-    if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up);
+    if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up, rr);
+    if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr);
+    if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up, rr);
+    if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up, rr);
+    if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up, rr);
     return nullptr;
 }
 
-static RKernel pick_rkernel(int D)
+static RKernel pick_rkernel(int D, bool cfromp = false)
 {
-    if (D == 16) return v2::hrow_kernel<16>;
-    if (D == 32) return v2::hrow_kernel<32>;
-    if (D == 64) return v2::hrow_kernel<64>;
-    if (D == 128) return v2::hrow_kernel<128>;
+    if (D == 16) return cfromp ? v2::hrow_kernel<16, true> : v2::hrow_kernel<16, false>;
+    if (D == 32) return cfromp ? v2::hrow_kernel<32, true> : v2::hrow_kernel<32, false>;
+    if (D == 64) return cfromp ? v2::hrow_kernel<64, true> : v2::hrow_kernel<64, false>;
+    if (D == 128) return cfromp ? v2::hrow_kernel<128, true> : v2::hrow_kernel<128, false>;
     return nullptr;
 }
 
-static RKernel pick_wkernel(int D, bool wide = false)
+template <int D>
+static RKernel wk_d(bool wide, int mode)
 {
-    if (D == 16) return wide ? v2::wta2_kernel<16, true> : v2::wta2_kernel<16, false>;
-    if (D == 32) return wide ? v2::wta2_kernel<32, true> : v2::wta2_kernel<32, false>;
-    if (D == 64) return wide ? v2::wta2_kernel<64, true> : v2::wta2_kernel<64, false>;
-    if (D == 128) return wide ? v2::wta2_kernel<128, true> : v2::wta2_kernel<128, false>;
+    if (mode == 1) return wide ? v2::wta2_kernel<D, true, 1> : v2::wta2_kernel<D, false, 1>;
+    if (mode == 2) return wide ? v2::wta2_kernel<D, true, 2> : v2::wta2_kernel<D, false, 2>;
+    return wide ? v2::wta2_kernel<D, true, 0> : v2::wta2_kernel<D, false, 0>;
+}
+
+static RKernel pick_wkernel(int D, bool wide = false, int mode = 0)
+{
+    if (D == 16) return wk_d<16>(wide, mode);
+    if (D == 32) return wk_d<32>(wide, mode);
+    if (D == 64) return wk_d<64>(wide, mode);
+    if (D == 128) return wk_d<128>(wide, mode);
     return nullptr;
 }
 
@@ -1104,7 +1179,6 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     auto no = [&](const char* why) { snprintf(pl.why, sizeof pl.why, "%s", why); pl.ok = false; return false; };
     if (p.nb > 32) return no("nb > 32 (u64 census)");
     if (p.bw * p.bh > 1) return no("SGBM block cost (> 8 bits per path) runs on engine D1");
-    if (p.lr_mode != 0) return no("the R2 right view (its own SGM) runs on engine D1");
     if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 128) return no("num_disp not in {16,32,64,128}");
     const int np = p.paths == 8 ? 3 : 1;
     if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");
@@ -1187,6 +1261,11 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     }
+    if (p.lr_mode == 1) {                            // R2: the right-referenced K_down
+        VKernel kr = pick_vkernel(pl.DC, T, pl.DPL, np, false, true);
+        cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
+        if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
     if (!wta2_plan(p, false, pl)) return no("min_disp + num_disp too large for the WTA window");
     pl.ok = true;
     return true;
@@ -1195,13 +1274,14 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
 // The WTA kernel's window: rows [256t, 256t + 255 + min + D - 1] of stage t.
 bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl)
 {
-    RKernel wk = pick_wkernel(p.D, wide);
-    if (!wk) return false;
+    if (!pick_wkernel(p.D, wide)) return false;
     pl.nbuf = ((v2::WTA_TX + p.min_disp + p.D + 31) / 32) * 32;
     pl.bstride = p.D + 2;               // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
     if (pl.rsmem > 200 * 1024) return false;
-    cudaFuncSetAttribute((const void*)wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.rsmem);
+    for (int mode = 0; mode < 3; ++mode)
+        cudaFuncSetAttribute((const void*)pick_wkernel(p.D, wide, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pl.rsmem);
     cudaGetLastError();
     pl.wide = wide;
     return true;
@@ -1235,7 +1315,7 @@ static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const
 int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes,
                     const void* cl, const void* cr, long long sig_stride,
                     uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,
-                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s)
+                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s, int variant)
 {
     if (stage == 0 || stage == 1) {
         VArgs a{};
@@ -1246,7 +1326,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         a.pin = reinterpret_cast<const uint16_t*>(pa); a.pouta = reinterpret_cast<uint16_t*>(pa);
         a.pa_stride = (long long)p.H * pl.cs * pl.w * p.D;
         a.pout16 = pab; a.cell_stride = cell_stride;
-        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1);
+        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1);
         return launch_vsweep(k, pl, nframes, a, stage == 1, s) == cudaSuccess ? 0 : -1;
     }
     (void)agg;
@@ -1257,10 +1337,10 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.p1x2 = (uint32_t)p.p1 * 0x10001u;
     r.p2x2 = (uint32_t)p.p2 * 0x10001u;
     if (stage == 2) {
-        RKernel k = pick_rkernel(p.D);
+        RKernel k = pick_rkernel(p.D, variant == 1);
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
     } else {
-        RKernel k = pick_wkernel(p.D, pl.wide);
+        RKernel k = pick_wkernel(p.D, pl.wide, variant);
         k<<<dim3(p.H, nframes), 32 * v2::WTA_WARPS, pl.rsmem, s>>>(r);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;

@@ -48,28 +48,50 @@ def test_rectified_pair_through_the_depth_path():
     compare_full(gpu_debug(d, rl, rr), oracle.compute(oracle.Params(**d), rl, rr, debug=True))
 
 
-@pytest.mark.parametrize("paths,mind,block,median", [(4, 0, 1, 0), (8, 0, 1, 0), (8, 2, 1, 0),
-                                                     (8, 0, 3, 0), (8, 0, 1, 3)])
-def test_r2_config_A(paths, mind, block, median):
+@pytest.mark.parametrize("paths,mind,block,median,engine", [
+    (4, 0, 1, 0, 1), (8, 0, 1, 0, 1), (8, 2, 1, 0, 1), (8, 0, 3, 0, 1), (8, 0, 1, 3, 1),
+    (4, 0, 1, 0, 3), (8, 0, 1, 0, 3), (8, 2, 1, 0, 3), (8, 0, 1, 3, 3)])
+def test_r2_config_A(paths, mind, block, median, engine):
     left, right, _ = synth.shift_pair(64, 48, 7, frame_idx=2)
     d = dict(synth.CONFIGS["A"].params_dict(), paths=paths, min_disp=mind, lr_mode=1,
              median_ksize=median)
     if block > 1:
         d.update(block_w=block, block_h=block, p1=8 * block * block, p2=32 * block * block)
-    g = gpu_debug(d, left, right)
+    g = gpu_debug(d, left, right, engine=engine)
     o = oracle.compute(oracle.Params(**d), left, right, debug=True)
     compare_full(g, o)
 
 
-def test_r2_config_B_full_frame():
+@pytest.mark.parametrize("engine", [1, 3])
+def test_r2_config_B_full_frame(engine):
     cfg = synth.CONFIGS["B"]
     left, right = synth.make_pair(cfg, 3)[:2]
     d = dict(cfg.params_dict(), lr_mode=1)
-    compare_full(gpu_debug(d, left, right), oracle.compute(oracle.Params(**d), left, right, debug=True))
+    compare_full(gpu_debug(d, left, right, engine=engine),
+                 oracle.compute(oracle.Params(**d), left, right, debug=True))
 
 
-def test_r2_rejects_engine_d3():
-    p = asd.Params(**dict(synth.CONFIGS["A"].params_dict(), lr_mode=1), engine=3)
-    with pytest.raises(asd.AsdError) as e:
-        asd.Stereo(p, 0, 1)
-    assert e.value.code == asd.ASD_E_UNSUPPORTED
+def test_r2_d3_batch_config_C():
+    """R2 inside the D3 group pipeline at config C (3 frames, groups of 2):
+    per-frame outputs and checksums equal the oracle's."""
+    import torch
+    from tests.gpu_util import assert_bits_equal, assert_depth_close
+    cfg = synth.CONFIGS["C"]
+    d = dict(cfg.params_dict(), lr_mode=1)
+    Ls, Rs = synth.frame_pool(cfg, 3)
+    with asd.Stereo(asd.Params(**d), 0, 4) as st:
+        assert st.engine == 3
+        st.group = 2
+        L = torch.from_numpy(Ls).cuda(); R = torch.from_numpy(Rs).cuda()
+        disp = torch.empty(3, cfg.height, cfg.width, device="cuda")
+        depth = torch.empty_like(disp)
+        stats = torch.zeros(3, 4, dtype=torch.int32, device="cuda")
+        st.asd_depth_batch(L, R, disp, depth, stats)
+        torch.cuda.synchronize()
+    disp, depth, stats = disp.cpu().numpy(), depth.cpu().numpy(), stats.cpu().numpy()
+    op = oracle.Params(**d)
+    for i in range(3):
+        o = oracle.compute(op, Ls[i], Rs[i])
+        assert_bits_equal(disp[i], o["disp"], f"disp {i}")
+        assert_depth_close(depth[i], o["depth"])
+        assert int(stats[i, 0]) & 0xFFFFFFFF == oracle.checksum(o["dstar_l"], o["mask"])
