@@ -33,7 +33,9 @@ struct asd_ctx {
     void* census_l = nullptr;
     void* census_r = nullptr;
     uint16_t* S = nullptr;
-    uint16_t* cb = nullptr;       // SGBM block cost volume [B][H][W][D] u16 (D1, block > 1)
+    uint16_t* cb = nullptr;       // SGBM block cost volume [B][H][W][D] u16 (D1, block > 1);
+                                  // D3: [B][H][cs*w][D] in the sweeps' private layout
+    uint16_t* cb2 = nullptr;      // D3 SGBM + R2: the right-referenced block cost
     uint16_t* SR = nullptr;       // right view's own aggregate [B][H][W][D] u16 (D1, lr_mode R2)
     bool wta2 = false;            // D1: WTA by the ring-window kernel (plan.nbuf / rsmem / wide)
     float* dl = nullptr;
@@ -209,11 +211,13 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     const size_t B = (size_t)max_batch;
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
     L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
-    L.cb = (engine == ASD_ENGINE_D1 && d.bw * d.bh > 1) ? align_up(B * d.ncell * 2) : 0;
+    const bool blk = d.bw * d.bh > 1;
+    L.cb = !blk ? 0 : engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2)
+                                              : align_up(B * d.H * pa_cols * d.D * 2);
     L.sr = (engine == ASD_ENGINE_D1 && d.lr_mode == 1) ? align_up(B * d.ncell * 2) : 0;
     L.pa = engine == ASD_ENGINE_D3 ? align_up(B * d.H * pa_cols * d.D * 2) : 0;   // P_A | C << 8, u16
     L.pab = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * 2) : 0;
-    L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell) : 0;
+    L.stash = engine == ASD_ENGINE_D3 ? align_up(B * d.ncell * (blk ? 2 : 1)) : 0;   // SGBM: u16
     L.r2 = (engine == ASD_ENGINE_D3 && d.lr_mode == 1) ? 1 : 0;   // doubles pa / pab / stash
     L.px_f32 = align_up(B * d.npx * 4);
     L.px_i16 = align_up(B * d.npx * 2);
@@ -221,7 +225,8 @@ Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
     L.stage_in = align_up(B * d.npx * 2);
     L.stage_out = align_up(B * d.npx * 2 * 4);
     L.stats = align_up(B * sizeof(asd_frame_stats));
-    L.total = 2 * L.sig + L.s + L.sr + L.cb + (L.pa + L.pab + L.stash) * (1 + L.r2) + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
+    L.total = 2 * L.sig + L.s + L.sr + L.cb * (1 + (engine == ASD_ENGINE_D3 ? L.r2 : 0)) +
+              (L.pa + L.pab + L.stash) * (1 + L.r2) + 2 * L.px_f32 + 2 * L.px_i16 + 2 * L.px_u8 +
               2 * (L.stage_in + L.stage_out + L.stats);
     return L;
 }
@@ -336,7 +341,9 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
     const int nslots = (int)c->ev_free.size();
     const int ngroups = (n + G - 1) / G;
     const long long pa_frame = (long long)p.H * c->plan.cs * c->plan.w * p.D;   // u16 elements
-    struct Slot { void* cl; void* cr; uint8_t* pa; uint16_t* pab; uint8_t* stash;
+    const bool blk = c->cb != nullptr;             // SGBM: block cost in the private layout
+    const int wpad = c->plan.cs * c->plan.w;
+    struct Slot { void* cl; void* cr; uint8_t* pa; uint16_t* pab; uint8_t* stash; uint16_t* cb; uint16_t* cb2;
                   uint8_t* pa2; uint16_t* pab2; uint8_t* stash2; FrameScratch g; };
     const bool r2 = c->pa2 != nullptr;             // R2: a right-referenced second pass (c24)
     auto slot_of = [&](int gi) {
@@ -346,10 +353,12 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         q.cr = (char*)c->census_r + b0 * npx * (long long)c->sig_bytes;
         q.pa = c->pa + b0 * pa_frame * 2;
         q.pab = c->pab + b0 * p.ncell;
-        q.stash = c->stash + b0 * p.ncell;
+        q.stash = c->stash + b0 * p.ncell * (blk ? 2 : 1);
+        q.cb = blk ? c->cb + b0 * pa_frame : nullptr;
+        q.cb2 = c->cb2 ? c->cb2 + b0 * pa_frame : nullptr;
         q.pa2 = r2 ? c->pa2 + b0 * pa_frame * 2 : nullptr;
         q.pab2 = r2 ? c->pab2 + b0 * p.ncell : nullptr;
-        q.stash2 = r2 ? c->stash2 + b0 * p.ncell : nullptr;
+        q.stash2 = r2 ? c->stash2 + b0 * p.ncell * (blk ? 2 : 1) : nullptr;
         q.g = fs;
         q.g.census_l = q.cl; q.g.census_r = q.cr;
         q.g.dl += b0 * npx; q.g.dr += b0 * npx; q.g.dstar_l += b0 * npx; q.g.dstar_r += b0 * npx;
@@ -377,6 +386,11 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             ProfScope ps(c, c->s_cen, ASD_STAGE_CENSUS, m * alg_bytes_census(p, c->sig_bytes));
             launch_census(p, m, il, ir, npx, q.cl, q.cr, npx, c->s_cen);
         }
+        if (blk) {                                     // SGBM: block cost(s), private layout
+            ProfScope ps(c, c->s_cen, ASD_STAGE_BLOCK, m * alg_bytes_block(p));
+            launch_block_cost(p, m, q.cl, q.cr, npx, q.cb, pa_frame, c->s_cen, false, wpad);
+            if (q.cb2) launch_block_cost(p, m, q.cl, q.cr, npx, q.cb2, pa_frame, c->s_cen, true, wpad);
+        }
         cudaEventRecord(c->ev_cen, c->s_cen);
     };
     cudaEventRecord(c->ev_fork, s);                    // inputs (and outputs) are ordered on s
@@ -390,7 +404,7 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         {
             ProfScope ps(c, c->s_hi, ASD_STAGE_DOWN, m * alg_bytes_down(p), m * alg_ops_sweep(p));
             if (launch_v2_stage(0, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
-                                nullptr, c->s_hi) != 0) {
+                                nullptr, c->s_hi, 0, q.cb) != 0) {
                 set_err(c, "down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                 return ASD_E_CUDA;
             }
@@ -400,7 +414,7 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         {
             ProfScope ps(c, c->s_hi, ASD_STAGE_UP, m * alg_bytes_up(p), m * alg_ops_up(p));
             if (launch_v2_stage(1, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
-                                nullptr, c->s_hi) != 0) {
+                                nullptr, c->s_hi, 0, q.cb) != 0) {
                 set_err(c, "up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                 return ASD_E_CUDA;
             }
@@ -410,7 +424,7 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             {
                 ProfScope ps(c, c->s_hi, ASD_STAGE_DOWN, m * alg_bytes_down(p), m * alg_ops_sweep(p));
                 if (launch_v2_stage(0, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
-                                    nullptr, c->s_hi, 1) != 0) {
+                                    nullptr, c->s_hi, 1, q.cb2) != 0) {
                     set_err(c, "right-view down sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                     return ASD_E_CUDA;
                 }
@@ -418,7 +432,7 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             {
                 ProfScope ps(c, c->s_hi, ASD_STAGE_UP, m * alg_bytes_up(p), m * alg_ops_up(p));
                 if (launch_v2_stage(1, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
-                                    nullptr, c->s_hi) != 0) {
+                                    nullptr, c->s_hi, 0, q.cb2) != 0) {
                     set_err(c, "right-view up sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
                     return ASD_E_CUDA;
                 }
@@ -429,7 +443,7 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
         {
             ProfScope ps(c, c->s_lo, ASD_STAGE_ROW, m * alg_bytes_row(p), m * alg_ops_row(p));
             launch_v2_stage(2, p, c->plan, m, q.cl, q.cr, npx, q.pa, q.pab, q.stash, p.ncell, q.g, npx,
-                            nullptr, c->s_lo);
+                            nullptr, c->s_lo, 0, q.cb);
         }
         if (agg_debug && gi == 0)            // S of frame 0 (natural order) before the WTA
             cudaMemcpyAsync(agg_debug, q.pab, (size_t)p.ncell * 2, cudaMemcpyDeviceToDevice, c->s_lo);
@@ -446,7 +460,7 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
             {
                 ProfScope ps(c, c->s_lo, ASD_STAGE_ROW, m * alg_bytes_row(p), m * alg_ops_row(p));
                 launch_v2_stage(2, p, c->plan, m, q.cr, q.cl, npx, q.pa2, q.pab2, q.stash2, p.ncell, q.g, npx,
-                                nullptr, c->s_lo, 1);
+                                nullptr, c->s_lo, 1, q.cb2);
             }
             {
                 ProfScope ps(c, c->s_lo, ASD_STAGE_WTA, m * alg_bytes_wta3(p), m * alg_ops_wta3(p));
@@ -560,7 +574,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
 void free_ctx(asd_ctx* c)
 {
     if (!c) return;
-    void* ptrs[] = {c->census_l, c->census_r, c->S, c->SR, c->cb, c->dl, c->dr, c->dstar_l, c->dstar_r,
+    void* ptrs[] = {c->census_l, c->census_r, c->S, c->SR, c->cb, c->cb2, c->dl, c->dr, c->dstar_l, c->dstar_r,
                     c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
@@ -667,6 +681,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     if (L.pa) alloc((void**)&c->pa, L.pa);
     if (L.pab) alloc((void**)&c->pab, L.pab);
     if (L.stash) alloc((void**)&c->stash, L.stash);
+    if (L.r2 && L.cb && c->engine == ASD_ENGINE_D3) alloc((void**)&c->cb2, L.cb);
     if (L.r2) {
         alloc((void**)&c->pa2, L.pa);
         alloc((void**)&c->pab2, L.pab);
@@ -728,7 +743,9 @@ int asd_launches_per_batch(const asd_ctx* ctx, int n)
     if (ctx->engine != ASD_ENGINE_D3)
         return chunks * (3 + (ctx->dp.paths + (ctx->cb ? 1 : 0)) * (ctx->SR ? 2 : 1));
     // per group: census, down, up, row, WTA, LR (+ down, up, row, WTA of the R2 right view)
-    return (ctx->pa2 ? 10 : 6) * ((n + ctx->group - 1) / ctx->group);
+    // (+ the SGBM block cost kernel(s) on the census stream)
+    const int per = (ctx->pa2 ? 10 : 6) + (ctx->cb ? (ctx->cb2 ? 2 : 1) : 0);
+    return per * ((n + ctx->group - 1) / ctx->group);
 }
 
 int asd_engine(const asd_ctx* ctx) { return ctx ? ctx->engine : 0; }

@@ -34,9 +34,11 @@ int launch_noise(const asd_noise* q, uint64_t seed, int n, int width, int height
                  uint32_t view, const float* clean, uint8_t* out, cudaStream_t s);
 
 // SGBM block cost volume CB (u16 [H][W][D] per frame), sgbm.cu.
+// priv_wpad > 0: write the D3 sweeps' private layout (D = 128, rows of
+// priv_wpad columns; cell_stride = the frame stride of that layout).
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
                        long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s,
-                       bool right_ref = false);
+                       bool right_ref = false, int priv_wpad = 0);
 
 // K4 WTA/uniqueness/sub-pixel, left + right view.
 // SR != nullptr: the right view is the WTA of its own aggregate SR (R2, c24).
@@ -57,6 +59,7 @@ struct V2Plan {
     int DPL, nbuf, bstride;
     size_t rsmem;
     bool wide;        // WTA keys in u32 (S may exceed 2^(16 - log2 D))
+    bool blk;         // SGBM: block-cost input, u16 partials without cost bits
     char why[128];
 };
 bool v2_plan(const DevParams& p, int device, V2Plan& pl);
@@ -72,7 +75,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
                     const void* cl, const void* cr, long long sig_stride,
                     uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,
                     const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s,
-                    int variant = 0);
+                    int variant = 0, const uint16_t* cbin = nullptr);
 
 // Debug: materialise the raw cost volume C [H][W][D] u8 from the census images.
 void launch_cost_volume(const DevParams& p, const void* cl, const void* cr, uint8_t* cost,

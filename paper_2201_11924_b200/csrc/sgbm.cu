@@ -29,10 +29,13 @@ constexpr int SB_RY = 16;            // rows per CTA (the block sum slides down 
 // ([bh][TX][D] u16, each thread touching only its own d), CB in registers;
 // each new row's census spans are staged in shared memory, so each (column,
 // row, d) Hamming distance is evaluated once per CTA instead of bh times.
-template <typename SigT, bool RR, int TX>
+// PRIV: write CB in the D3 sweeps' private layout (D = 128: pixel x, disparity
+// d = 32 chunk + 16 half + 4 q + j at u16 (x & ~7) * D + (32 q + 4 (x & 7) +
+// chunk) * 8 + 2 j + half of a row of wpad columns) instead of [H][W][D].
+template <typename SigT, bool RR, int TX, bool PRIV>
 __global__ void __launch_bounds__(256)
 block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base,
-                  long long sig_stride, uint16_t* __restrict__ cb_base, long long cell_stride)
+                  long long sig_stride, uint16_t* __restrict__ cb_base, long long cell_stride, int wpad)
 {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = p.W, H = p.H, D = p.D;
@@ -99,10 +102,21 @@ block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __r
         }
     };
     auto write_row = [&](int y) {
-        uint16_t* out = cb_base + frame * cell_stride + ((long long)y * W + x0) * D + d;
+        if constexpr (PRIV) {
+            const int r = d & 31;
+            const int dpart = (32 * ((r & 15) >> 2) + (d >> 5)) * 8 + 2 * (r & 3) + (r >> 4);
+            uint16_t* out = cb_base + frame * cell_stride + (long long)y * wpad * D + dpart;
 #pragma unroll
-        for (int i = 0; i < TX; ++i)
-            if (x0 + i < W) out[(long long)i * D] = (uint16_t)cb[i];
+            for (int i = 0; i < TX; ++i) {
+                const int x = x0 + i;
+                if (x < W) out[(long long)(x & ~7) * D + 32 * (x & 7)] = (uint16_t)cb[i];
+            }
+        } else {
+            uint16_t* out = cb_base + frame * cell_stride + ((long long)y * W + x0) * D + d;
+#pragma unroll
+            for (int i = 0; i < TX; ++i)
+                if (x0 + i < W) out[(long long)i * D] = (uint16_t)cb[i];
+        }
     };
     for (int v = 0; v < p.bh; ++v) {                 // rows y0 - bv .. y0 + bv -> slots 0 .. bh-1
         hrow(y0 - bv + v, v);
@@ -126,40 +140,44 @@ static size_t block_cost_smem(const DevParams& p, size_t sig)
     return (b + 15) & ~size_t(15);
 }
 
-template <typename SigT, bool RR, int TX>
+template <typename SigT, bool RR, int TX, bool PRIV>
 static bool launch_bc(const DevParams& p, int nframes, const void* ref, const void* mat,
-                      long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s)
+                      long long sig_stride, uint16_t* cb, long long cell_stride, int wpad, cudaStream_t s)
 {
     const size_t sm = block_cost_smem<TX>(p, sizeof(SigT));
     if (sm > 200 * 1024) return false;
     dim3 grid((p.W + TX - 1) / TX, (p.H + SB_RY - 1) / SB_RY, nframes);
-    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    block_cost_kernel<SigT, RR, TX><<<grid, p.D, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat, sig_stride, cb,
-                                                          cell_stride);
+    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR, TX, PRIV>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    block_cost_kernel<SigT, RR, TX, PRIV><<<grid, p.D, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat, sig_stride,
+                                                                cb, cell_stride, wpad);
     return true;
 }
 
-template <typename SigT, bool RR>
+template <typename SigT, bool RR, bool PRIV>
 static void launch_bc_tx(const DevParams& p, int nframes, const void* ref, const void* mat,
-                         long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s)
+                         long long sig_stride, uint16_t* cb, long long cell_stride, int wpad, cudaStream_t s)
 {
-    if (!launch_bc<SigT, RR, 32>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s))
-        launch_bc<SigT, RR, 8>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
+    if (!launch_bc<SigT, RR, 32, PRIV>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wpad, s))
+        launch_bc<SigT, RR, 8, PRIV>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wpad, s);
 }
 
 void launch_block_cost(const DevParams& p, int nframes, const void* cl, const void* cr,
                        long long sig_stride, uint16_t* cb, long long cell_stride, cudaStream_t s,
-                       bool right_ref)
+                       bool right_ref, int priv_wpad)
 {
     const void* ref = right_ref ? cr : cl;
     const void* mat = right_ref ? cl : cr;
-    if (p.nb <= 32) {
-        if (right_ref) launch_bc_tx<uint32_t, true>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
-        else launch_bc_tx<uint32_t, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
+    const int wp = priv_wpad;
+    if (p.nb > 32) {                                  // (D3 needs nb <= 32: never private)
+        if (right_ref) launch_bc_tx<unsigned long long, true, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, 0, s);
+        else launch_bc_tx<unsigned long long, false, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, 0, s);
+    } else if (wp > 0) {
+        if (right_ref) launch_bc_tx<uint32_t, true, true>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wp, s);
+        else launch_bc_tx<uint32_t, false, true>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wp, s);
     } else {
-        if (right_ref) launch_bc_tx<unsigned long long, true>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
-        else launch_bc_tx<unsigned long long, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, s);
+        if (right_ref) launch_bc_tx<uint32_t, true, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, 0, s);
+        else launch_bc_tx<uint32_t, false, false>(p, nframes, ref, mat, sig_stride, cb, cell_stride, 0, s);
     }
 }
 

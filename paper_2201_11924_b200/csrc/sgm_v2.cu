@@ -83,6 +83,18 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned 
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// one arrive announcing `bytes` of transaction for the phase, and bulk copies
+// that only complete transaction bytes (several per phase)
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_tx(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity)
 {
     asm volatile("{\n .reg .pred P;\n WAIT_%=:\n"
@@ -118,6 +130,7 @@ struct VArgs {
     long long cell_stride;    // H*W*D
     long long pa_stride;      // frame stride of the P_A buffer: H * (cs*w) * D
     int ablate;               // timing experiments only (ASD_V2_ABLATE, builds with -DASD_ABLATE)
+    const uint16_t* cbin;     // BLK: SGBM block cost, K_down's private layout (frame stride pa_stride)
 };
 
 // Ablation switches exist only in experiment builds (-DASD_ABLATE); in the
@@ -194,7 +207,11 @@ struct VGeom {
 // RR (K_down only): the right view is the reference (R2, reading c24): a.cl is
 // then the right census, a.cr the left one, and the matched column of local
 // disparity j is x + delta instead of x - delta.
-template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false>
+// BLK (SGBM, reading c19): the cost is the block cost CB of sgbm.cu, read
+// by TMA in this kernel's private layout (K_down: CB ring instead of census
+// staging; K_up: a CB ring beside the P_A ring), and the handoffs carry the
+// wider partials without the cost bits: K_down writes P_A (u16), K_up P_AB.
+template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
 __global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
 {
@@ -217,7 +234,10 @@ vsweep_kernel(VArgs a)
     const int sw = G::slot_words(w);
     const bool clustered = NP == 3 && a.cs > 1 && !ABL(a, 1);
 
-    const int nslot = UP ? 0 : NSLOT;
+    const int nslot = (UP || BLK) ? 0 : NSLOT;
+    constexpr bool RING = UP || BLK;                 // TMA ring(s) of per-row input blocks
+    constexpr int KR = (UP && BLK) ? 2 : KU;         // ring depth (two rings in BLK K_up)
+    constexpr int NRING = (UP && BLK) ? 2 : 1;
     uint32_t* cens = smem;                   // [NSLOT][sw] (K_down): left row, then T right-row slices
     uint32_t* hL = cens + nslot * sw;        // [2][nw][T][NR]   (NP == 3)
     uint32_t* hR = hL + 2 * nw * T * NR;
@@ -227,9 +247,11 @@ vsweep_kernel(VArgs a)
     // global stores of P_AB can be issued as contiguous 512-byte warp stores
     uint32_t* stg0 = NP == 3 ? hRM + 2 * nw : cens + nslot * sw;
     uint32_t* stg = stg0 + warp * (16 * DC);
-    // K_up input ring: KU rows of this CTA's (w columns x D) u16 block, TMA-loaded
+    // input ring(s): KR rows of this CTA's (w columns x D) u16 block, TMA-loaded
+    // (K_up: P_A | C, or P_A then CB for BLK; BLK K_down: CB)
     uint16_t* ring = reinterpret_cast<uint16_t*>(stg0 + (UP ? nw * 16 * DC : 0));
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + (UP ? KU * w * D : 0));
+    uint16_t* ring2 = ring + KR * w * D;             // BLK K_up: the CB ring
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + (RING ? NRING * KR * w * D : 0));
     // K_down -> K_up handoff in a private layout: the warp's (CPW columns x D)
     // block is contiguous and instruction q of lane l covers 16 bytes at
     // 512*q + 16*l, i.e. warp-contiguous stores and loads (row stride cs*w).
@@ -299,23 +321,39 @@ vsweep_kernel(VArgs a)
     const bool xin = x < W;
     // K_up: P_A and C of one row from K_down's packed words (reg k = cells d0+k, d0+NR+k)
     const unsigned row_bytes = (unsigned)(w * D * 2);
-    auto issue_row = [&](int i) {                    // K_up: TMA the i-th processed row into the ring
-        if (UP && threadIdx.x == 0 && i < H && !ABL(a, 64))
-            bulk_g2s(ring + (i % KU) * w * D,
-                     a.pin + frame * a.pa_stride + ((long long)row_of(i) * wpad + x0) * D, row_bytes,
-                     mbar + (i % KU));
+    auto issue_row = [&](int i) {                    // TMA the i-th processed row into the ring(s)
+        if (RING && threadIdx.x == 0 && i < H && !ABL(a, 64)) {
+            const long long roff = ((long long)row_of(i) * wpad + x0) * D;
+            uint64_t* bar = mbar + (i % KR);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_arrive_expect(bar, row_bytes * (unsigned)NRING);
+            if (UP) bulk_g2s_tx(ring + (i % KR) * w * D, a.pin + frame * a.pa_stride + roff, row_bytes, bar);
+            if (BLK) bulk_g2s_tx((UP ? ring2 : ring) + (i % KR) * w * D, a.cbin + frame * a.pa_stride + roff,
+                                 row_bytes, bar);
+        }
     };
     auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
-        if (!ABL(a, 64)) mbar_wait(mbar + (i % KU), (unsigned)((i / KU) & 1));
-        const uint4* src = reinterpret_cast<const uint4*>(ring + (i % KU) * w * D + (warp * CPW) * D) + lane;
+        if (!ABL(a, 64)) mbar_wait(mbar + (i % KR), (unsigned)((i / KR) & 1));
+        const long long boff = (long long)(i % KR) * w * D + (warp * CPW) * D;
+        const uint4* src = reinterpret_cast<const uint4*>(ring + boff) + lane;
+        const uint4* src2 = reinterpret_cast<const uint4*>((UP ? ring2 : ring) + boff) + lane;
 #pragma unroll
         for (int q = 0; q < NR / 4; ++q) {
-            const uint4 v = src[32 * q];
-            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+            if constexpr (BLK) {                     // (P_A words and) CB words as they are
+                const uint4 cv = src2[32 * q];
+                c[4 * q] = cv.x; c[4 * q + 1] = cv.y; c[4 * q + 2] = cv.z; c[4 * q + 3] = cv.w;
+                if constexpr (UP) {
+                    const uint4 v = src[32 * q];
+                    pa[4 * q] = v.x; pa[4 * q + 1] = v.y; pa[4 * q + 2] = v.z; pa[4 * q + 3] = v.w;
+                }
+            } else {
+                const uint4 v = src[32 * q];
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                pa[4 * q + j] = w4[j] & 0x00FF00FFu;
-                c[4 * q + j] = __byte_perm(w4[j], 0u, 0x4341);    // (C_lo, C_hi) as u16x2
+                for (int j = 0; j < 4; ++j) {
+                    pa[4 * q + j] = w4[j] & 0x00FF00FFu;
+                    c[4 * q + j] = __byte_perm(w4[j], 0u, 0x4341);    // (C_lo, C_hi) as u16x2
+                }
             }
         }
     };
@@ -366,13 +404,13 @@ vsweep_kernel(VArgs a)
     uint32_t PA[NR];
 
     if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
-    if (UP) {
+    if (RING) {
         if (threadIdx.x == 0) {
-            for (int s2 = 0; s2 < KU; ++s2) mbar_init(mbar + s2, 1);
+            for (int s2 = 0; s2 < KR; ++s2) mbar_init(mbar + s2, 1);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
         __syncthreads();
-        for (int i0 = 0; i0 < KU; ++i0) issue_row(i0);
+        for (int i0 = 0; i0 < KR; ++i0) issue_row(i0);
     } else {
         for (int i0 = 0; i0 < NSLOT - 1; ++i0)
             if (i0 < H) stage(row_of(i0), i0);
@@ -380,7 +418,7 @@ vsweep_kernel(VArgs a)
     }
     arrive();
     wait();
-    if (UP) load_pin(0, PA, C);
+    if (RING) load_pin(0, PA, C);
     else cost(row_of(0), 0, C);
 
     for (int i = 0; i < H; ++i) {
@@ -455,13 +493,13 @@ vsweep_kernel(VArgs a)
             Mv = 0u;
         }
         // ---- K_down: stage row i+5 (async), make row i+1's copies complete, publish
-        if (!UP) {
+        if (!RING) {
             if (i + NSLOT - 1 < H) stage(row_of(i + NSLOT - 1), (i + NSLOT - 1) % NSLOT);
             else cp_async_commit();                  // keep one group per row
             cp_async_wait<NSLOT - 2>();
         }
         arrive();
-        issue_row(i + KU);                            // K_up: row i's ring slot is free now
+        issue_row(i + KR);                            // ring input: row i's slot is free now
         // ---- partial sum out (after the release so it does not wait on these stores)
         if (!ABL(a, 2)) {
             uint32_t s[NR];
@@ -469,16 +507,18 @@ vsweep_kernel(VArgs a)
             for (int k = 0; k < NR; ++k) s[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
             if (!UP) {
                 // P_A (<= 255) | C << 8 (C <= 63): the up sweep needs no census
+                // (BLK: P_A alone, the up sweep reads CB itself)
                 uint4* dst = reinterpret_cast<uint4*>(a.pouta + frame * a.pa_stride +
                                                       ((long long)y * wpad + (x - col)) * D) + lane;
+                constexpr uint32_t CS = BLK ? 0u : 256u;
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q)
-                    dst[32 * q] = make_uint4(s[4 * q] + C[4 * q] * 256u, s[4 * q + 1] + C[4 * q + 1] * 256u,
-                                             s[4 * q + 2] + C[4 * q + 2] * 256u, s[4 * q + 3] + C[4 * q + 3] * 256u);
+                    dst[32 * q] = make_uint4(s[4 * q] + C[4 * q] * CS, s[4 * q + 1] + C[4 * q + 1] * CS,
+                                             s[4 * q + 2] + C[4 * q + 2] * CS, s[4 * q + 3] + C[4 * q + 3] * CS);
             } else {
                 // P_AB (<= 510) | C << 9: the right->left row sweep needs no census
 #pragma unroll
-                for (int k = 0; k < NR; ++k) s[k] += PA[k] + C[k] * 512u;
+                for (int k = 0; k < NR; ++k) s[k] += PA[k] + C[k] * (BLK ? 0u : 512u);
                 uint32_t o[NR];
                 if (DPL_ROW == 4) {
 #pragma unroll
@@ -519,7 +559,7 @@ vsweep_kernel(VArgs a)
         }
         // ---- next row's cost while the barrier completes
         if (i + 1 < H) {
-            if (UP) load_pin(i + 1, PA, C);
+            if (RING) load_pin(i + 1, PA, C);
             else cost(row_of(i + 1), (i + 1) % NSLOT, C);
         }
     }
@@ -541,6 +581,9 @@ struct RArgs {
     int nbuf;                 // rows of the WTA kernel's S window
     int bstride;              // u16 per window row (D + 2)
     uint32_t p1x2, p2x2;      // P1, P2 in both u16 halves
+    const uint16_t* cb;       // SGBM: block cost in the sweeps' private layout
+    long long cb_stride;      // its frame stride (H * wpad * D)
+    int wpad;                 // its row length in columns (cs * w)
 };
 
 constexpr uint32_t NONE16 = 0xFFFFu;
@@ -1013,6 +1056,115 @@ hrow_kernel(RArgs a)
     }
 }
 
+// SGBM row pass (D = 128, reading c19): the costs come from the block-cost
+// volume in the sweeps' private layout (lane l's four disparities 4l..4l+3 are
+// one half of the four words of 16-byte piece (q = l % 4, lane' = 4 (x % 8) +
+// l / 8) of the pixel's 8-column block), the partial P_AB is the full u16 word
+// and the left->right path is stashed as u16 (it exceeds 8 bits).
+template <int D>
+__global__ void __launch_bounds__(32 * HROW_WARPS)
+hrow_blk_kernel(RArgs a)
+{
+    static_assert(D == 128, "SGBM row pass: D = 128 only");
+    constexpr int NRR = 2, SG = 8;
+    const DevParams& p = a.p;
+    const int W = p.W, H = p.H;
+    const int frame = blockIdx.y;
+    const int y = blockIdx.x * HROW_WARPS + (threadIdx.x >> 5);
+    if (y >= H) return;
+    const int lane = threadIdx.x & 31;
+    const int d0 = lane * 4;
+    const long long rowcell = frame * a.cell_stride + (long long)y * W * D + d0;
+    uint16_t* stash = reinterpret_cast<uint16_t*>(a.stash) + rowcell;
+    uint16_t* pab = a.pab + rowcell;
+    const uint16_t* cbrow = a.cb + frame * a.cb_stride + (long long)y * a.wpad * D
+                          + (32 * (lane & 3) + (lane >> 3)) * 8;
+    const uint32_t sel = ((lane >> 2) & 1) ? 0x7632u : 0x5410u;
+    auto cost = [&](int x, uint32_t (&Cc)[NRR]) {      // (A, B) = ((d0, d0+2), (d0+1, d0+3))
+        const uint4 v = *reinterpret_cast<const uint4*>(cbrow + (long long)(x & ~7) * D + 32 * (x & 7));
+        Cc[0] = __byte_perm(v.x, v.z, sel);
+        Cc[1] = __byte_perm(v.y, v.w, sel);
+    };
+    // ------------------------------------------------ left -> right
+    {
+        uint32_t L[NRR] = {0u, 0u}, M = 0u;
+        uint32_t Cg[SG][NRR], Cn[SG][NRR];
+        auto load = [&](int xb, uint32_t (&CC)[SG][NRR]) {
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                if (xb + k < W) cost(xb + k, CC[k]);
+                else { CC[k][0] = 0u; CC[k][1] = 0u; }
+            }
+        };
+        auto fwd = [&](int xs, const uint32_t (&CC)[SG][NRR]) {
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int x = xs + k;
+                if (x < W) {
+                    uint32_t Ln[NRR];
+                    M = row_rec<D>(a.p1x2, a.p2x2, lane, CC[k], L, M, Ln);
+                    L[0] = Ln[0]; L[1] = Ln[1];
+                    *reinterpret_cast<uint2*>(stash + (long long)x * D) = make_uint2(Ln[0], Ln[1]);
+                }
+            }
+        };
+        load(0, Cg);
+        for (int xs = 0; xs < W; xs += 2 * SG) {
+            load(xs + SG, Cn);
+            fwd(xs, Cg);
+            if (xs + SG >= W) break;
+            load(xs + 2 * SG, Cg);
+            fwd(xs + SG, Cn);
+        }
+    }
+    __syncwarp();
+    // ------------------------------------------------ right -> left, S out
+    {
+        uint32_t L[NRR] = {0u, 0u}, M = 0u;
+        uint32_t P[SG][NRR], Cg[SG][NRR], Sx[SG][NRR], Pn[SG][NRR], Cn[SG][NRR], Sn[SG][NRR];
+        auto load = [&](int xb, uint32_t (&PP)[SG][NRR], uint32_t (&CC)[SG][NRR], uint32_t (&SS)[SG][NRR]) {
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int x = xb + k;
+                if (x >= 0 && x < W) {
+                    const uint2 u = *reinterpret_cast<const uint2*>(pab + (long long)x * D);
+                    const uint2 t = *reinterpret_cast<const uint2*>(stash + (long long)x * D);
+                    PP[k][0] = u.x; PP[k][1] = u.y;
+                    SS[k][0] = t.x; SS[k][1] = t.y;
+                    cost(x, CC[k]);
+                } else {
+                    PP[k][0] = PP[k][1] = 0u; SS[k][0] = SS[k][1] = 0u; CC[k][0] = CC[k][1] = 0u;
+                }
+            }
+        };
+        auto bwd = [&](int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&CC)[SG][NRR],
+                       const uint32_t (&SS)[SG][NRR]) {
+#pragma unroll
+            for (int k = SG - 1; k >= 0; --k) {
+                const int x = xs + k;
+                if (x < W) {
+                    uint32_t Ln[NRR];
+                    M = row_rec<D>(a.p1x2, a.p2x2, lane, CC[k], L, M, Ln);
+                    L[0] = Ln[0]; L[1] = Ln[1];
+                    const uint32_t s0 = PP[k][0] + SS[k][0] + Ln[0];
+                    const uint32_t s1 = PP[k][1] + SS[k][1] + Ln[1];
+                    *reinterpret_cast<uint2*>(pab + (long long)x * D) =
+                        make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
+                }
+            }
+        };
+        const int xtop = ((W - 1) / SG) * SG;
+        load(xtop, P, Cg, Sx);
+        for (int xs = xtop; xs >= 0; xs -= 2 * SG) {
+            load(xs - SG, Pn, Cn, Sn);
+            bwd(xs, P, Cg, Sx);
+            if (xs - SG < 0) break;
+            load(xs - 2 * SG, P, Cg, Sx);
+            bwd(xs - SG, Pn, Cn, Sn);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- K_wta
 // WTA / uniqueness / sub-pixel for the left view and the re-indexed right view
 // (K4 semantics, post.cu) from S rows staged in shared memory.  One CTA (8
@@ -1125,9 +1277,15 @@ static VKernel vk(int np, bool up, bool rr)
     return np == 3 ? v2::vsweep_kernel<DC, T, 3, false, DPL> : v2::vsweep_kernel<DC, T, 1, false, DPL>;
 }
 
-// rr: the K_down instance with the right view as reference (R2)
-static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = false)
+// rr: the K_down instance with the right view as reference (R2); blk: the SGBM
+// instances (D = 128: DC = 32, T = 4, 8 paths only)
+static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = false, bool blk = false)
 {
+    if (blk) {
+        if (DC != 32 || T != 4 || DPL != 4 || np != 3) return nullptr;
+        if (up) return v2::vsweep_kernel<32, 4, 3, true, 4, false, true>;
+        return rr ? v2::vsweep_kernel<32, 4, 3, false, 4, true, true> : v2::vsweep_kernel<32, 4, 3, false, 4, false, true>;
+    }
     if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up, rr);
     if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr);
     if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up, rr);
@@ -1162,14 +1320,17 @@ static RKernel pick_wkernel(int D, bool wide = false, int mode = 0)
     return nullptr;
 }
 
-static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up)
+static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up, bool blk = false)
 {
     const int nw = w * T / 32;
     const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
-    size_t words = up ? 0 : (size_t)v2::NSLOT * ((size_t)w + (size_t)T * cstr);
+    size_t words = (up || blk) ? 0 : (size_t)v2::NSLOT * ((size_t)w + (size_t)T * cstr);
     if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
     words += (size_t)nw * 16 * DC;                    // K_up output staging
-    if (up) words += (size_t)v2::KU * w * D / 2 + 2 * v2::KU + 4;   // TMA ring + mbarriers (+ align)
+    if (up || blk) {                                  // TMA ring(s) + mbarriers (+ align)
+        const int kr = (up && blk) ? 2 : v2::KU, nring = (up && blk) ? 2 : 1;
+        words += (size_t)nring * kr * w * D / 2 + 2 * kr + 4;
+    }
     return words * 4;
 }
 
@@ -1178,14 +1339,18 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     pl = V2Plan{};
     auto no = [&](const char* why) { snprintf(pl.why, sizeof pl.why, "%s", why); pl.ok = false; return false; };
     if (p.nb > 32) return no("nb > 32 (u64 census)");
-    if (p.bw * p.bh > 1) return no("SGBM block cost (> 8 bits per path) runs on engine D1");
     if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 128) return no("num_disp not in {16,32,64,128}");
     const int np = p.paths == 8 ? 3 : 1;
-    if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");
-    int ks = 1;
-    while ((1 << ks) < p.D) ++ks;
-    const long long smax = (long long)p.paths * (p.nb + p.p2);
-    if ((smax << ks) + (1 << ks) - 1 > 0xFFFE) return no("S << log2(D) exceeds 16-bit WTA keys");
+    if (p.bw * p.bh > 1) {
+        // SGBM: u16 partials without cost bits (S <= 65534 validated by asd_create), u32 WTA keys
+        if (p.D != 128 || np != 3) return no("SGBM on engine D3 needs num_disp = 128 and 8 paths");
+    } else {
+        if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");
+        int ks = 1;
+        while ((1 << ks) < p.D) ++ks;
+        const long long smax = (long long)p.paths * (p.nb + p.p2);
+        if ((smax << ks) + (1 << ks) - 1 > 0xFFFE) return no("S << log2(D) exceeds 16-bit WTA keys");
+    }
     pl.NP = np;
     pl.DPL = p.D <= 64 ? 2 : 4;
     if (p.D == 16) { pl.DC = 16; pl.T = 1; }
@@ -1196,9 +1361,11 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     if (p.D == 128 && force && force[0] == '1') { pl.DC = 16; pl.T = 8; }
     const int T = pl.T, CPW = 32 / T;
     const int maxt = pl.DC == 32 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
-    VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false);
-    VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true);
-    if (!kd || !ku) return no("no sweep kernel instance");
+    const bool blk = p.bw * p.bh > 1;                // SGBM block cost (reading c19)
+    pl.blk = blk;
+    VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk);
+    VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk);
+    if (!kd || !ku) return no(blk ? "SGBM on engine D3 needs num_disp = 128 and 8 paths" : "no sweep kernel instance");
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double best = -1.0;
@@ -1212,8 +1379,8 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         const int threads = w * T;
         if (threads > maxt) continue;
         if (np == 1 && cs > 1 && threads < 128) continue;
-        const size_t smd = vsmem_bytes(w, p.D, T, pl.DC, np, false);
-        const size_t sm = vsmem_bytes(w, p.D, T, pl.DC, np, true);
+        const size_t smd = vsmem_bytes(w, p.D, T, pl.DC, np, false, blk);
+        const size_t sm = vsmem_bytes(w, p.D, T, pl.DC, np, true, blk);
         if (sm > 220 * 1024 || smd > 220 * 1024) continue;
         cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smd);
         cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1256,17 +1423,17 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         pl.w = w;
         pl.cs = (p.W + w - 1) / w;
         pl.vthreads = w * T;
-        pl.vsmem = vsmem_bytes(w, p.D, T, pl.DC, np, false);
-        pl.vsmem_up = vsmem_bytes(w, p.D, T, pl.DC, np, true);
+        pl.vsmem = vsmem_bytes(w, p.D, T, pl.DC, np, false, blk);
+        pl.vsmem_up = vsmem_bytes(w, p.D, T, pl.DC, np, true, blk);
         cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     }
     if (p.lr_mode == 1) {                            // R2: the right-referenced K_down
-        VKernel kr = pick_vkernel(pl.DC, T, pl.DPL, np, false, true);
+        VKernel kr = pick_vkernel(pl.DC, T, pl.DPL, np, false, true, blk);
         cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
-    if (!wta2_plan(p, false, pl)) return no("min_disp + num_disp too large for the WTA window");
+    if (!wta2_plan(p, blk, pl)) return no("min_disp + num_disp too large for the WTA window");
     pl.ok = true;
     return true;
 }
@@ -1315,7 +1482,8 @@ static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const
 int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes,
                     const void* cl, const void* cr, long long sig_stride,
                     uint8_t* pa, uint16_t* pab, uint8_t* stash, long long cell_stride,
-                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s, int variant)
+                    const FrameScratch& fs, long long px_stride, uint16_t* agg, cudaStream_t s, int variant,
+                    const uint16_t* cbin)
 {
     if (stage == 0 || stage == 1) {
         VArgs a{};
@@ -1326,7 +1494,8 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         a.pin = reinterpret_cast<const uint16_t*>(pa); a.pouta = reinterpret_cast<uint16_t*>(pa);
         a.pa_stride = (long long)p.H * pl.cs * pl.w * p.D;
         a.pout16 = pab; a.cell_stride = cell_stride;
-        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1);
+        a.cbin = cbin;
+        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1, pl.blk);
         return launch_vsweep(k, pl, nframes, a, stage == 1, s) == cudaSuccess ? 0 : -1;
     }
     (void)agg;
@@ -1336,8 +1505,9 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.nbuf = pl.nbuf; r.bstride = pl.bstride;
     r.p1x2 = (uint32_t)p.p1 * 0x10001u;
     r.p2x2 = (uint32_t)p.p2 * 0x10001u;
+    r.cb = cbin; r.cb_stride = (long long)p.H * pl.cs * pl.w * p.D; r.wpad = pl.cs * pl.w;
     if (stage == 2) {
-        RKernel k = pick_rkernel(p.D, variant == 1);
+        RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1);
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
     } else {
         RKernel k = pick_wkernel(p.D, pl.wide, variant);

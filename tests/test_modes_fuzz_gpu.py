@@ -21,6 +21,11 @@ CASES = [
     (90, 33, 16, 4, 9, 9, 4, 3, 5, 1),        # nb = 40 (u64 census): D1 only
     (33, 50, 64, 0, 9, 7, 8, 7, 0, 0),
     (12, 9, 16, 0, 3, 3, 8, 3, 3, 1),         # tiny image
+    # SGBM at D = 128 (engine D3: block cost in the sweeps' private layout)
+    (300, 37, 128, 0, 9, 7, 8, 3, 0, 0),
+    (257, 21, 128, 5, 7, 7, 8, 3, 3, 1),
+    (130, 20, 128, 2, 5, 5, 8, 5, 0, 1),
+    (1283, 9, 128, 0, 9, 7, 8, 3, 5, 0),      # several cluster CTAs, ragged last CTA
 ]
 
 

@@ -62,24 +62,26 @@ def test_sgbm_block_1x1_equals_sgm():
     assert_bits_equal(g0["disp"], g1["disp"], "disp")
 
 
-def test_sgbm_rejects_engine_d3():
+def test_sgbm_d3_needs_d128():
+    """SGBM on engine D3 is built for num_disp = 128 (config A has 16): D1 only."""
     p = asd.Params(**_cfg("A", 3, 3), engine=3)
     with pytest.raises(asd.AsdError) as e:
         asd.Stereo(p, 0, 1)
     assert e.value.code == asd.ASD_E_UNSUPPORTED
 
 
-def test_sgbm_batch_config_C_sampled():
-    """Config C with a 3x3 block in a batch of 2 (bench-sized frames): the
-    per-frame checksums and valid counts equal the oracle's; S at sampled
-    pixels equals the oracle's per-pixel route."""
+@pytest.mark.parametrize("engine", [1, 3])
+def test_sgbm_batch_config_C_sampled(engine):
+    """Config C with a 3x3 block in a batch of 2 (bench-sized frames) on both
+    engines (D3: block cost in the sweeps' private layout, u16 partials): the
+    per-frame disparities, depths, checksums and valid counts equal the oracle's."""
     import torch
     cfg = synth.CONFIGS["C"]
     d = _cfg("C", 3, 3)
     Ls, Rs = synth.frame_pool(cfg, 2)
-    p = asd.Params(**d)
+    p = asd.Params(**d, engine=engine)
     with asd.Stereo(p, 0, 2) as st:
-        assert st.engine == 1
+        assert st.engine == engine
         L = torch.from_numpy(Ls).cuda(); R = torch.from_numpy(Rs).cuda()
         disp = torch.empty(2, cfg.height, cfg.width, device="cuda")
         depth = torch.empty_like(disp)
