@@ -1062,11 +1062,11 @@ hrow_kernel(RArgs a)
 // l / 8) of the pixel's 8-column block), the partial P_AB is the full u16 word
 // and the left->right path is stashed as u16 (it exceeds 8 bits).
 template <int D>
-__global__ void __launch_bounds__(32 * HROW_WARPS)
+__global__ void __launch_bounds__(32 * HROW_WARPS, 4)
 hrow_blk_kernel(RArgs a)
 {
     static_assert(D == 128, "SGBM row pass: D = 128 only");
-    constexpr int NRR = 2, SG = 8;
+    constexpr int NRR = 2, SG = 4;
     const DevParams& p = a.p;
     const int W = p.W, H = p.H;
     const int frame = blockIdx.y;

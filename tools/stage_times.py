@@ -17,11 +17,18 @@ ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--timeline", action="store_true", help="print the per-launch timeline")
 ap.add_argument("--group", type=int, default=0, help="D3 pipeline group (frames); 0 = default")
+ap.add_argument("--block", type=int, default=1, help="SGBM block (P1/P2 scaled by its area)")
+ap.add_argument("--lr-mode", type=int, default=0)
 args = ap.parse_args()
 cfg = synth.CONFIGS[args.config]
 d = cfg.params_dict()
 if args.paths:
     d["paths"] = args.paths
+if args.block > 1:
+    a2 = args.block * args.block
+    d.update(block_w=args.block, block_h=args.block, p1=8 * a2, p2=32 * a2)
+if args.lr_mode:
+    d["lr_mode"] = args.lr_mode
 Lp, Rp = synth.frame_pool(cfg, 4)
 idx = [i % 4 for i in range(args.frames)]
 L = torch.from_numpy(Lp[idx]).cuda(); R = torch.from_numpy(Rp[idx]).cuda()
