@@ -32,11 +32,16 @@ constexpr int SB_RY = 16;            // rows per CTA (the block sum slides down 
 // PRIV: write CB in the D3 sweeps' private layout (D = 128: pixel x, disparity
 // d = 32 chunk + 16 half + 4 q + j at u16 (x & ~7) * D + (32 q + 4 (x & 7) +
 // chunk) * 8 + 2 j + half of a row of wpad columns) instead of [H][W][D].
-template <typename SigT, bool RR, int TX, bool PRIV>
+// BW > 0: the block width as a compile-time constant: the horizontal window
+// then lives in registers (fully unrolled over the TX + BW - 1 block columns)
+// and invalid census words carry bit 31 (MARK; needs nb <= 31) instead of
+// separate validity flags.  BW == 0: the generic form.
+template <typename SigT, bool RR, int TX, bool PRIV, int BW = 0>
 __global__ void __launch_bounds__(256)
 block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base,
                   long long sig_stride, uint16_t* __restrict__ cb_base, long long cell_stride, int wpad)
 {
+    constexpr bool MARK = BW > 0;
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int W = p.W, H = p.H, D = p.D;
     const int bu = p.bw / 2, bv = p.bh / 2;
@@ -62,14 +67,14 @@ block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __r
         const int r = i / NC, c = i - r * NC;
         const int xx = x0 - bu + c, yy = y0 - bv + r;
         const bool ok = yy >= 0 && yy < H && xx >= 0 && xx < W && census_valid(p, xx, yy);
-        Ls[i] = ok ? cl[(long long)yy * W + xx] : (SigT)0;
+        Ls[i] = ok ? cl[(long long)yy * W + xx] : (MARK ? (SigT)0x80000000u : (SigT)0);
         Lv[i] = ok;
     }
     for (int i = threadIdx.x; i < NY * NRW; i += blockDim.x) {
         const int r = i / NRW, c = i - r * NRW;
         const int xr = xr0 + c, yy = y0 - bv + r;
         const bool ok = yy >= 0 && yy < H && xr >= 0 && xr < W && census_valid(p, xr, yy);
-        Rs[i] = ok ? cr[(long long)yy * W + xr] : (SigT)0;
+        Rs[i] = ok ? cr[(long long)yy * W + xr] : (MARK ? (SigT)0x80000000u : (SigT)0);
         Rv[i] = ok;
     }
     __syncthreads();
@@ -82,13 +87,28 @@ block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __r
         const unsigned char* lv = Lv + (size_t)r * NC;
         const unsigned char* rv = Rv + (size_t)r * NRW;
         uint32_t run = 0;
-        for (int c = 0; c < NC; ++c) {              // window sums over bw block columns
-            const int rc = RR ? c + d : c + (D - 1) - d;
-            const uint32_t cv = (lv[c] && rv[rc]) ? (uint32_t)popc_sig(L[c] ^ R[rc]) : (uint32_t)p.nb;
-            Cc[(size_t)c * D + d] = (uint16_t)cv;
-            run += cv;
-            if (c >= p.bw) run -= Cc[(size_t)(c - p.bw) * D + d];
-            if (c + 1 >= p.bw) Hr[((size_t)slot * TX + (c + 1 - p.bw)) * D + d] = (uint16_t)run;
+        if constexpr (BW > 0) {                      // register window, marked census words
+            const SigT* Rd = R + (RR ? d : (D - 1) - d);
+            const uint32_t nbv = (uint32_t)p.nb;
+            uint32_t win[BW];
+#pragma unroll
+            for (int c = 0; c < TX + BW - 1; ++c) {
+                const uint32_t l = (uint32_t)L[c], r2 = (uint32_t)Rd[c];
+                const uint32_t cv = ((l | r2) & 0x80000000u) ? nbv : (uint32_t)__popc(l ^ r2);
+                run += cv;
+                if (c >= BW) run -= win[c % BW];
+                win[c % BW] = cv;
+                if (c + 1 >= BW) Hr[((size_t)slot * TX + (c + 1 - BW)) * D + d] = (uint16_t)run;
+            }
+        } else {
+            for (int c = 0; c < NC; ++c) {          // window sums over bw block columns
+                const int rc = RR ? c + d : c + (D - 1) - d;
+                const uint32_t cv = (lv[c] && rv[rc]) ? (uint32_t)popc_sig(L[c] ^ R[rc]) : (uint32_t)p.nb;
+                Cc[(size_t)c * D + d] = (uint16_t)cv;
+                run += cv;
+                if (c >= p.bw) run -= Cc[(size_t)(c - p.bw) * D + d];
+                if (c + 1 >= p.bw) Hr[((size_t)slot * TX + (c + 1 - p.bw)) * D + d] = (uint16_t)run;
+            }
         }
     };
     uint32_t cb[TX];
@@ -140,6 +160,16 @@ static size_t block_cost_smem(const DevParams& p, size_t sig)
     return (b + 15) & ~size_t(15);
 }
 
+template <typename SigT, bool RR, int TX, bool PRIV, int BW>
+static void launch_bc_k(const DevParams& p, dim3 grid, size_t sm, const void* ref, const void* mat,
+                        long long sig_stride, uint16_t* cb, long long cell_stride, int wpad, cudaStream_t s)
+{
+    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR, TX, PRIV, BW>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    block_cost_kernel<SigT, RR, TX, PRIV, BW><<<grid, p.D, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat,
+                                                                    sig_stride, cb, cell_stride, wpad);
+}
+
 template <typename SigT, bool RR, int TX, bool PRIV>
 static bool launch_bc(const DevParams& p, int nframes, const void* ref, const void* mat,
                       long long sig_stride, uint16_t* cb, long long cell_stride, int wpad, cudaStream_t s)
@@ -147,10 +177,11 @@ static bool launch_bc(const DevParams& p, int nframes, const void* ref, const vo
     const size_t sm = block_cost_smem<TX>(p, sizeof(SigT));
     if (sm > 200 * 1024) return false;
     dim3 grid((p.W + TX - 1) / TX, (p.H + SB_RY - 1) / SB_RY, nframes);
-    cudaFuncSetAttribute((const void*)block_cost_kernel<SigT, RR, TX, PRIV>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    block_cost_kernel<SigT, RR, TX, PRIV><<<grid, p.D, sm, s>>>(p, (const SigT*)ref, (const SigT*)mat, sig_stride,
-                                                                cb, cell_stride, wpad);
+    const bool mark = sizeof(SigT) == 4 && p.nb <= 31;      // bit 31 free for the invalid marker
+    if (mark && p.bw == 3) launch_bc_k<SigT, RR, TX, PRIV, 3>(p, grid, sm, ref, mat, sig_stride, cb, cell_stride, wpad, s);
+    else if (mark && p.bw == 5) launch_bc_k<SigT, RR, TX, PRIV, 5>(p, grid, sm, ref, mat, sig_stride, cb, cell_stride, wpad, s);
+    else if (mark && p.bw == 7) launch_bc_k<SigT, RR, TX, PRIV, 7>(p, grid, sm, ref, mat, sig_stride, cb, cell_stride, wpad, s);
+    else launch_bc_k<SigT, RR, TX, PRIV, 0>(p, grid, sm, ref, mat, sig_stride, cb, cell_stride, wpad, s);
     return true;
 }
 
