@@ -738,14 +738,39 @@ __device__ __forceinline__ void wta_right_lin(const DevParams& p, uint16_t* b0, 
         }
         kb = min(k0, k1);
     } else {
-        uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
+        // packed keys, plus the minimum S of each 8-disparity block for the
+        // second-best search below (no second pass over the diagonal)
+        uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu, bm[D / 8];
 #pragma unroll
         for (int d = 0; d < D; d += 4) {
-            k0 = vmin2(k0, pair(d) * (1u << KS) + ((uint32_t)d | ((uint32_t)(d + 1) << 16)));
-            k1 = vmin2(k1, pair(d + 2) * (1u << KS) + ((uint32_t)(d + 2) | ((uint32_t)(d + 3) << 16)));
+            const uint32_t pa = pair(d), pb = pair(d + 2);
+            k0 = vmin2(k0, pa * (1u << KS) + ((uint32_t)d | ((uint32_t)(d + 1) << 16)));
+            k1 = vmin2(k1, pb * (1u << KS) + ((uint32_t)(d + 2) | ((uint32_t)(d + 3) << 16)));
+            bm[d / 8] = (d % 8 == 0) ? vmin2(pa, pb) : vmin2(bm[d / 8], vmin2(pa, pb));
         }
         const uint32_t km = vmin2(k0, k1);
         kb = min(km & 0xFFFFu, km >> 16);
+        dstar = (int)(kb & ((1u << KS) - 1u));
+        const uint32_t s0 = kb >> KS;
+        const uint16_t* c0 = b0 + dstar * STEP;
+        const uint32_t cm = dstar >= 1 ? c0[-STEP] : NONE16;
+        const uint32_t cp = dstar + 1 < D ? c0[STEP] : NONE16;
+        // second best over |d - d*| >= 2: whole blocks clear of d*-1..d*+1 from
+        // their minima, the (one or two) blocks holding them element by element
+        const int blo = max(dstar - 1, 0) >> 3, bhi = min(dstar + 1, D - 1) >> 3;
+        uint32_t sec = 0xFFFFFFFFu;
+#pragma unroll
+        for (int b = 0; b < D / 8; ++b)
+            if (b < blo || b > bhi) sec = vmin2(sec, bm[b]);
+        uint32_t s2 = min(sec & 0xFFFFu, sec >> 16);
+        for (int b = blo; b <= bhi; ++b)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int d = 8 * b + j;
+                if (d < dstar - 1 || d > dstar + 1) s2 = min(s2, (uint32_t)b0[d * STEP]);
+            }
+        finish_wta(p, dstar, s0, s2, cm, cp, uf, disp);
+        return;
     }
     dstar = (int)(kb & ((1u << KS) - 1u));
     const uint32_t s0 = kb >> KS;
