@@ -1235,13 +1235,25 @@ wta2_kernel(RArgs a)
         const int hi = min(W, x0 + WTA_TX + p.min_disp + D - 1);
         __syncthreads();                              // previous stage done with the window
         {   // thread t copies word t % CH of rows x0 + t / CH, + RSTEP, ...
+            // (32-bit shared address and global pointer stepped, 4 copies per trip)
             constexpr int RSTEP = 32 * WTA_WARPS / CH;
             const int c = threadIdx.x % CH;
-            int slot = threadIdx.x / CH;
-            const uint16_t* src = S + (long long)(x0 + slot) * D + c * 2;
-            for (; x0 + slot < hi; slot += RSTEP, src += RSTEP * D)
-                cp_async4(reinterpret_cast<uint32_t*>(sbuf + slot * BS + c * 2),
-                          reinterpret_cast<const uint32_t*>(src), true);
+            const int slot0 = threadIdx.x / CH;
+            const int n = (hi - x0 - slot0 + RSTEP - 1) / RSTEP;     // rows this thread copies
+            unsigned sa = smem_u32(sbuf + slot0 * BS + c * 2);
+            const uint16_t* src = S + (long long)(x0 + slot0) * D + c * 2;
+            constexpr unsigned SSTEP = RSTEP * BS * 2;
+            int k = 0;
+            for (; k + 4 <= n; k += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n"
+                                 :: "r"(sa + u * SSTEP), "l"(src + u * RSTEP * D) : "memory");
+                sa += 4 * SSTEP;
+                src += 4 * RSTEP * D;
+            }
+            for (; k < n; ++k, sa += SSTEP, src += RSTEP * D)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(sa), "l"(src) : "memory");
         }
         cp_async_commit();
         cp_async_wait<0>();
