@@ -606,12 +606,19 @@ __device__ __forceinline__ void finish_wta(const DevParams& p, int dstar, uint32
     disp = __fadd_rn((float)(p.min_disp + dstar), off);
 }
 
+#ifndef ASD_WTA_PAD
+#define ASD_WTA_PAD 2
+#define ASD_WTA_CHUNK 4
+#endif
+constexpr int WTA_PAD = ASD_WTA_PAD;      // u16 of padding per window row
+constexpr int WTA_CHUNK = ASD_WTA_CHUNK;  // bytes per cp.async of the window fill
+
 template <int D> struct RowGeom {
     static constexpr int DPL = D == 128 ? 4 : 2;     // disparities per lane
     static constexpr int NRR = DPL / 2;              // u16x2 registers per lane
     static constexpr int ACT = D / DPL;              // active lanes
     static constexpr int NB = D + 40;                // rows of the S window (D + 32 + one sub-group)
-    static constexpr int BS = D + 2;                 // u16 per WTA ring row: an odd number of
+    static constexpr int BS = D + WTA_PAD;           // u16 per WTA window row (WTA_PAD = 2: an odd number of
                                                      // 4-byte words, so the 32 lanes of the
                                                      // diagonal (right-view) scan hit 32 banks
     static constexpr int KS = D <= 16 ? 4 : D <= 32 ? 5 : D <= 64 ? 6 : 7;   // key shift = log2(D)
@@ -1227,7 +1234,7 @@ wta2_kernel(RArgs a)
         a.fs.mask_r[o] = MASK_BORDER;
         a.fs.dr[o] = 0.0f;
     }
-    constexpr int CH = D * 2 / 4;                     // 4-byte words per S row (window rows are 4-byte aligned)
+    constexpr int CH = D * 2 / WTA_CHUNK;             // copy pieces per S row
     const int nstage = (W + WTA_TX - 1) / WTA_TX;
     for (int t = 0; t < nstage; ++t) {
         // linear window of this stage: row x at slot x - x0, rows [x0, hi)
@@ -1240,20 +1247,24 @@ wta2_kernel(RArgs a)
             const int c = threadIdx.x % CH;
             const int slot0 = threadIdx.x / CH;
             const int n = (hi - x0 - slot0 + RSTEP - 1) / RSTEP;     // rows this thread copies
-            unsigned sa = smem_u32(sbuf + slot0 * BS + c * 2);
-            const uint16_t* src = S + (long long)(x0 + slot0) * D + c * 2;
+            constexpr int PU = WTA_CHUNK / 2;                  // u16 per piece
+            unsigned sa = smem_u32(sbuf + slot0 * BS + c * PU);
+            const uint16_t* src = S + (long long)(x0 + slot0) * D + c * PU;
             constexpr unsigned SSTEP = RSTEP * BS * 2;
+            auto cp = [](unsigned dst, const uint16_t* g) {
+                if constexpr (WTA_CHUNK == 16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(dst), "l"(g) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" :: "r"(dst), "l"(g), "n"(WTA_CHUNK) : "memory");
+            };
             int k = 0;
             for (; k + 4 <= n; k += 4) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n"
-                                 :: "r"(sa + u * SSTEP), "l"(src + u * RSTEP * D) : "memory");
+                for (int u = 0; u < 4; ++u) cp(sa + u * SSTEP, src + u * RSTEP * D);
                 sa += 4 * SSTEP;
                 src += 4 * RSTEP * D;
             }
-            for (; k < n; ++k, sa += SSTEP, src += RSTEP * D)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(sa), "l"(src) : "memory");
+            for (; k < n; ++k, sa += SSTEP, src += RSTEP * D) cp(sa, src);
         }
         cp_async_commit();
         cp_async_wait<0>();
@@ -1480,7 +1491,7 @@ bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl)
 {
     if (!pick_wkernel(p.D, wide)) return false;
     pl.nbuf = ((v2::WTA_TX + p.min_disp + p.D + 31) / 32) * 32;
-    pl.bstride = p.D + 2;               // RowGeom<D>::BS
+    pl.bstride = p.D + v2::WTA_PAD;     // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
     if (pl.rsmem > 200 * 1024) return false;
     for (int mode = 0; mode < 3; ++mode)
