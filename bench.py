@@ -213,6 +213,90 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------ the paper's Table II workload
+TABLE2_FPS = {64: (414.51, 342.24), 96: (326.79, 268.98), 128: (281.26, 232.49), 256: (147.13, 128.56)}
+
+
+def run_table2(args):
+    """--table2 D: the paper's own benchmark (Table II):
+    960x540 IR pair -> 4-path SGM (or SGBM with --block) with uniqueness,
+    sub-pixel, LR, median 3 and depth, registered to a 1920x1080 RGB frame
+    (reading c16).  One step = a batch of frames through asd_depth_batch +
+    asd_register_depth; e2e adds the H2D of the pair and the D2H of the
+    registered depth.  vs_baseline = value / the paper's RTX 4090 FPS for the
+    same D (another GPU: context for the like-for-like workload)."""
+    import numpy as np
+    import torch
+    import paper_2201_11924_b200 as asd
+    import synth
+    D = args.table2
+    cfg = synth.CONFIGS[f"T{D}"]
+    params = run_params(cfg, args.block, args.lr_mode, 3)
+    B, H, W = args.frames, cfg.height, cfg.width
+    dev = torch.device("cuda", 0)
+    pool_L, pool_R = synth.frame_pool(cfg, POOL)
+    idx = [f % POOL for f in range(B)]
+    Lh = torch.from_numpy(pool_L[idx]).pin_memory()
+    Rh = torch.from_numpy(pool_R[idx]).pin_memory()
+    L, R = Lh.to(dev), Rh.to(dev)
+    disp = torch.empty(B, H, W, device=dev)
+    depth = torch.empty_like(disp)
+    reg = torch.empty(B, 1080, 1920, device=dev)
+    regh = torch.empty(B, 1080, 1920).pin_memory()
+    ir = (W, H, float(cfg.focal_px), float(cfg.focal_px), (W - 1) / 2, (H - 1) / 2)
+    rgb = (1920, 1080, 2.0 * float(cfg.focal_px), 2.0 * float(cfg.focal_px), 959.5, 539.5)
+    eye, t = np.eye(3, dtype=np.float32), [-0.015, 0.0, 0.0]          # D415-like RGB offset
+    probe = asd.Stereo(asd.Params(**params), 0, 1)
+    fpw = probe.frames_per_wave
+    probe.close()
+    mb = max(1, (MAX_BATCH // fpw) * fpw) if fpw > 0 else MAX_BATCH
+    st = asd.Stereo(asd.Params(**params), 0, mb)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        st.asd_depth_batch(L, R, disp, depth, None, stream=stream)
+        asd.register_depth(ir, rgb, eye, t, depth, out=reg, stream=stream)
+
+    def step_e2e():
+        L.copy_(Lh, non_blocking=True)
+        R.copy_(Rh, non_blocking=True)
+        step()
+        regh.copy_(reg, non_blocking=True)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1)
+
+    with ClockSampler(0) as clk:
+        ms = timed(step)
+    ms_e2e = timed(step_e2e)
+    value = B * args.steps / (ms / 1e3)
+    paper = TABLE2_FPS[D][1 if args.block > 1 else 0]
+    line = {"metric": f"SimSense {'SGBM' if args.block > 1 else 'SGM'} FPS, Table II workload "
+                      f"(960x540 -> 1920x1080, 4-path, D={D})",
+            "value": round(value, 2), "unit": "frames/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": round(value / paper, 2), "dtype": "u16", "data": "synthetic",
+            "config": {"workload": f"T{D}: 960x540, D={D}, census 9x7, P1={params['p1']} P2={params['p2']}, "
+                                   f"4-path SGM{' block %dx%d' % (args.block, args.block) if args.block > 1 else ''}, "
+                                   "uniqueness 10%, LR 1 px, sub-pixel, median 3, depth, registration to 1920x1080",
+                       "frames_per_step": B, "engine": st.plan_info,
+                       "paper": {"fps": paper, "hardware": "1x RTX 4090 (P:296)", "source": "PAPER.md Table II"}},
+            "clocks": clk.summary(),
+            "e2e": {"value": round(B * args.steps / (ms_e2e / 1e3), 2), "unit": "frames/s",
+                    "h2d_bytes_per_step": int(Lh.numel() + Rh.numel()), "d2h_bytes_per_step": int(4 * regh.numel()),
+                    "api": "asd_depth_batch + asd_register_depth, torch pinned copies"}}
+    print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -229,9 +313,13 @@ def main():
                     help="SGBM block size (odd; 1 = SGM, the headline line)")
     ap.add_argument("--lr-mode", type=int, default=0, help="right view: 0 = R1 (headline), 1 = R2")
     ap.add_argument("--median", type=int, default=0, help="median ksize 0 / 3 / 5")
+    ap.add_argument("--table2", type=int, default=0, choices=[0, 64, 96, 128, 256],
+                    help="the paper's Table II workload at this max disparity (not the headline line)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.table2:
+        return run_table2(args)
 
     import numpy as np
     import torch

@@ -1330,9 +1330,13 @@ static VKernel vk(int np, bool up, bool rr)
 static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = false, bool blk = false)
 {
     if (blk) {
-        if (DC != 32 || T != 4 || DPL != 4 || np != 3) return nullptr;
-        if (up) return v2::vsweep_kernel<32, 4, 3, true, 4, false, true>;
-        return rr ? v2::vsweep_kernel<32, 4, 3, false, 4, true, true> : v2::vsweep_kernel<32, 4, 3, false, 4, false, true>;
+        if (DC != 32 || T != 4 || DPL != 4) return nullptr;
+        if (np == 3) {
+            if (up) return v2::vsweep_kernel<32, 4, 3, true, 4, false, true>;
+            return rr ? v2::vsweep_kernel<32, 4, 3, false, 4, true, true> : v2::vsweep_kernel<32, 4, 3, false, 4, false, true>;
+        }
+        if (up) return v2::vsweep_kernel<32, 4, 1, true, 4, false, true>;
+        return rr ? v2::vsweep_kernel<32, 4, 1, false, 4, true, true> : v2::vsweep_kernel<32, 4, 1, false, 4, false, true>;
     }
     if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up, rr);
     if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr);
@@ -1391,7 +1395,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     const int np = p.paths == 8 ? 3 : 1;
     if (p.bw * p.bh > 1) {
         // SGBM: u16 partials without cost bits (S <= 65534 validated by asd_create), u32 WTA keys
-        if (p.D != 128 || np != 3) return no("SGBM on engine D3 needs num_disp = 128 and 8 paths");
+        if (p.D != 128) return no("SGBM on engine D3 needs num_disp = 128");
     } else {
         if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");
         int ks = 1;
@@ -1413,7 +1417,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     pl.blk = blk;
     VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk);
     VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk);
-    if (!kd || !ku) return no(blk ? "SGBM on engine D3 needs num_disp = 128 and 8 paths" : "no sweep kernel instance");
+    if (!kd || !ku) return no(blk ? "SGBM on engine D3 needs num_disp = 128" : "no sweep kernel instance");
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double best = -1.0;

@@ -78,6 +78,12 @@ CONFIGS = {
     "C": StereoConfig("C", 1280, 720, 128, 9, 7, 8, _f(1280), tag=3),
     "D": StereoConfig("D", 1920, 1080, 256, 9, 7, 8, _f(1920), tag=4),
     "E": StereoConfig("E", 1280, 720, 128, 9, 7, 8, _f(1280), frames=4096, tag=3),
+    # the paper's Table II workload: 960x540 input, 4-path SGM,
+    # max disparity 64 / 96 / 128 / 256 (census window unstated: 9x7, as C)
+    "T64": StereoConfig("T64", 960, 540, 64, 9, 7, 4, _f(960), tag=5),
+    "T96": StereoConfig("T96", 960, 540, 96, 9, 7, 4, _f(960), tag=5),
+    "T128": StereoConfig("T128", 960, 540, 128, 9, 7, 4, _f(960), tag=5),
+    "T256": StereoConfig("T256", 960, 540, 256, 9, 7, 4, _f(960), tag=5),
 }
 
 

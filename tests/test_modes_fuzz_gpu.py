@@ -26,6 +26,8 @@ CASES = [
     (257, 21, 128, 5, 7, 7, 8, 3, 3, 1),
     (130, 20, 128, 2, 5, 5, 8, 5, 0, 1),
     (1283, 9, 128, 0, 9, 7, 8, 3, 5, 0),      # several cluster CTAs, ragged last CTA
+    (333, 19, 128, 0, 9, 7, 4, 3, 3, 0),      # 4-path SGBM (D3: vertical-only strips)
+    (200, 25, 128, 3, 7, 7, 4, 5, 0, 1),      # 4-path SGBM + R2
 ]
 
 
