@@ -1369,6 +1369,7 @@ static RKernel pick_wkernel(int D, bool wide = false, int mode = 0)
     if (D == 32) return wk_d<32>(wide, mode);
     if (D == 64) return wk_d<64>(wide, mode);
     if (D == 128) return wk_d<128>(wide, mode);
+    if (D == 96) return wk_d<96>(wide, mode);                // engine D1 only (WTA window kernel)
     return nullptr;
 }
 

@@ -28,6 +28,8 @@ CASES = [
     (1283, 9, 128, 0, 9, 7, 8, 3, 5, 0),      # several cluster CTAs, ragged last CTA
     (333, 19, 128, 0, 9, 7, 4, 3, 3, 0),      # 4-path SGBM (D3: vertical-only strips)
     (200, 25, 128, 3, 7, 7, 4, 5, 0, 1),      # 4-path SGBM + R2
+    (150, 30, 96, 0, 9, 7, 4, 1, 3, 0),       # D = 96 (D1 with the window WTA kernel)
+    (97, 20, 96, 5, 5, 5, 8, 3, 0, 0),        # D = 96 SGBM (u32 WTA keys)
 ]
 
 
