@@ -663,8 +663,9 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     // kernel (wta2), with u32 keys when S can reach 2^(16 - log2 D).
     c->wta2 = false;
     if (c->engine == ASD_ENGINE_D1 && c->dp.lr_mode == 0 &&
-        (c->dp.D == 16 || c->dp.D == 32 || c->dp.D == 64 || c->dp.D == 96 || c->dp.D == 128)) {
-        const int ks = c->dp.D <= 16 ? 4 : c->dp.D <= 32 ? 5 : c->dp.D <= 64 ? 6 : 7;
+        (c->dp.D == 16 || c->dp.D == 32 || c->dp.D == 64 || c->dp.D == 96 || c->dp.D == 128 ||
+         c->dp.D == 256)) {
+        const int ks = c->dp.D <= 16 ? 4 : c->dp.D <= 32 ? 5 : c->dp.D <= 64 ? 6 : c->dp.D <= 128 ? 7 : 8;
         const long long smax = (long long)c->dp.paths * ((long long)c->dp.bw * c->dp.bh * c->dp.nb + c->dp.p2);
         if (wta2_plan(c->dp, smax >= (1ll << (16 - ks)), c->plan)) c->wta2 = true;
     }

@@ -621,7 +621,7 @@ template <int D> struct RowGeom {
     static constexpr int BS = D + WTA_PAD;           // u16 per WTA window row (WTA_PAD = 2: an odd number of
                                                      // 4-byte words, so the 32 lanes of the
                                                      // diagonal (right-view) scan hit 32 banks
-    static constexpr int KS = D <= 16 ? 4 : D <= 32 ? 5 : D <= 64 ? 6 : 7;   // key shift = log2(D)
+    static constexpr int KS = D <= 16 ? 4 : D <= 32 ? 5 : D <= 64 ? 6 : D <= 128 ? 7 : 8;   // ceil(log2 D)
 };
 
 // Left view, one pixel per lane, from its window row r[0..D) (natural order).
@@ -1209,6 +1209,8 @@ hrow_blk_kernel(RArgs a)
 // conflicts.
 constexpr int WTA_WARPS = 8;
 constexpr int WTA_TX = 32 * WTA_WARPS;
+// D = 256 (engine D1 only): stages of 128 pixels (4 warps) so the window fits
+__host__ __device__ constexpr int wta_warps(int D) { return D > 128 ? 4 : WTA_WARPS; }
 
 
 // MODE 0: left view + re-indexed right view (R1).  MODE 1: left view only
@@ -1235,15 +1237,16 @@ wta2_kernel(RArgs a)
         a.fs.dr[o] = 0.0f;
     }
     constexpr int CH = D * 2 / WTA_CHUNK;             // copy pieces per S row
-    const int nstage = (W + WTA_TX - 1) / WTA_TX;
+    constexpr int TX = 32 * wta_warps(D);
+    const int nstage = (W + TX - 1) / TX;
     for (int t = 0; t < nstage; ++t) {
         // linear window of this stage: row x at slot x - x0, rows [x0, hi)
-        const int x0 = t * WTA_TX;
-        const int hi = min(W, x0 + WTA_TX + p.min_disp + D - 1);
+        const int x0 = t * TX;
+        const int hi = min(W, x0 + TX + p.min_disp + D - 1);
         __syncthreads();                              // previous stage done with the window
         {   // thread t copies word t % CH of rows x0 + t / CH, + RSTEP, ...
             // (32-bit shared address and global pointer stepped, 4 copies per trip)
-            constexpr int RSTEP = 32 * WTA_WARPS / CH;
+            constexpr int RSTEP = TX / CH;
             const int c = threadIdx.x % CH;
             const int slot0 = threadIdx.x / CH;
             const int n = (hi - x0 - slot0 + RSTEP - 1) / RSTEP;     // rows this thread copies
@@ -1370,6 +1373,7 @@ static RKernel pick_wkernel(int D, bool wide = false, int mode = 0)
     if (D == 64) return wk_d<64>(wide, mode);
     if (D == 128) return wk_d<128>(wide, mode);
     if (D == 96) return wk_d<96>(wide, mode);                // engine D1 only (WTA window kernel)
+    if (D == 256) return wk_d<256>(wide, mode);
     return nullptr;
 }
 
@@ -1495,7 +1499,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
 bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl)
 {
     if (!pick_wkernel(p.D, wide)) return false;
-    pl.nbuf = ((v2::WTA_TX + p.min_disp + p.D + 31) / 32) * 32;
+    pl.nbuf = ((32 * v2::wta_warps(p.D) + p.min_disp + p.D + 31) / 32) * 32;
     pl.bstride = p.D + v2::WTA_PAD;     // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
     if (pl.rsmem > 200 * 1024) return false;
@@ -1514,7 +1518,7 @@ void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16
     r.p = p; r.pab = const_cast<uint16_t*>(S); r.cell_stride = cell_stride; r.fs = fs; r.px_stride = px_stride;
     r.nbuf = pl.nbuf; r.bstride = pl.bstride;
     RKernel k = pick_wkernel(p.D, pl.wide);
-    k<<<dim3(p.H, nframes), 32 * v2::WTA_WARPS, pl.rsmem, s>>>(r);
+    k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
 }
 
 static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const VArgs& a, bool up, cudaStream_t s)
@@ -1564,7 +1568,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
     } else {
         RKernel k = pick_wkernel(p.D, pl.wide, variant);
-        k<<<dim3(p.H, nframes), 32 * v2::WTA_WARPS, pl.rsmem, s>>>(r);
+        k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -30,6 +30,8 @@ CASES = [
     (200, 25, 128, 3, 7, 7, 4, 5, 0, 1),      # 4-path SGBM + R2
     (150, 30, 96, 0, 9, 7, 4, 1, 3, 0),       # D = 96 (D1 with the window WTA kernel)
     (97, 20, 96, 5, 5, 5, 8, 3, 0, 0),        # D = 96 SGBM (u32 WTA keys)
+    (300, 21, 256, 0, 9, 7, 4, 1, 3, 0),      # D = 256, 4 paths: packed u16 keys in the window WTA
+    (140, 17, 256, 7, 7, 5, 8, 1, 0, 0),      # D = 256, 8 paths: u32 keys
 ]
 
 
