@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "frames/s and Gcell/s (W·H·D) at 1280×720×D128 8-path; HBM GB/s vs peak"
 CONFIG = "C"
+METRIC_D = "frames/s and Gcell/s (W·H·D) at 1920×1080×D256 8-path (config D); HBM GB/s vs peak"
 FRAMES_PER_STEP = 128          # inputs 128 x 2 x 0.92 MB = 236 MB per step > 126 MB L2
 POOL = 8                       # distinct synthetic frames (kernels are data-oblivious)
 CRITICAL = ("census", "down", "up")   # D3 stages on the high-priority (critical) stream
@@ -115,10 +116,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def run_params(cfg, block: int, lr_mode: int = 0, median: int = 0) -> dict:
+def run_params(cfg, block: int, lr_mode: int = 0, median: int = 0, engine: int = 0) -> dict:
     """Config parameters; block > 1 = SGBM with P1 = 8*area, P2 = 32*area (S:388);
-    lr_mode 1 = the R2 right view (reading c24); median = median ksize (c20)."""
+    lr_mode 1 = the R2 right view (reading c24); median = median ksize (c20);
+    engine 0 = auto, 1 = D1, 3 = D3."""
     d = cfg.params_dict()
+    if engine:
+        d.update(engine=engine)
     if block > 1:
         d.update(block_w=block, block_h=block, p1=8 * block * block, p2=32 * block * block)
     if lr_mode:
@@ -128,8 +132,11 @@ def run_params(cfg, block: int, lr_mode: int = 0, median: int = 0) -> dict:
     return d
 
 
-def workload(block: int, lr_mode: int = 0, median: int = 0) -> str:
+def workload(block: int, lr_mode: int = 0, median: int = 0, cfg_name: str = "C") -> str:
     extra = (", R2 right view" if lr_mode else "") + (f", median {median}" if median else "")
+    if cfg_name == "D":
+        return ("D: 1920x1080, D=256, census 9x7, P1=8 P2=32, 8-path SGM, uniqueness 10%, LR 1 px, "
+                "sub-pixel, depth (cost-volume-pressure stress)" + extra)
     if block > 1:
         a = block * block
         return (f"C-SGBM{block}x{block}: 1280x720, D=128, census 9x7, {block}x{block} block, "
@@ -202,7 +209,7 @@ def run_reference(args):
             "ms_per_step": round(1000 * tot / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 6),
-            "config": {"workload": workload(args.block, args.lr_mode, args.median),
+            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config),
                        "frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "frames/s", "cores": nworkers,
                              "kind": "oracle",
@@ -215,6 +222,44 @@ def run_reference(args):
 
 # ------------------------------------------------ the paper's Table II workload
 TABLE2_FPS = {64: (414.51, 342.24), 96: (326.79, 268.98), 128: (281.26, 232.49), 256: (147.13, 128.56)}
+
+
+def d1_gate(asd, params, L, R, dev, hbm_peak, steps: int = 2, frames: int = 32):
+    """North-star gate: the aggregation kernel of engine D1 (sgm_dir_kernel, one
+    path direction per launch, u16 S read-modify-write = 4 B/cell, HBM-bound by
+    design) against the HBM roofline, measured live on the same frames: its
+    average launch duration from the library's CUDA events on the launching
+    stream, algorithmic bytes / duration.  D1 runs the whole
+    path (census, 8 directions, WTA, LR/depth) serially; fps is that engine's."""
+    import torch
+    n = min(frames, L.shape[0])
+    d = dict(params, engine=1)
+    st = asd.Stereo(asd.Params(**d), dev.index, n)
+    Lg, Rg = L[:n].contiguous(), R[:n].contiguous()
+    disp = torch.empty(n, L.shape[1], L.shape[2], device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        st.asd_depth_batch(Lg, Rg, disp, disp, None, stream=stream)
+    torch.cuda.synchronize(dev)
+    st.profile_begin(4096)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        st.asd_depth_batch(Lg, Rg, disp, disp, None, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    prof = st.profile_end()
+    st.close()
+    ms = e0.elapsed_time(e1)
+    dp = prof["dir"]
+    avg = dp["ms"] / max(1, dp["launches"])
+    alg = dp["alg_bytes"] / max(1, dp["launches"])
+    ach = alg / (avg / 1e3) / 1e9
+    return {"kernel": "sgm_dir_kernel (engine D1, one path direction per launch)", "bound": "hbm",
+            "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
+            "target_frac": 0.6, "alg_bytes_per_launch": alg, "avg_launch_ms": round(avg, 4),
+            "launches": dp["launches"], "engine_fps": round(n * steps / (ms / 1e3), 1),
+            "note": "all 8 directions averaged; 2 B/cell for the first (write-only), 4 B/cell for the others"}
 
 
 def run_table2(args):
@@ -309,12 +354,17 @@ def main():
                     help="frames per asd_depth_batch chunk (0: a whole number of cluster waves, ~32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gate", action="store_true", help="skip the D1 aggregation-kernel HBM gate measurement")
     ap.add_argument("--block", type=int, default=1,
                     help="SGBM block size (odd; 1 = SGM, the headline line)")
     ap.add_argument("--lr-mode", type=int, default=0, help="right view: 0 = R1 (headline), 1 = R2")
     ap.add_argument("--median", type=int, default=0, help="median ksize 0 / 3 / 5")
     ap.add_argument("--table2", type=int, default=0, choices=[0, 64, 96, 128, 256],
                     help="the paper's Table II workload at this max disparity (not the headline line)")
+    ap.add_argument("--engine", type=int, default=0, choices=[0, 1, 3],
+                    help="0 = auto (D3 where its envelope allows), 1 = D1 (per-direction, HBM-bound), 3 = D3")
+    ap.add_argument("--config", default=CONFIG, choices=["C", "D"],
+                    help="C = the headline 1280x720 D=128 line; D = 1920x1080 D=256 (engine D1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -338,8 +388,8 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    cfg = synth.CONFIGS[CONFIG]
-    params = run_params(cfg, args.block, args.lr_mode, args.median)
+    cfg = synth.CONFIGS[args.config]
+    params = run_params(cfg, args.block, args.lr_mode, args.median, args.engine)
     B = args.frames
     H, W = cfg.height, cfg.width
     pool_L, pool_R = synth.frame_pool(cfg, POOL)
@@ -480,24 +530,29 @@ def main():
             pipeline = {"group_frames": st.group, "critical_stages": list(CRITICAL),
                         "critical_stream_busy": round(busy / max(1e-9, span), 4),
                         "note": "stage_ms are per-kernel event sums; row/wta/lr overlap the sweeps"}
+        gate = None
+        if not args.no_gate and args.block == 1 and args.lr_mode == 0:
+            gate = d1_gate(asd, params, L, R, dev, hbm_peak)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(params, pool_L, pool_R)
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": world,
+            "metric": METRIC if args.config == "C" else METRIC_D, "value": round(value, 3), "unit": "frames/s",
+            "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
             "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 3),
-            "config": {"workload": workload(args.block, args.lr_mode, args.median),
+            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config),
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
-                       "l2": "inputs larger than L2 (236 MB/step/GPU) + per-frame scratch > L2",
+                       "l2": f"inputs larger than L2 ({2 * B * H * W / 1e6:.0f} MB/step/GPU) + per-frame scratch > L2",
                        "engine": st.plan_info},
             "roofline": roof,
             "stage_ms": {k: round(prof[k]["ms"], 3) for k in asd.abi.STAGES if prof[k]["launches"]},
             "stage_share": stage_share,
             "pipeline": pipeline,
+            "hbm_gate": gate,
             "clocks": clk.summary(),
             "gpu_launches": lp * args.steps,
             "checksum_frames": int(len(st_all)),

@@ -20,8 +20,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "lib", "libasd.so")
+# experiment builds (tools/ab.sh): ASD_VARIANT=name builds lib/variants/name.so
+# from csrc/ (or ASD_CSRC) with the ASD_NVCC_DEFS defines, in build/name/
+_VARIANT = os.environ.get("ASD_VARIANT", "")
+CSRC = os.environ.get("ASD_CSRC", CSRC) if _VARIANT else CSRC
+BUILD = os.path.join(PKG, "build", _VARIANT) if _VARIANT else os.path.join(PKG, "build")
+LIB = (os.path.join(PKG, "lib", "variants", _VARIANT + ".so") if _VARIANT
+       else os.path.join(PKG, "lib", "libasd.so"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NO_FMA = {"post.cu", "sgm_v2.cu", "register.cu", "noise.cu", "rectify.cu"}
 
