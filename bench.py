@@ -209,7 +209,8 @@ def run_reference(args):
             "ms_per_step": round(1000 * tot / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 6),
-            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config),
+            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config)
+                                   + (f"; E: job of {args.job} frames per step sharded over {world} GPU(s)" if args.job else ""),
                        "frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "frames/s", "cores": nworkers,
                              "kind": "oracle",
@@ -255,7 +256,15 @@ def d1_gate(asd, params, L, R, dev, hbm_peak, steps: int = 2, frames: int = 32):
     avg = dp["ms"] / max(1, dp["launches"])
     alg = dp["alg_bytes"] / max(1, dp["launches"])
     ach = alg / (avg / 1e3) / 1e9
-    return {"kernel": "sgm_dir_kernel (engine D1, one path direction per launch)", "bound": "hbm",
+    traffic = None          # ncu dram bytes per launch (profiles/ncu_traffic.json "dir": per frame, all 8 directions averaged)
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            per_frame = json.load(open(tpath)).get("dir")
+            traffic = per_frame * n if per_frame is not None else None
+        except Exception:
+            traffic = None
+    return {"kernel": "sgm_dir_kernel (engine D1, one path direction per launch)", "bound": "hbm", "traffic": traffic,
             "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
             "target_frac": 0.6, "alg_bytes_per_launch": alg, "avg_launch_ms": round(avg, 4),
             "launches": dp["launches"], "engine_fps": round(n * steps / (ms / 1e3), 1),
@@ -355,6 +364,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the D1 aggregation-kernel HBM gate measurement")
+    ap.add_argument("--job", type=int, default=0,
+                    help="config E: a fixed job of this many frames per step (e.g. 4096), frame-sharded over the ranks (strong scaling)")
     ap.add_argument("--block", type=int, default=1,
                     help="SGBM block size (odd; 1 = SGM, the headline line)")
     ap.add_argument("--lr-mode", type=int, default=0, help="right view: 0 = R1 (headline), 1 = R2")
@@ -390,10 +401,19 @@ def main():
 
     cfg = synth.CONFIGS[args.config]
     params = run_params(cfg, args.block, args.lr_mode, args.median, args.engine)
-    B = args.frames
     H, W = cfg.height, cfg.width
     pool_L, pool_R = synth.frame_pool(cfg, POOL)
-    f0, f1 = shard_range(world * B, rank, world)          # this rank's frames of the job
+    if args.job:
+        # config E: one fixed job of args.job frames per step, frame-sharded across the
+        # ranks; total work fixed as N grows -> strong scaling
+        if args.job % world:
+            raise SystemExit(f"--job {args.job} must divide evenly over {world} ranks (stats all_gather)")
+        f0, f1 = shard_range(args.job, rank, world)
+        B = f1 - f0
+        args.no_e2e = True          # pinned host copies of a 4096-frame job exceed the host budget
+    else:
+        B = args.frames
+        f0, f1 = shard_range(world * B, rank, world)      # this rank's frames of the job
     idx = [f % POOL for f in range(f0, f1)]
     L = torch.from_numpy(pool_L[idx]).to(dev)
     R = torch.from_numpy(pool_R[idx]).to(dev)
@@ -436,7 +456,7 @@ def main():
     timeline = st.profile_timeline(lp * args.steps + 16)
     prof = st.profile_end()
     ms_max = max_over_ranks(ms, dev)
-    frames_total = world * B * args.steps
+    frames_total = (args.job if args.job else world * B) * args.steps
     value = frames_total / (ms_max / 1000.0)
 
     # ---- per-frame stats gather (NCCL, after timing) + parity of checksums
@@ -540,10 +560,12 @@ def main():
             "metric": METRIC if args.config == "C" else METRIC_D, "value": round(value, 3), "unit": "frames/s",
             "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+            "higher_is_better": True, "scaling": "strong" if args.job else "weak", "vs_baseline": None,
+            "dtype": "u16",
             "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 3),
-            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config),
+            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config)
+                                   + (f"; E: job of {args.job} frames per step sharded over {world} GPU(s)" if args.job else ""),
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
                        "l2": f"inputs larger than L2 ({2 * B * H * W / 1e6:.0f} MB/step/GPU) + per-frame scratch > L2",

@@ -105,7 +105,10 @@ __device__ __forceinline__ uint32_t popc_w(unsigned long long v) { return __popc
 #ifndef ASD_DIR_PFL2
 #define ASD_DIR_PFL2 8
 #endif
-template <int DPL> struct DirPF { static constexpr int v = DPL <= 4 ? ASD_DIR_PF : (ASD_DIR_PF + 1) / 2; };
+#ifndef ASD_DIR_PF8
+#define ASD_DIR_PF8 ((ASD_DIR_PF + 1) / 2)    // ring depth at DPL = 8 (D > 128)
+#endif
+template <int DPL> struct DirPF { static constexpr int v = DPL <= 4 ? ASD_DIR_PF : ASD_DIR_PF8; };
 
 __device__ __forceinline__ void prefetch_l2(const void* p)
 { asm volatile("prefetch.global.L2 [%0];\n" :: "l"(p)); }

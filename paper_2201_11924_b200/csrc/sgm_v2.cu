@@ -192,8 +192,14 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
 // slice of the right row its DC disparities read (w + DC - 1 words), placed at
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
-constexpr int NSLOT = 4;          // census rows in flight (K_down): rows i+1 .. i+3
-constexpr int KU = 3;             // K_up input rows in flight (TMA bulk ring)
+#ifndef ASD_NSLOT
+#define ASD_NSLOT 4               // 6 and 8 measured no faster (tools/runs/d3ab.sh)
+#endif
+#ifndef ASD_KU
+#define ASD_KU 3                  // 5 measured no faster
+#endif
+constexpr int NSLOT = ASD_NSLOT;  // census rows in flight (K_down): rows i+1 .. i+NSLOT-1
+constexpr int KU = ASD_KU;        // K_up input rows in flight (TMA bulk ring)
 
 template <int DC, int T>
 struct VGeom {
