@@ -285,7 +285,7 @@ def run_table2(args):
     import synth
     D = args.table2
     cfg = synth.CONFIGS[f"T{D}"]
-    params = run_params(cfg, args.block, args.lr_mode, 3)
+    params = run_params(cfg, args.block, args.lr_mode, 3, args.engine)
     B, H, W = args.frames, cfg.height, cfg.width
     dev = torch.device("cuda", 0)
     pool_L, pool_R = synth.frame_pool(cfg, POOL)

@@ -120,8 +120,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p)
 #ifndef ASD_DIR_MINB
 #define ASD_DIR_MINB 1
 #endif
+#ifndef ASD_DIR_WARPS
+#define ASD_DIR_WARPS 4              // lines (warps) per CTA
+#endif
+#ifndef ASD_DIR_SYNC
+#define ASD_DIR_SYNC 0               // vertical lines: CTA barrier every this many steps (0 = none)
+#endif
 template <int DPL, typename SigT, bool FIRST, int MODE, bool FULLW>
-__global__ void __launch_bounds__(128, ASD_DIR_MINB)
+__global__ void __launch_bounds__(32 * ASD_DIR_WARPS, ASD_DIR_MINB)
 sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
                const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base, long long sig_stride,
                uint16_t* __restrict__ S_base, long long s_stride, const uint16_t* __restrict__ cv_base,
@@ -136,6 +142,10 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
     const int chain = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (chain >= nchains) return;
+    // vertical lines all have length H: keep the CTA's adjacent columns in step so
+    // their S rows reach DRAM together (named barrier over the CTA's live warps)
+    const int live_thr = 32 * min((int)(blockDim.x >> 5), nchains - (int)(blockIdx.x * (blockDim.x >> 5)));
+    const bool dosync = ASD_DIR_SYNC > 0 && rx == 0;
     const int frame = blockIdx.y;
     // reference / matched census (swapped for the right-view reference)
     const SigT* cl = (RR ? cr_base : cl_base) + frame * sig_stride;
@@ -230,6 +240,8 @@ sgm_dir_kernel(DevParams p, int rx, int ry, int nchains, int act,
     uint32_t M2 = 0;                                   // M | M << 16
     const bool has_prev = lane > 0, has_next = lane < act - 1;
     for (int i0 = 0; i0 < len; i0 += PF) {
+        if (ASD_DIR_SYNC > 0 && dosync && i0 % ASD_DIR_SYNC == 0)
+            asm volatile("bar.sync 1, %0;" :: "r"(live_thr) : "memory");
 #pragma unroll
         for (int k = 0; k < PF; ++k) {
             const int i = i0 + k;
@@ -301,7 +313,7 @@ static void launch_dir_t(const DevParams& p, int nframes, int rx, int ry, bool f
                          uint16_t* S, long long s_stride, cudaStream_t s, const uint16_t* cv, bool right_ref)
 {
     const int n = num_chains(p, rx, ry);
-    dim3 grid((n + 3) / 4, nframes), block(128);
+    dim3 grid((n + ASD_DIR_WARPS - 1) / ASD_DIR_WARPS, nframes), block(32 * ASD_DIR_WARPS);
     const long long pstep = (long long)ry * p.W + rx, sinc = pstep * p.D;
     const unsigned long long nbm = p.nb >= 64 ? ~0ull : ((1ull << p.nb) - 1);
     const SigT* l = (const SigT*)cl;

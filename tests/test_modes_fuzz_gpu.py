@@ -32,6 +32,11 @@ CASES = [
     (97, 20, 96, 5, 5, 5, 8, 3, 0, 0),        # D = 96 SGBM (u32 WTA keys)
     (300, 21, 256, 0, 9, 7, 4, 1, 3, 0),      # D = 256, 4 paths: packed u16 keys in the window WTA
     (140, 17, 256, 7, 7, 5, 8, 1, 0, 0),      # D = 256, 8 paths: u32 keys
+    # engine D1 lane layouts (DPL = D / act): partial warps and lines without an all-valid interval
+    (120, 19, 80, 9, 7, 7, 8, 1, 0, 1),       # D = 80: 4 per lane, 20 active lanes, R2
+    (260, 15, 144, 20, 9, 7, 8, 1, 0, 0),     # D = 144: 8 per lane, 18 active lanes, min_disp 20
+    (60, 12, 240, 0, 5, 5, 4, 1, 0, 1),       # D = 240 > W: every matched window range is partial
+    (75, 14, 112, 33, 7, 5, 8, 3, 0, 0),      # D = 112 SGBM (cost from CB), min_disp 33
 ]
 
 
