@@ -225,7 +225,7 @@ def run_reference(args):
 TABLE2_FPS = {64: (414.51, 342.24), 96: (326.79, 268.98), 128: (281.26, 232.49), 256: (147.13, 128.56)}
 
 
-def d1_gate(asd, params, L, R, dev, hbm_peak, steps: int = 2, frames: int = 32):
+def d1_gate(asd, params, L, R, dev, hbm_peak, steps: int = 2, frames: int = 32, traffic_ok: bool = True):
     """North-star gate: the aggregation kernel of engine D1 (sgm_dir_kernel, one
     path direction per launch, u16 S read-modify-write = 4 B/cell, HBM-bound by
     design) against the HBM roofline, measured live on the same frames: its
@@ -258,7 +258,7 @@ def d1_gate(asd, params, L, R, dev, hbm_peak, steps: int = 2, frames: int = 32):
     ach = alg / (avg / 1e3) / 1e9
     traffic = None          # ncu dram bytes per launch (profiles/ncu_traffic.json "dir": per frame, all 8 directions averaged)
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if traffic_ok and os.path.exists(tpath):
         try:
             per_frame = json.load(open(tpath)).get("dir")
             traffic = per_frame * n if per_frame is not None else None
@@ -510,8 +510,8 @@ def main():
                        if prof[k]["launches"]}
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath):
-            try:
+        if os.path.exists(tpath) and args.config == "C" and args.block == 1 and args.lr_mode == 0:
+            try:                      # the ncu capture in the file is of the config-C headline line
                 per_frame = json.load(open(tpath)).get(top)
                 if per_frame is not None:
                     traffic = per_frame * (st.group if st.engine == 3 else min(args.max_batch, B))
@@ -552,7 +552,7 @@ def main():
                         "note": "stage_ms are per-kernel event sums; row/wta/lr overlap the sweeps"}
         gate = None
         if not args.no_gate and args.block == 1 and args.lr_mode == 0:
-            gate = d1_gate(asd, params, L, R, dev, hbm_peak)
+            gate = d1_gate(asd, params, L, R, dev, hbm_peak, traffic_ok=args.config == "C")
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(params, pool_L, pool_R)
