@@ -839,21 +839,23 @@ __device__ __forceinline__ void row_cost(const DevParams& p, int lane, uint32_t 
 // lane: the u32 minimum over lanes of (m << 16 | m) is the packed minimum, so
 // no unpack/repack is needed, and P1 / P2 come packed from the kernel
 // arguments (constant-bank operands).
+// eprev / enext: INF2 in the lanes without a d-1 / d+1 neighbour lane (lane 0 /
+// lane ACT-1), 0 elsewhere -- ORed into the shuffled words (every Q half is
+// < 2^15, so Q | 0x7FFF = INF), which keeps the edge test out of the loop.
 template <int D>
-__device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int lane,
+__device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, uint32_t eprev, uint32_t enext,
                                             const uint32_t (&C)[RowGeom<D>::NRR],
                                             const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t Mpk,
                                             uint32_t (&Ln)[RowGeom<D>::NRR])
 {
     constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
+    const int lane = threadIdx.x & 31;
     const uint32_t MP2 = Mpk + p2x2;
     uint32_t mm;
     if constexpr (DPL == 4) {
         const uint32_t QA = Lp[0] + p1x2, QB = Lp[NRR - 1] + p1x2;
-        uint32_t prevB = __shfl_up_sync(FULL, QB, 1);
-        uint32_t nextA = __shfl_down_sync(FULL, QA, 1);
-        if (lane == 0) prevB = INF2;
-        if (lane == ACT - 1) nextA = INF2;
+        const uint32_t prevB = __shfl_up_sync(FULL, QB, 1) | eprev;
+        const uint32_t nextA = __shfl_down_sync(FULL, QA, 1) | enext;
         const uint32_t dm1A = __byte_perm(prevB, QB, 0x5432);
         const uint32_t dp1B = __byte_perm(QA, nextA, 0x5432);
         uint32_t tA = vmin2(vmin2(dm1A, QB), Lp[0]);
@@ -865,10 +867,8 @@ __device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int la
         mm = vmin2(Ln[0], Ln[NRR - 1]);
     } else {
         const uint32_t Q = Lp[0] + p1x2;
-        uint32_t prev = __shfl_up_sync(FULL, Q, 1);
-        uint32_t next = __shfl_down_sync(FULL, Q, 1);
-        if (lane == 0) prev = INF2;
-        if (lane == ACT - 1) next = INF2;
+        const uint32_t prev = __shfl_up_sync(FULL, Q, 1) | eprev;
+        const uint32_t next = __shfl_down_sync(FULL, Q, 1) | enext;
         const uint32_t dm1 = __byte_perm(prev, Q, 0x5432);
         const uint32_t dp1 = __byte_perm(Q, next, 0x5432);
         uint32_t t = vmin2(vmin2(dm1, dp1), Lp[0]);
@@ -881,6 +881,15 @@ __device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int la
     return __reduce_min_sync(FULL, m2);
 }
 
+template <int D>
+__device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int lane,
+                                            const uint32_t (&C)[RowGeom<D>::NRR],
+                                            const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t Mpk,
+                                            uint32_t (&Ln)[RowGeom<D>::NRR])
+{
+    return row_rec<D>(p1x2, p2x2, lane == 0 ? INF2 : 0u, lane == RowGeom<D>::ACT - 1 ? INF2 : 0u, C, Lp, Mpk, Ln);
+}
+
 // ---------------------------------------------------------------- K_row
 // Horizontal paths, one warp per row, no shared memory (occupancy bound only by
 // registers).  Left->right: L stashed as u8.  Right->left: S = P_AB + L_lr +
@@ -890,7 +899,13 @@ constexpr int HROW_WARPS = 4;
 // CFROMP (R2's right-referenced pass, reading c24): the left->right path takes
 // its cost from the P_AB | C << 9 words instead of the census images.
 template <int D, bool CFROMP = false>
-__global__ void __launch_bounds__(32 * HROW_WARPS)
+#ifndef ASD_HROW_MINB
+#define ASD_HROW_MINB 1               // 6 (<= 80 registers, spills) measured slower
+#endif
+#ifndef ASD_HROW_SMEM
+#define ASD_HROW_SMEM 0               // dynamic shared memory per row CTA: caps its occupancy
+#endif
+__global__ void __launch_bounds__(32 * HROW_WARPS, ASD_HROW_MINB)
 hrow_kernel(RArgs a)
 {
     using G = RowGeom<D>;
@@ -903,6 +918,7 @@ hrow_kernel(RArgs a)
     if (y >= H) return;
     const int lane = threadIdx.x & 31;
     const bool active = ACT == 32 || lane < ACT;
+    const uint32_t eprev = lane == 0 ? INF2 : 0u, enext = lane == ACT - 1 ? INF2 : 0u;   // row_rec edge masks
     const int d0 = lane * DPL;
     const int lim0 = -p.min_disp - p.R;
     const int ngrp = (W + 31) >> 5;
@@ -952,7 +968,7 @@ hrow_kernel(RArgs a)
                     uint32_t Cc[NRR], Ln[NRR];
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) Cc[r] = (PP[k][r] >> 9) & 0x003F003Fu;
-                    M = row_rec<D>(a.p1x2, a.p2x2, lane, Cc, L, M, Ln);
+                    M = row_rec<D>(a.p1x2, a.p2x2, eprev, enext, Cc, L, M, Ln);
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                     if (active) {
@@ -1000,7 +1016,7 @@ hrow_kernel(RArgs a)
                             const bool vx = F || (vrow && x >= p.R && x < W - p.R);
                             uint32_t Cc[NRR], Ln[NRR];
                             row_cost<D, F>(p, lane, clv, vx, x + lim0, wnd, Cc);
-                            M = row_rec<D>(a.p1x2, a.p2x2, lane, Cc, L, M, Ln);
+                            M = row_rec<D>(a.p1x2, a.p2x2, eprev, enext, Cc, L, M, Ln);
 #pragma unroll
                             for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                             if (active) {
@@ -1053,8 +1069,13 @@ hrow_kernel(RArgs a)
         };
         const int xtop = ((W - 1) / SG) * SG;              // sub-groups aligned to SG
         // one sub-group of SG pixels from the buffers PP / SS (x = xs + SG-1 .. xs)
-        auto group = [&](int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG]) {
-            const bool whole = xs + SG <= W;
+        // S vector of pixel x: pab + x * D in one IMAD.WIDE.U32 (x >= 0)
+        auto svec = [&](int x) {
+            return reinterpret_cast<uint16_t*>(reinterpret_cast<uintptr_t>(pab) + (unsigned long long)(unsigned)x * (2u * D));
+        };
+        // whole: all SG pixels inside the row (called with a literal, so each
+        // call site inlines its own copy without the per-pixel bound test)
+        auto group = [&](const bool whole, int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG]) {
 #pragma unroll
             for (int k = SG - 1; k >= 0; --k) {
                 const int x = xs + k;
@@ -1065,17 +1086,17 @@ hrow_kernel(RArgs a)
                         Pv[r] = PP[k][r] & 0x01FF01FFu;
                         Cc[r] = (PP[k][r] >> 9) & 0x003F003Fu;
                     }
-                    M = row_rec<D>(a.p1x2, a.p2x2, lane, Cc, L, M, Ln);
+                    M = row_rec<D>(a.p1x2, a.p2x2, eprev, enext, Cc, L, M, Ln);
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                     if (active) {
                         if constexpr (DPL == 4) {
                             const uint32_t s0 = Pv[0] + __byte_perm(SS[k], 0u, 0x4140) + Ln[0];
                             const uint32_t s1 = Pv[NRR - 1] + __byte_perm(SS[k], 0u, 0x4342) + Ln[NRR - 1];
-                            *reinterpret_cast<uint2*>(pab + (long long)x * D) =
+                            *reinterpret_cast<uint2*>(svec(x)) =
                                 make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
                         } else {
-                            *reinterpret_cast<uint32_t*>(pab + (long long)x * D) =
+                            *reinterpret_cast<uint32_t*>(svec(x)) =
                                 Pv[0] + __byte_perm(SS[k], 0u, 0x4140) + Ln[0];
                         }
                     }
@@ -1083,13 +1104,17 @@ hrow_kernel(RArgs a)
             }
         };
         // ping-pong between the two buffer sets (no register copies)
+        auto run_group = [&](int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG]) {
+            if (xs + SG <= W) group(true, xs, PP, SS);
+            else group(false, xs, PP, SS);
+        };
         load_sg(xtop, P, Sx);
         for (int xs = xtop; xs >= 0; xs -= 2 * SG) {
             load_sg(xs - SG, Pn, Sn);
-            group(xs, P, Sx);
+            run_group(xs, P, Sx);
             if (xs - SG < 0) break;
             load_sg(xs - 2 * SG, P, Sx);
-            group(xs - SG, Pn, Sn);
+            run_group(xs - SG, Pn, Sn);
         }
     }
 }
@@ -1571,7 +1596,9 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.cb = cbin; r.cb_stride = (long long)p.H * pl.cs * pl.w * p.D; r.wpad = pl.cs * pl.w;
     if (stage == 2) {
         RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1);
-        k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, 0, s>>>(r);
+        const int hsm = pl.blk ? 0 : ASD_HROW_SMEM;
+        if (hsm > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+        k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, hsm, s>>>(r);
     } else {
         RKernel k = pick_wkernel(p.D, pl.wide, variant);
         k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
