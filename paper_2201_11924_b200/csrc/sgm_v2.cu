@@ -1238,10 +1238,13 @@ hrow_blk_kernel(RArgs a)
 // views run fully unrolled with immediate offsets.  Window rows are D + 2 u16:
 // an odd word stride keeps the diagonal right-view reads free of bank
 // conflicts.
-constexpr int WTA_WARPS = 8;
+#ifndef ASD_WTA_WARPS
+#define ASD_WTA_WARPS 8
+#endif
+constexpr int WTA_WARPS = ASD_WTA_WARPS;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 // D = 256 (engine D1 only): stages of 128 pixels (4 warps) so the window fits
-__host__ __device__ constexpr int wta_warps(int D) { return D > 128 ? 4 : WTA_WARPS; }
+__host__ __device__ constexpr int wta_warps(int D) { return D > 128 ? (WTA_WARPS < 4 ? WTA_WARPS : 4) : WTA_WARPS; }
 
 
 // MODE 0: left view + re-indexed right view (R1).  MODE 1: left view only
