@@ -88,12 +88,25 @@ census4_kernel(DevParams p, const uint8_t* __restrict__ left, const uint8_t* __r
     uint32_t* out = (view ? out_r : out_l) + frame * sig_stride;
     const int x0 = blockIdx.x * C4_PX, y0 = blockIdx.y * C4_TY;
     const int tid = threadIdx.y * C4_TX + threadIdx.x;
-    // base copy: byte c of row r = I(x0 + c - R, y0 + r - Q), 0 outside the image
+    // base copy: byte c of row r = I(x0 + c - R, y0 + r - Q), 0 outside the image.
+    // R % 4 == 0 (9-wide windows) and W % 4 == 0: word w of a row is the aligned
+    // image word at x0 - R + 4w, loaded whole when it lies inside the image.
     uint8_t* base = reinterpret_cast<uint8_t*>(&tile[0][0][0]);
-    for (int i = tid; i < TH * TWW * 4; i += C4_TX * C4_TY) {
-        const int r = i / (TWW * 4), c = i - r * (TWW * 4);
-        const int gx = x0 + c - R, gy = y0 + r - Q;
-        base[i] = (c < TWB && gx >= 0 && gx < p.W && gy >= 0 && gy < p.H) ? img[(long long)gy * p.W + gx] : 0;
+    if (R % 4 == 0 && (p.W & 3) == 0) {
+        for (int i = tid; i < TH * TWW; i += C4_TX * C4_TY) {
+            const int r = i / TWW, w = i - r * TWW;
+            const int gx = x0 - R + 4 * w, gy = y0 + r - Q;
+            uint32_t v = 0u;
+            if (4 * w < TWB && gy >= 0 && gy < p.H && gx >= 0 && gx + 3 < p.W)
+                v = __ldg(reinterpret_cast<const unsigned*>(img + (long long)gy * p.W + gx));
+            tile[0][r][w] = v;                          // gx + 3 >= W: whole word past the row end
+        }
+    } else {
+        for (int i = tid; i < TH * TWW * 4; i += C4_TX * C4_TY) {
+            const int r = i / (TWW * 4), c = i - r * (TWW * 4);
+            const int gx = x0 + c - R, gy = y0 + r - Q;
+            base[i] = (c < TWB && gx >= 0 && gx < p.W && gy >= 0 && gy < p.H) ? img[(long long)gy * p.W + gx] : 0;
+        }
     }
     __syncthreads();
     // shifted copies s = 1..3: word w = bytes 4w + s .. 4w + s + 3 of the base row
