@@ -217,6 +217,11 @@ struct VGeom {
 // by TMA in this kernel's private layout (K_down: CB ring instead of census
 // staging; K_up: a CB ring beside the P_A ring), and the handoffs carry the
 // wider partials without the cost bits: K_down writes P_A (u16), K_up P_AB.
+#ifndef ASD_VLATE
+#define ASD_VLATE 0
+#endif
+constexpr bool VLATE = ASD_VLATE;
+
 template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
 __global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
@@ -485,19 +490,24 @@ vsweep_kernel(VArgs a)
                 if (chunk == 0) wRm[ws * nw] = Mr;
             }
         }
-        // ---- vertical path: predecessor = own column (after the halo stores)
-        if (!ABL(a, 32)) {
-            uint32_t Ln[NR], mnew;
-            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
+        // ---- vertical path: predecessor = own column.  It reads no halo, so it
+        // runs either after the halo stores (in flight meanwhile) or, with
+        // VLATE, after the row's arrive, covering the cluster barrier.
+        auto vertical = [&]() {
+            if (!ABL(a, 32)) {
+                uint32_t Ln[NR], mnew;
+                path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
 #pragma unroll
-            for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
-            Mv = mnew;
-        }
-        if (!xin) {
+                for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
+                Mv = mnew;
+            }
+            if (!xin) {
 #pragma unroll
-            for (int k = 0; k < NR; ++k) Lv[k] = 0u;
-            Mv = 0u;
-        }
+                for (int k = 0; k < NR; ++k) Lv[k] = 0u;
+                Mv = 0u;
+            }
+        };
+        if (!(VLATE && NP == 3)) vertical();
         // ---- K_down: stage row i+5 (async), make row i+1's copies complete, publish
         if (!RING) {
             if (i + NSLOT - 1 < H) stage(row_of(i + NSLOT - 1), (i + NSLOT - 1) % NSLOT);
@@ -506,6 +516,7 @@ vsweep_kernel(VArgs a)
         }
         arrive();
         issue_row(i + KR);                            // ring input: row i's slot is free now
+        if (VLATE && NP == 3) vertical();
         // ---- partial sum out (after the release so it does not wait on these stores)
         if (!ABL(a, 2)) {
             uint32_t s[NR];
@@ -1242,6 +1253,10 @@ hrow_blk_kernel(RArgs a)
 #define ASD_WTA_WARPS 8
 #endif
 constexpr int WTA_WARPS = ASD_WTA_WARPS;
+#ifndef ASD_WTA_SPLIT
+#define ASD_WTA_SPLIT 1
+#endif
+constexpr bool WTA_SPLIT = ASD_WTA_SPLIT;
 constexpr int WTA_TX = 32 * WTA_WARPS;
 // D = 256 (engine D1 only): stages of 128 pixels (4 warps) so the window fits
 __host__ __device__ constexpr int wta_warps(int D) { return D > 128 ? (WTA_WARPS < 4 ? WTA_WARPS : 4) : WTA_WARPS; }
@@ -1294,17 +1309,27 @@ wta2_kernel(RArgs a)
                 else
                     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" :: "r"(dst), "l"(g), "n"(WTA_CHUNK) : "memory");
             };
+            // WTA_SPLIT: two commit groups, the stage's own rows [x0, x0 + TX)
+            // (all the left view reads) first, so the fill of the rows past the
+            // stage (right view only; not loaded at all when MODE != 0) overlaps
+            // the left view
+            const int na = WTA_SPLIT ? max(0, (min(TX, hi - x0) - slot0 + RSTEP - 1) / RSTEP) : n;
             int k = 0;
-            for (; k + 4 <= n; k += 4) {
+            for (; k + 4 <= na; k += 4) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) cp(sa + u * SSTEP, src + u * RSTEP * D);
                 sa += 4 * SSTEP;
                 src += 4 * RSTEP * D;
             }
-            for (; k < n; ++k, sa += SSTEP, src += RSTEP * D) cp(sa, src);
+            for (; k < na; ++k, sa += SSTEP, src += RSTEP * D) cp(sa, src);
+            if (WTA_SPLIT) {
+                cp_async_commit();
+                for (; MODE == 0 && k < n; ++k, sa += SSTEP, src += RSTEP * D) cp(sa, src);
+            }
         }
         cp_async_commit();
-        cp_async_wait<0>();
+        if (WTA_SPLIT) cp_async_wait<1>();
+        else cp_async_wait<0>();
         __syncthreads();
         // left view
         {
@@ -1322,6 +1347,7 @@ wta2_kernel(RArgs a)
             }
         }
         if constexpr (MODE != 0) continue;           // R2 passes: one view per launch
+        if (WTA_SPLIT) cp_async_wait<0>();
         __syncthreads();                              // left poisoning done before diagonal reads
         // right view
         {
