@@ -35,7 +35,7 @@ CONFIG = "C"
 METRIC_D = "frames/s and Gcell/s (W·H·D) at 1920×1080×D256 8-path (config D); HBM GB/s vs peak"
 FRAMES_PER_STEP = 128          # inputs 128 x 2 x 0.92 MB = 236 MB per step > 126 MB L2
 POOL = 8                       # distinct synthetic frames (kernels are data-oblivious)
-CRITICAL = ("census", "down", "up")   # D3 stages on the high-priority (critical) stream
+CRITICAL = ("census", "block", "down", "up")   # D3 stages on the high-priority streams (s_cen, s_hi)
 MAX_BATCH = 32                 # frames in flight per asd_depth_batch chunk
 
 
@@ -176,14 +176,64 @@ def oracle_frames_parallel(params, Ls, Rs, nworkers):
     return time.perf_counter() - t0, out
 
 
-def cpu_baseline(params, Ls, Rs):
+def _oracle_sig(o) -> tuple:
+    """(checksum, valid count) of one oracle frame -- the per-frame statistics
+    the library's asd_frame_stats carries (SURVEY §8(e) checksum)."""
+    import oracle
+    return (oracle.checksum(o["dstar_l"], o["mask"]), int((o["mask"] == 0).sum()))
+
+
+def cpu_baseline(params, Ls, Rs, cfg_name="C"):
+    """The oracle timed on the host cores (one full frame per thread); also
+    returns the (checksum, valid) of every pool frame it computed, which the
+    parity check of the GPU frames reuses."""
     nworkers, cores = oracle_workers()
-    wall, _ = oracle_frames_parallel(params, Ls, Rs, nworkers)
+    wall, outs = oracle_frames_parallel(params, Ls, Rs, nworkers)
+    sigs = {i % len(Ls): _oracle_sig(o) for i, o in enumerate(outs)}
     return {"value": round(nworkers / wall, 4), "unit": "frames/s", "cores": nworkers,
             "kind": "oracle",
-            "sample": f"{nworkers} full config-C frames (1280x720 D128 8-path"
-                      f"{', SGBM block' if params.get('block_w', 1) > 1 else ''}), one per host thread "
-                      f"on {nworkers} of {cores} cores, plain-C oracle (gcc -O2), wall {wall:.1f} s"}
+            "sample": f"{nworkers} full config-{cfg_name} frames"
+                      f"{' (SGBM block)' if params.get('block_w', 1) > 1 else ''}, one per host thread "
+                      f"on {nworkers} of {cores} cores, plain-C oracle (gcc -O2), wall {wall:.1f} s"}, sigs
+
+
+def oracle_pool_sigs(params, Ls, Rs, have: dict | None = None) -> dict:
+    """(checksum, valid) of every frame of the pool, by the oracle (frames not in
+    `have` are computed, one per host thread, memory-bounded)."""
+    import oracle
+    sigs = dict(have or {})
+    todo = [i for i in range(len(Ls)) if i not in sigs]
+    if not todo:
+        return sigs
+    nworkers, _ = oracle_workers()
+    p = oracle.Params(**params)
+    oracle.lib()
+    for k in range(0, len(todo), nworkers):
+        part = todo[k:k + nworkers]
+        res = {}
+
+        def run(i):
+            res[i] = _oracle_sig(oracle.compute(p, Ls[i], Rs[i]))
+
+        ths = [threading.Thread(target=run, args=(i,)) for i in part]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        sigs.update(res)
+    return sigs
+
+
+def parity_check(stats, frame_ids, sigs) -> dict:
+    """Every GPU frame's (checksum, valid) against the oracle's for the same
+    input (frame f is pool[f % POOL]).  stats: int array [n, 4]."""
+    bad = []
+    for row, f in zip(stats, frame_ids):
+        cs, valid = sigs[f % POOL]
+        if (int(row[0]) & 0xFFFFFFFF) != cs or int(row[1]) != valid:
+            bad.append(int(f))
+    return {"frames": len(frame_ids), "mismatches": len(bad), "first_bad": bad[:8],
+            "oracle_frames": len(sigs), "check": "per-frame (checksum of d* and mask, valid count) == oracle"}
 
 
 def run_reference(args):
@@ -210,7 +260,7 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 6),
             "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config)
-                                   + (f"; E: job of {args.job} frames per step sharded over {world} GPU(s)" if args.job else ""),
+                                   + (f"; E: job of {args.job} frames per step (CPU oracle: a bounded sample)" if args.job else ""),
                        "frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "frames/s", "cores": nworkers,
                              "kind": "oracle",
@@ -352,6 +402,52 @@ def run_table2(args):
 
 
 # ----------------------------------------------------------------- GPU arm
+# Integer lane-ops per cell of each D3 kernel: SURVEY §8(d)'s model (o = 5.5
+# packed u16x2 lane-ops per cell-path of the recursion, + 2 per cell where the
+# Hamming cost is evaluated; the library reports these as alg_ops) and the
+# minimal packed model of DESIGN.md §5 (2.5 per cell-path, 3 per cell of cost).
+def op_models(stage: str, paths: int, blk: bool):
+    np_ = 3 if paths == 8 else 1
+    c8, cmin = (0.0, 0.0) if blk else (2.0, 3.0)
+    return {"down": (np_ * 5.5 + c8, np_ * 2.5 + cmin), "up": (np_ * 5.5, np_ * 2.5 + 2.0),
+            "row": (2 * 5.5 + c8, 2 * 2.5 + cmin + 2.0)}.get(stage)
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks
+    (one per GPU, NCCL) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}), flush=True)
+        return 2
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def gather_and_check(stats, ms: float, sigs_fn, device=None):
+    """After the timed region: max of the timer over ranks (all_reduce MAX) and
+    all_gather of the per-frame stats (NCCL on GPUs, gloo in the CPU test); on
+    rank 0 every gathered frame's (checksum, valid) is compared with the
+    oracle's (sigs_fn() -> {pool index: (checksum, valid)}).  Shards are
+    contiguous and equal, so the gathered row i is global frame i.  Returns
+    (ms_max, all_stats [frames, 4] int numpy, parity dict or None off rank 0)."""
+    import torch.distributed as dist
+    from paper_2201_11924_b200.dist import gather_frame_stats, max_over_ranks
+    ms_max = max_over_ranks(ms, device)
+    allst = gather_frame_stats(stats).cpu().numpy()
+    rank = dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
+    if rank != 0:
+        return ms_max, allst, None
+    return ms_max, allst, parity_check(allst, list(range(len(allst))), sigs_fn())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -364,6 +460,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the D1 aggregation-kernel HBM gate measurement")
+    ap.add_argument("--no-parity", action="store_true", help="skip the per-frame oracle check (profiling runs)")
     ap.add_argument("--job", type=int, default=0,
                     help="config E: a fixed job of this many frames per step (e.g. 4096), frame-sharded over the ranks (strong scaling)")
     ap.add_argument("--block", type=int, default=1,
@@ -375,12 +472,15 @@ def main():
     ap.add_argument("--engine", type=int, default=0, choices=[0, 1, 3],
                     help="0 = auto (D3 where its envelope allows), 1 = D1 (per-direction, HBM-bound), 3 = D3")
     ap.add_argument("--config", default=CONFIG, choices=["C", "D"],
-                    help="C = the headline 1280x720 D=128 line; D = 1920x1080 D=256 (engine D1)")
+                    help="C = the headline 1280x720 D=128 line; D = 1920x1080 D=256")
+    ap.add_argument("--p2", type=int, default=0, help="override P2 (e.g. 40: outside the 16-bit-key envelope)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     if args.table2:
         return run_table2(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
 
     import numpy as np
     import torch
@@ -388,7 +488,7 @@ def main():
 
     import paper_2201_11924_b200 as asd
     import synth
-    from paper_2201_11924_b200.dist import gather_frame_stats, max_over_ranks, shard_range
+    from paper_2201_11924_b200.dist import shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -401,6 +501,8 @@ def main():
 
     cfg = synth.CONFIGS[args.config]
     params = run_params(cfg, args.block, args.lr_mode, args.median, args.engine)
+    if args.p2:
+        params["p2"] = args.p2
     H, W = cfg.height, cfg.width
     pool_L, pool_R = synth.frame_pool(cfg, POOL)
     if args.job:
@@ -439,10 +541,11 @@ def main():
         step()
     torch.cuda.synchronize(dev)
 
-    # ---- timed region: K steps, CUDA events, per-stage events inside libasd
+    # ---- timed region: K steps, CUDA events on the launching stream, no
+    # instrumentation inside (the per-stage profile is a separate pass below)
     lp = st.launches_per_batch(B)
-    st.profile_begin(max_launches=lp * args.steps + 16)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats.zero_()
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize(dev)
@@ -453,17 +556,21 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
     ms = e0.elapsed_time(e1)
-    timeline = st.profile_timeline(lp * args.steps + 16)
-    prof = st.profile_end()
-    ms_max = max_over_ranks(ms, dev)
-    frames_total = (args.job if args.job else world * B) * args.steps
-    value = frames_total / (ms_max / 1000.0)
+    stats_timed = stats.clone()                 # the last timed step's per-frame stats
 
-    # ---- per-frame stats gather (NCCL, after timing) + parity of checksums
-    st_all = gather_frame_stats(stats).cpu().numpy()
+    # ---- profiled pass (library CUDA events around every launch): stage_ms,
+    # the dominant kernel's average launch time, the pipeline timeline
+    psteps = max(1, min(args.steps, 3))
+    st.profile_begin(max_launches=lp * psteps + 16)
+    for _ in range(psteps):
+        step()
+    torch.cuda.synchronize(dev)
+    timeline = st.profile_timeline(lp * psteps + 16)
+    prof = st.profile_end()
+    frames_total = (args.job if args.job else world * B) * args.steps
 
     # ---- end-to-end through the host entry point (pinned host buffers)
-    e2e = None
+    e2e, sh = None, None
     if not args.no_e2e:
         Lh = torch.from_numpy(pool_L[idx]).pin_memory()
         Rh = torch.from_numpy(pool_R[idx]).pin_memory()
@@ -474,6 +581,7 @@ def main():
             st.asd_depth_batch_host(Lh, Rh, dh, zh, sh, stream=stream)
         barrier()
         torch.cuda.synchronize(dev)
+        sh.zero_()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0.record(stream)
         for _ in range(args.steps):
@@ -481,24 +589,48 @@ def main():
         h1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
+        from paper_2201_11924_b200.dist import max_over_ranks
         t2 = max_over_ranks(h0.elapsed_time(h1), dev)
         e2e = {"value": round(frames_total / (t2 / 1000.0), 3), "unit": "frames/s",
                "h2d_bytes_per_step": int(Lh.numel() + Rh.numel()),
                "d2h_bytes_per_step": int(4 * (dh.numel() + zh.numel()) + 16 * B),
                "api": "asd_depth_batch_host"}
 
+    # ---- stats gather (NCCL, after timing) + per-frame parity vs the oracle
+    cpu = None
+    sigs_cache = {}
+
+    def sigs_fn():
+        nonlocal cpu
+        if not sigs_cache:
+            have = {}
+            if world == 1 and not args.no_cpu_baseline:
+                cpu, have = cpu_baseline(params, pool_L, pool_R, args.config)
+            sigs_cache.update(oracle_pool_sigs(params, pool_L, pool_R, have))
+        return sigs_cache
+
+    no_sigs = (lambda: {i: (0, 0) for i in range(POOL)})
+    ms_max, st_all, parity = gather_and_check(stats_timed, ms, no_sigs if args.no_parity else sigs_fn, dev)
+    parity_e2e = None
+    if sh is not None:
+        sh_dev = sh.to(dev)
+        _, _, parity_e2e = gather_and_check(sh_dev, 0.0, no_sigs if args.no_parity else sigs_fn, dev)
+    value = frames_total / (ms_max / 1000.0)
+
     if rank == 0:
+        if world == 1 and not args.no_cpu_baseline and cpu is None:
+            cpu, _ = cpu_baseline(params, pool_L, pool_R, args.config)
         pk = peaks()
         hbm_peak = pk["hbm_gbs"] if pk else 6650.0
         sm_mhz = pk.get("sm_max_mhz", 1965.0) if pk else 1965.0
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         alu_peak = nsm * 128 * sm_mhz * 1e6 / 1e12       # T int lane-ops/s
-        # Dominant kernel: D3 runs the cluster sweeps (and the census feeding
-        # them) back to back on a high-priority stream -- the step's critical
-        # path -- while row/WTA/LR fill the SMs the clusters leave free, so their
-        # event durations include waiting for SMs; D1 runs serially.
+        # Dominant kernel: D3 runs the census/block cost and the cluster sweeps
+        # on high-priority streams -- the step's critical path -- while
+        # row/WTA/LR fill the SMs the clusters leave free, so their event
+        # durations include waiting for SMs; D1 runs serially.
         crit = CRITICAL if st.engine == 3 else asd.abi.STAGES
-        top = max(crit, key=lambda k: prof[k]["ms"])
+        top = max((k for k in crit if prof[k]["launches"]), key=lambda k: prof[k]["ms"])
         tp = prof[top]
         nl = max(1, tp["launches"])
         avg_ms = tp["ms"] / nl
@@ -508,13 +640,21 @@ def main():
         tot_ms = sum(prof[k]["ms"] for k in asd.abi.STAGES)
         stage_share = {k: round(prof[k]["ms"] / max(1e-9, tot_ms), 4) for k in asd.abi.STAGES
                        if prof[k]["launches"]}
-        traffic = None
+        frames_per_launch = st.group if st.engine == 3 else min(args.max_batch, B)
+        traffic, step_dram = None, None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath) and args.config == "C" and args.block == 1 and args.lr_mode == 0:
+        headline = args.config == "C" and args.block == 1 and args.lr_mode == 0 and not args.p2
+        if os.path.exists(tpath) and headline:
             try:                      # the ncu capture in the file is of the config-C headline line
-                per_frame = json.load(open(tpath)).get(top)
-                if per_frame is not None:
-                    traffic = per_frame * (st.group if st.engine == 3 else min(args.max_batch, B))
+                tj = json.load(open(tpath))
+                if tj.get(top) is not None:
+                    traffic = tj[top] * frames_per_launch
+                ks = [k for k in ("census", "down", "up", "row", "wta", "lr") if tj.get(k) is not None]
+                step_dram = {"bytes_per_frame": round(sum(tj[k] for k in ks)), "kernels": ks,
+                             "survey_8d_algorithmic_bytes_per_frame": [0.26e9, 0.50e9],
+                             "ratio_to_8d": [round(sum(tj[k] for k in ks) / 0.50e9, 2),
+                                             round(sum(tj[k] for k in ks) / 0.26e9, 2)],
+                             "source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch / frames)"}
             except Exception:
                 traffic = None
         if alg_o > 0:
@@ -522,17 +662,24 @@ def main():
             roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2),
                     "unit": "Tops/s", "frac": round(ach / alu_peak, 4), "traffic": traffic,
                     "alg_ops_per_launch": alg_o,
+                    "op_model": "SURVEY §8(d): 5.5 packed lane-ops per cell-path + 2 per cell of Hamming cost",
                     "peak_source": f"{nsm} SMs x 128 int lane-ops/clk x {sm_mhz:.0f} MHz "
-                                   "(tools/ubench.cu measured 123.5/clk/SM)",
+                                   "(profiles/r02_ubench.txt: VIMNMX.U16x2 / IADD3 issue 123-128 lane-ops/clk/SM)",
                     "hbm_view": {"achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
                                  "frac": round(hbm_ach / hbm_peak, 4)}}
+            m = op_models(top, params["paths"], args.block > 1)
+            if m:
+                roof["frac_minimal_model"] = round(ach / alu_peak * m[1] / m[0], 4)
+                roof["minimal_model"] = "DESIGN.md §5: 2.5 lane-ops per cell-path + 3 per cell of cost"
         else:
             roof = {"bound": "hbm", "achieved": round(hbm_ach, 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(hbm_ach / hbm_peak, 4), "traffic": traffic,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md"}
         roof.update({"kernel": KERNEL_NAMES[top], "alg_bytes_per_launch": alg_b,
-                     "avg_launch_ms": round(avg_ms, 4), "launches": nl})
-        # share of the timed region the critical (sweep) stream is busy
+                     "avg_launch_ms": round(avg_ms, 4), "launches": nl, "frames_per_launch": frames_per_launch})
+        if step_dram:
+            roof["step_dram"] = step_dram
+        # share of the profiled pass the critical (sweep) streams are busy
         pipeline = None
         if timeline and st.engine == 3:
             iv = sorted((a, b) for k, a, b in timeline if k in CRITICAL)
@@ -549,13 +696,11 @@ def main():
             span = max(b for _, _, b in timeline) - min(a for _, a, _ in timeline)
             pipeline = {"group_frames": st.group, "critical_stages": list(CRITICAL),
                         "critical_stream_busy": round(busy / max(1e-9, span), 4),
-                        "note": "stage_ms are per-kernel event sums; row/wta/lr overlap the sweeps"}
+                        "profiled_steps": psteps,
+                        "note": "stage_ms from a separate profiled pass; row/wta/lr overlap the sweeps"}
         gate = None
         if not args.no_gate and args.block == 1 and args.lr_mode == 0:
             gate = d1_gate(asd, params, L, R, dev, hbm_peak, traffic_ok=args.config == "C")
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(params, pool_L, pool_R)
         line = {
             "metric": METRIC if args.config == "C" else METRIC_D, "value": round(value, 3), "unit": "frames/s",
             "n_gpus": world,
@@ -565,13 +710,15 @@ def main():
             "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 3),
             "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config)
+                                   + (f" (P2={args.p2})" if args.p2 else "")
                                    + (f"; E: job of {args.job} frames per step sharded over {world} GPU(s)" if args.job else ""),
                        "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
                        "distinct_frames": POOL,
                        "l2": f"inputs larger than L2 ({2 * B * H * W / 1e6:.0f} MB/step/GPU) + per-frame scratch > L2",
                        "engine": st.plan_info},
             "roofline": roof,
-            "stage_ms": {k: round(prof[k]["ms"], 3) for k in asd.abi.STAGES if prof[k]["launches"]},
+            "parity": parity if not args.no_parity else None,
+            "stage_ms": {k: round(prof[k]["ms"] / psteps, 3) for k in asd.abi.STAGES if prof[k]["launches"]},
             "stage_share": stage_share,
             "pipeline": pipeline,
             "hbm_gate": gate,
@@ -582,13 +729,20 @@ def main():
             "valid_frac": round(float(st_all[:, 1].astype(np.int64).sum()) / (len(st_all) * H * W), 4),
         }
         if e2e:
+            if parity_e2e is not None and not args.no_parity:
+                e2e["parity"] = parity_e2e
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
+        bad = (0 if args.no_parity else parity["mismatches"] + (parity_e2e["mismatches"] if parity_e2e else 0))
+        if bad:
+            print(f"PARITY FAILURE: {bad} frame(s) differ from the oracle", file=sys.stderr, flush=True)
     st.close()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0 and not args.no_parity and (parity["mismatches"] or (parity_e2e and parity_e2e["mismatches"])):
+        sys.exit(1)
 
 
 if __name__ == "__main__":

@@ -112,15 +112,19 @@ def load(path: str = LIB_PATH):
 
 @dataclass
 class Params:
-    """asd_params (include/asd.h; SPEC S:257-260 StereoConfig, defaults)."""
+    """asd_params (include/asd.h; fields of SPEC S:257-260 StereoConfig).
+
+    The defaults are this repo's config-C defaults (8 paths, median off), not
+    SPEC S:388's (4 paths, median 3).  p1 / p2 left as None follow S:388 scaled
+    by the block area: P1 = 8 * bw * bh, P2 = 32 * bw * bh (8 / 32 for SGM)."""
     width: int
     height: int
     num_disp: int = 64
     min_disp: int = 0
     census_w: int = 9
     census_h: int = 7
-    p1: int = 8
-    p2: int = 32
+    p1: int | None = None
+    p2: int | None = None
     paths: int = 8
     uniqueness: int = 10
     lr_max_diff: float = 1.0
@@ -132,6 +136,13 @@ class Params:
     block_h: int = 1
     median_ksize: int = 0      # 0 / 3 / 5 (reading c20)
     lr_mode: int = 0           # right view: 0 = R1 re-index (c10), 1 = R2 own SGM (c24)
+
+    def __post_init__(self):
+        area = max(1, self.block_w) * max(1, self.block_h)
+        if self.p1 is None:
+            self.p1 = 8 * area
+        if self.p2 is None:
+            self.p2 = 32 * area
 
     def c(self) -> asd_params:
         return asd_params(self.width, self.height, self.min_disp, self.num_disp, self.census_w,
@@ -256,24 +267,61 @@ class Stereo:
     def __exit__(self, *exc):
         self.close()
 
+    # ---- argument checks (the C ABI takes raw pointers: shapes, dtypes,
+    # contiguity and placement are verified here, before any pointer leaves) ----
+    def _io(self, host: bool, batch: bool, left, right, out_disp, out_depth, stats=None) -> int:
+        import torch
+        H, W = self.params.height, self.params.width
+        lead = (left.shape[0],) if batch else ()
+        if batch and left.dim() != 3:
+            raise ValueError(f"left must be [n][{H}][{W}], got {tuple(left.shape)}")
+        n = left.shape[0] if batch else 1
+
+        def chk(t, name, dtype, shape):
+            if t is None:
+                return
+            if t.dtype != dtype:
+                raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+            if tuple(t.shape) != shape:
+                raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {shape}")
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+            if host:
+                if t.is_cuda:
+                    raise ValueError(f"{name} must be a host (CPU, ideally pinned) tensor")
+            elif not (t.is_cuda and t.device.index == self.device):
+                raise ValueError(f"{name} must be on cuda:{self.device}, got {t.device}")
+
+        chk(left, "left", torch.uint8, lead + (H, W))
+        chk(right, "right", torch.uint8, lead + (H, W))
+        chk(out_disp, "out_disp", torch.float32, lead + (H, W))
+        chk(out_depth, "out_depth", torch.float32, lead + (H, W))
+        chk(stats, "stats", torch.int32, (n, 4))
+        return n
+
     # ---- device entry points (torch CUDA tensors) ----
     def asd_depth(self, left, right, out_disp=None, out_depth=None, stream=None):
+        self._io(False, False, left, right, out_disp, out_depth)
         _check(self._lib.asd_depth(self._ctx, _ptr(left), _ptr(right), _ptr(out_disp),
                                    _ptr(out_depth), _stream(stream)), self._ctx)
 
     def asd_depth_batch(self, left, right, out_disp=None, out_depth=None, stats=None, stream=None):
-        n = left.shape[0]
+        n = self._io(False, True, left, right, out_disp, out_depth, stats)
         _check(self._lib.asd_depth_batch(self._ctx, n, _ptr(left), _ptr(right), _ptr(out_disp),
                                          _ptr(out_depth), _ptr(stats), _stream(stream)), self._ctx)
 
     def asd_depth_debug(self, left, right, outs: dict, out_disp=None, out_depth=None, stream=None):
+        self._io(False, False, left, right, out_disp, out_depth)
+        for k, v in outs.items():
+            if v is not None and not (v.is_cuda and v.is_contiguous()):
+                raise ValueError(f"debug output {k} must be a contiguous CUDA tensor")
         d = asd_debug_out(**{k: (v.data_ptr() if v is not None else None) for k, v in outs.items()})
         _check(self._lib.asd_depth_debug(self._ctx, _ptr(left), _ptr(right), ctypes.byref(d),
                                          _ptr(out_disp), _ptr(out_depth), _stream(stream)), self._ctx)
 
     # ---- host entry point (CPU tensors, ideally pinned) ----
     def asd_depth_batch_host(self, left, right, out_disp=None, out_depth=None, stats=None, stream=None):
-        n = left.shape[0]
+        n = self._io(True, True, left, right, out_disp, out_depth, stats)
         _check(self._lib.asd_depth_batch_host(self._ctx, n, _ptr(left), _ptr(right), _ptr(out_disp),
                                               _ptr(out_depth), _ptr(stats), _stream(stream)), self._ctx)
 

@@ -283,14 +283,22 @@ static double alg_bytes_down(const DevParams& p) { return 2.0 * p.ncell; }
 static double alg_bytes_up(const DevParams& p) { return 4.0 * p.ncell; }
 static double alg_bytes_row(const DevParams& p) { return 6.0 * p.ncell; }
 static double alg_bytes_wta3(const DevParams& p) { return 2.0 * p.ncell + 2.0 * p.npx * 7; }
-// Integer lane-ops per cell of the minimal packed formulation:
-// 2.5 per cell-path of recursion (5 u16x2 instructions per two disparities),
-// 2.5 per cell of cost (XOR, POPC, half a pack), 0.5 per cell of partial
-// output; hrow evaluates the cost twice and adds S (1); the WTA 1.5 per cell
-// and view (half a key IMAD, half a min, half a second-pass min).
-static double alg_ops_sweep(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2.5 * p.ncell + 3.0 * p.ncell; }
-static double alg_ops_up(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 2.5 * p.ncell + 2.0 * p.ncell; }
-static double alg_ops_row(const DevParams& p) { return 2 * 2.5 * p.ncell + 2.5 * p.ncell + 2.0 * p.ncell; }
+// Integer lane-ops per cell, SURVEY §8(d)'s model: o = 5.5 packed (u16x2)
+// lane-ops per cell-path of the recursion, + 2 per cell where the Hamming cost
+// is evaluated (XOR + POPC).  The down sweep evaluates the cost (SGBM: reads the
+// block cost instead), the up sweep takes it from the down sweep's partial
+// words, the row kernel evaluates it again in its left->right pass.  (DESIGN.md
+// §5 also quotes the minimal packed model, 2.5 per cell-path; bench.py prints
+// the fraction under both.)
+static double alg_ops_sweep(const DevParams& p)
+{
+    return (p.paths == 8 ? 3 : 1) * 5.5 * p.ncell + (p.bw * p.bh > 1 ? 0.0 : 2.0) * p.ncell;
+}
+static double alg_ops_up(const DevParams& p) { return (p.paths == 8 ? 3 : 1) * 5.5 * p.ncell; }
+static double alg_ops_row(const DevParams& p)
+{
+    return 2 * 5.5 * p.ncell + (p.bw * p.bh > 1 ? 0.0 : 2.0) * p.ncell;
+}
 static double alg_ops_wta3(const DevParams& p) { return 3.0 * p.ncell; }
 
 // Frames per D3 pipeline group; max_batch / group scratch slots, one
@@ -674,6 +682,11 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
     bool ok = true;
     auto alloc = [&](void** q, size_t bytes) {
         if (ok && cudaMalloc(q, bytes) != cudaSuccess) ok = false;
+#ifdef ASD_CHECKED
+        // checked builds: poison all scratch, so a read of a cell no kernel
+        // wrote changes the results (the initcheck of this build)
+        if (ok) cudaMemset(*q, 0xA5, bytes);
+#endif
     };
     alloc(&c->census_l, L.sig); alloc(&c->census_r, L.sig);
     if (L.s) alloc((void**)&c->S, L.s);

@@ -89,10 +89,12 @@ census4_kernel(DevParams p, const uint8_t* __restrict__ left, const uint8_t* __r
     const int x0 = blockIdx.x * C4_PX, y0 = blockIdx.y * C4_TY;
     const int tid = threadIdx.y * C4_TX + threadIdx.x;
     // base copy: byte c of row r = I(x0 + c - R, y0 + r - Q), 0 outside the image.
-    // R % 4 == 0 (9-wide windows) and W % 4 == 0: word w of a row is the aligned
-    // image word at x0 - R + 4w, loaded whole when it lies inside the image.
+    // R % 4 == 0 (9-wide windows), W % 4 == 0 and a 4-byte aligned frame base
+    // (the caller's pointer is not required to be aligned, asd.h): word w of a
+    // row is the aligned image word at x0 - R + 4w, loaded whole when it lies
+    // inside the image.  Otherwise the byte fill below.
     uint8_t* base = reinterpret_cast<uint8_t*>(&tile[0][0][0]);
-    if (R % 4 == 0 && (p.W & 3) == 0) {
+    if (R % 4 == 0 && (p.W & 3) == 0 && (reinterpret_cast<uintptr_t>(img) & 3) == 0) {
         for (int i = tid; i < TH * TWW; i += C4_TX * C4_TY) {
             const int r = i / TWW, w = i - r * TWW;
             const int gx = x0 - R + 4 * w, gy = y0 + r - Q;

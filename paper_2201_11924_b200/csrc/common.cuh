@@ -2,6 +2,7 @@
 // sm_100a kernels of libasd (product code; shares nothing with oracle/).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace asd {
@@ -41,6 +42,34 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
     h ^= h >> 16; h *= 0x85ebca6bu; h ^= h >> 13; h *= 0xc2b2ae35u; h ^= h >> 16;
     return h;
 }
+
+// Checked builds (-DASD_CHECKED, tools/checked.sh; never the production
+// library): ASD_ASSERT traps on a violated index invariant, and ASD_JITTER
+// puts a pseudo-random __nanosleep (up to ~1 us, one warp in four per site) at
+// the synchronisation points of the pipelined kernels, so that a missing
+// barrier, fence or mbarrier wait shows up as an oracle mismatch in repeated
+// runs (compute-sanitizer is not available on the GPU pool).
+#ifdef ASD_CHECKED
+#define ASD_ASSERT(c)                                                                      \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("ASD_ASSERT %s failed at %s:%d block (%d,%d) thread %d\n", #c, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);          \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+__device__ __forceinline__ void asd_jitter(unsigned site)
+{
+    unsigned h = (unsigned)clock64() ^ (site * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu) ^
+                 (blockIdx.y * 0xC2B2AE35u) ^ ((threadIdx.x >> 5) * 0x27D4EB2Fu);
+    h ^= h >> 16; h *= 0x7FEB352Du; h ^= h >> 15;
+    if ((h & 3) == 0) __nanosleep(h >> 22);
+}
+#define ASD_JITTER(site) asd_jitter(site)
+#else
+#define ASD_ASSERT(c) ((void)0)
+#define ASD_JITTER(site) ((void)0)
+#endif
 
 // Per-frame pointers of one in-flight frame slot.
 struct FrameScratch {

@@ -279,6 +279,8 @@ vsweep_kernel(VArgs a)
     // row).  K_up reads its costs from K_down's packed output instead.
     auto stage = [&](int yrow, int slot) {
         if (UP || ABL(a, 64)) { if (!UP) cp_async_commit(); return; }
+        ASD_JITTER(6);
+        ASD_ASSERT(slot >= 0 && slot < NSLOT && yrow >= 0 && yrow < H);
         uint32_t* sl = cens + slot * sw;
         const uint32_t* rl = cl + (long long)yrow * W;
         const uint32_t* rr = cr + (long long)yrow * W;
@@ -334,6 +336,7 @@ vsweep_kernel(VArgs a)
     const unsigned row_bytes = (unsigned)(w * D * 2);
     auto issue_row = [&](int i) {                    // TMA the i-th processed row into the ring(s)
         if (RING && threadIdx.x == 0 && i < H && !ABL(a, 64)) {
+            ASD_JITTER(4);
             const long long roff = ((long long)row_of(i) * wpad + x0) * D;
             uint64_t* bar = mbar + (i % KR);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -345,6 +348,7 @@ vsweep_kernel(VArgs a)
     };
     auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
         if (!ABL(a, 64)) mbar_wait(mbar + (i % KR), (unsigned)((i / KR) & 1));
+        ASD_JITTER(5);
         const long long boff = (long long)(i % KR) * w * D + (warp * CPW) * D;
         const uint4* src = reinterpret_cast<const uint4*>(ring + boff) + lane;
         const uint4* src2 = reinterpret_cast<const uint4*>((UP ? ring2 : ring) + boff) + lane;
@@ -372,13 +376,14 @@ vsweep_kernel(VArgs a)
     // rows; only the edge warps wrote into neighbouring CTAs (DSMEM), so only they
     // pay a cluster-scope fence before the relaxed cluster arrive.
     auto arrive = [&]() {
+        ASD_JITTER(1);
         __syncthreads();
         if (clustered) {
             if (warp == 0 || warp == nw - 1) fence_cluster();
             cluster_arrive_relaxed();
         }
     };
-    auto wait = [&]() { if (clustered) cluster_wait(); };
+    auto wait = [&]() { if (clustered) cluster_wait(); ASD_JITTER(2); };
 
     // halo write targets of this thread, slot 0 (slot 1 = + hslot / + nw), fixed for the kernel
     const int hslot = nw * T * NR;
@@ -477,6 +482,7 @@ vsweep_kernel(VArgs a)
         // path so the DSMEM stores are in flight while it runs
         if (NP == 3) {
             const int ws = i & 1;
+            ASD_JITTER(3);
             if (wL) {                        // my "L" state feeds column x+1 next row
                 uint4* d4 = reinterpret_cast<uint4*>(wL + ws * hslot);
 #pragma unroll
@@ -1330,6 +1336,7 @@ wta2_kernel(RArgs a)
         cp_async_commit();
         if (WTA_SPLIT) cp_async_wait<1>();
         else cp_async_wait<0>();
+        ASD_JITTER(7);
         __syncthreads();
         // left view
         {
@@ -1348,6 +1355,7 @@ wta2_kernel(RArgs a)
         }
         if constexpr (MODE != 0) continue;           // R2 passes: one view per launch
         if (WTA_SPLIT) cp_async_wait<0>();
+        ASD_JITTER(8);
         __syncthreads();                              // left poisoning done before diagonal reads
         // right view
         {
@@ -1474,8 +1482,10 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     else if (p.D == 32) { pl.DC = 32; pl.T = 1; }
     else if (p.D == 64) { pl.DC = 32; pl.T = 2; }
     else { pl.DC = 32; pl.T = 4; }
+#ifdef ASD_ABLATE                                    // experiment builds only (tools/ab.sh)
     const char* force = getenv("ASD_V2_DC16");
     if (p.D == 128 && force && force[0] == '1') { pl.DC = 16; pl.T = 8; }
+#endif
     const int T = pl.T, CPW = 32 / T;
     const int maxt = pl.DC == 32 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
     const bool blk = p.bw * p.bh > 1;                // SGBM block cost (reading c19)
@@ -1486,8 +1496,12 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double best = -1.0;
-    const char* fcs = getenv("ASD_V2_CS");            // testing aid: force a cluster size
+#ifdef ASD_ABLATE
+    const char* fcs = getenv("ASD_V2_CS");            // experiment builds: force a cluster size
     const int force_cs = fcs ? atoi(fcs) : 0;
+#else
+    const int force_cs = 0;
+#endif
     for (int cs = 1; cs <= 16; ++cs) {
         if (force_cs > 0 && cs != force_cs) continue;
         int w = (p.W + cs - 1) / cs;
@@ -1606,8 +1620,10 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         VArgs a{};
         a.p = p; a.w = pl.w; a.cs = pl.cs;
         a.cl = (const uint32_t*)cl; a.cr = (const uint32_t*)cr; a.sig_stride = sig_stride;
+#ifdef ASD_ABLATE
         static const int ablate = getenv("ASD_V2_ABLATE") ? atoi(getenv("ASD_V2_ABLATE")) : 0;
         a.ablate = ablate;
+#endif
         a.pin = reinterpret_cast<const uint16_t*>(pa); a.pouta = reinterpret_cast<uint16_t*>(pa);
         a.pa_stride = (long long)p.H * pl.cs * pl.w * p.D;
         a.pout16 = pab; a.cell_stride = cell_stride;

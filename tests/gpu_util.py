@@ -95,3 +95,38 @@ def compare_full(g: dict, o: dict, stages=True):
     assert_bits_equal(g["disp_r"], o["dr"], "dr")
     assert_bits_equal(g["disp"], o["disp"], "disp")
     assert_depth_close(g["depth"], o["depth"])
+
+
+def oracle_frames(d: dict, Ls, Rs, threads: int = 0) -> list:
+    """oracle.compute on every frame, one frame per host thread (ctypes releases
+    the GIL), memory-bounded (about 1.6 GB per config-C frame)."""
+    import os
+    import threading
+    p = oracle.Params(**{k: v for k, v in d.items() if k != "engine"})
+    oracle.lib()
+    n = len(Ls)
+    if threads <= 0:
+        try:
+            import psutil
+            mem = int(psutil.virtual_memory().available // (2.0 * 1.6e9 * max(1, p.width * p.height * p.num_disp / 117964800)))
+        except Exception:
+            mem = 4
+        threads = max(1, min(n, len(os.sched_getaffinity(0)), mem, 16))
+    out = [None] * n
+    for k in range(0, n, threads):
+        part = list(range(k, min(n, k + threads)))
+
+        def run(i):
+            out[i] = oracle.compute(p, Ls[i], Rs[i])
+
+        ths = [threading.Thread(target=run, args=(i,)) for i in part]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    return out
+
+
+def oracle_sig(o) -> tuple:
+    """(checksum, valid count) of an oracle frame (asd_frame_stats fields)."""
+    return oracle.checksum(o["dstar_l"], o["mask"]), int((o["mask"] == 0).sum())

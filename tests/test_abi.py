@@ -122,3 +122,30 @@ def test_rectify_validation(lib):
     assert lib.asd_rectify(sing, 0, 8, 8, None, None, None) == asd.ASD_E_INVALID_ARG
     assert lib.asd_rectify(eye, -1, 8, 8, None, None, None) == asd.ASD_E_INVALID_ARG
     assert lib.asd_rectify(eye, 0, 8, 8, None, None, None) == asd.ASD_OK
+
+
+def test_binding_argument_checks():
+    """The binding verifies dtype, shape, contiguity and placement before a raw
+    pointer reaches the C ABI (no GPU needed: the checks run first)."""
+    import torch
+    st = asd.Stereo.__new__(asd.Stereo)
+    st.params, st.device = asd.Params(64, 48, 16, census_w=5, census_h=5), 0
+    u8 = torch.zeros(2, 48, 64, dtype=torch.uint8)
+    f32 = torch.zeros(2, 48, 64)
+    s32 = torch.zeros(2, 4, dtype=torch.int32)
+    assert st._io(True, True, u8, u8, f32, f32, s32) == 2          # host path: CPU tensors ok
+    with pytest.raises(ValueError):
+        st._io(False, True, u8, u8, None, None)                     # device path: CPU tensor
+    with pytest.raises(TypeError):
+        st._io(True, True, u8.float(), u8, None, None)              # wrong dtype
+    with pytest.raises(ValueError):
+        st._io(True, True, u8, u8[:1], None, None)                  # right has fewer frames
+    with pytest.raises(ValueError):
+        st._io(True, True, u8, u8, f32[:, :, :32], None)            # wrong width
+    with pytest.raises(ValueError):
+        st._io(True, True, u8, u8.transpose(1, 2).contiguous().transpose(1, 2), None, None)
+    with pytest.raises(ValueError):
+        st._io(True, True, u8, u8, None, None, torch.zeros(3, 4, dtype=torch.int32))
+    p = asd.Params(64, 48, 16, block_w=3, block_h=3)
+    assert (p.p1, p.p2) == (72, 288)                                # S:388 scaled by the block area
+    assert (asd.Params(64, 48, 16).p1, asd.Params(64, 48, 16).p2) == (8, 32)

@@ -65,3 +65,59 @@ def test_gloo_world2_gather_and_max():
     assert tmax == 2.5
     assert [row[1] for row in allst] == list(range(10))
     assert [row[0] for row in allst] == [1000 + f for f in range(10)]
+
+
+# ---- bench.py's multi-rank report path (shard -> timed stats -> gather ->
+# per-frame oracle check on rank 0), driven with a stubbed step over gloo
+def _bench_worker(rank, world, port, q, corrupt):
+    import torch.distributed as dist
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B = 6
+        f0, f1 = shard_range(world * B, rank, world)
+        sigs = {i: (0xA0000000 + 17 * i, 1000 + i) for i in range(bench.POOL)}   # stand-in oracle
+        stats = torch.zeros(B, 4, dtype=torch.int32)
+        for k, f in enumerate(range(f0, f1)):          # the stubbed step: frame f = pool[f % POOL]
+            cs, valid = sigs[f % bench.POOL]
+            stats[k, 0] = torch.tensor(cs, dtype=torch.int64).to(torch.int32)
+            stats[k, 1] = valid
+            if f == corrupt:
+                stats[k, 1] += 1
+        calls = []
+
+        def sigs_fn():
+            calls.append(rank)
+            return sigs
+
+        ms_max, allst, parity = bench.gather_and_check(stats, 10.0 + rank, sigs_fn)
+        q.put((rank, ms_max, allst.shape[0], parity, calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("corrupt", [-1, 9])
+def test_gloo_world2_bench_report_path(corrupt):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q, corrupt)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, ms_max, nrows, parity, calls = q.get(timeout=120)
+        res[r] = (ms_max, nrows, parity, calls)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == res[1][0] == 11.0            # max over ranks
+    assert res[0][1] == res[1][1] == 12              # every frame of the job gathered
+    assert res[1][2] is None and res[1][3] == []     # only rank 0 consults the oracle
+    par = res[0][2]
+    assert res[0][3] == [0] and par["frames"] == 12
+    if corrupt < 0:
+        assert par["mismatches"] == 0
+    else:
+        assert par["mismatches"] == 1 and par["first_bad"] == [corrupt]
