@@ -205,13 +205,15 @@ struct Layout {
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 // pa_cols: columns of a P_A row (D3 pads it to the sweep grid, cs*w >= W).
-Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols)
+// cbuf: D3 runs its u16-partial (BLK) instances (SGBM, or SGM beyond the u8
+// partial range, V2Plan::blk), so a cost buffer in the sweeps' layout exists.
+Layout layout(const DevParams& d, int max_batch, int engine, int pa_cols, bool cbuf = false)
 {
     Layout L{};
     const size_t B = (size_t)max_batch;
     L.sig = align_up(B * d.npx * (d.nb <= 32 ? 4 : 8));
     L.s = engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2) : 0;
-    const bool blk = d.bw * d.bh > 1;
+    const bool blk = d.bw * d.bh > 1 || (engine == ASD_ENGINE_D3 && cbuf);
     L.cb = !blk ? 0 : engine == ASD_ENGINE_D1 ? align_up(B * d.ncell * 2)
                                               : align_up(B * d.H * pa_cols * d.D * 2);
     L.sr = (engine == ASD_ENGINE_D1 && d.lr_mode == 1) ? align_up(B * d.ncell * 2) : 0;
@@ -629,7 +631,7 @@ size_t asd_scratch_bytes(const asd_params* p, int max_batch)
         int dev = 0;
         cudaGetDevice(&dev);
         V2Plan pl;
-        if (v2_plan(d, dev, pl)) return layout(d, max_batch, ASD_ENGINE_D3, pl.cs * pl.w).total;
+        if (v2_plan(d, dev, pl)) return layout(d, max_batch, ASD_ENGINE_D3, pl.cs * pl.w, pl.blk).total;
         cudaGetLastError();
     }
     return layout(d, max_batch, engine, d.W).total;
@@ -678,7 +680,8 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         if (wta2_plan(c->dp, smax >= (1ll << (16 - ks)), c->plan)) c->wta2 = true;
     }
     Layout L = layout(c->dp, max_batch, c->engine,
-                      c->engine == ASD_ENGINE_D3 ? c->plan.cs * c->plan.w : c->dp.W);
+                      c->engine == ASD_ENGINE_D3 ? c->plan.cs * c->plan.w : c->dp.W,
+                      c->engine == ASD_ENGINE_D3 && c->plan.blk);
     bool ok = true;
     auto alloc = [&](void** q, size_t bytes) {
         if (ok && cudaMalloc(q, bytes) != cudaSuccess) ok = false;

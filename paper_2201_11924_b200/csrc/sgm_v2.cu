@@ -61,6 +61,11 @@ __device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc, 
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" :: "r"(sa), "l"(gsrc), "r"(valid ? 4 : 0) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
@@ -115,6 +120,35 @@ __device__ __forceinline__ void fence_cluster()
 __device__ __forceinline__ void cluster_wait()
 {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Decoupled sweeps (vsweep_dec_kernel): point-to-point mbarrier signals
+// between neighbouring warps instead of a CTA / cluster barrier per row.
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, unsigned rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+// arrive with CTA-scope release: orders this warp's halo stores (the writing
+// lanes synchronise with the arriving lane through __syncwarp first)
+__device__ __forceinline__ void mbar_arrive_local(uint32_t addr)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" :: "r"(addr) : "memory");
+}
+// arrive on a neighbouring CTA's barrier; the writing lanes fenced at cluster
+// scope before (fence.acq_rel.cluster), so the arrive itself is relaxed
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr)
+{
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" :: "r"(cluster_addr) : "memory");
+}
+// wait for a phase completed by a remote arrive: poll relaxed, then one
+// cluster-scope acquire fence (an acquire poll would invalidate L1 per try)
+__device__ __forceinline__ void mbar_wait_remote(uint64_t* bar, unsigned parity)
+{
+    asm volatile("{\n .reg .pred P;\n WAITR_%=:\n"
+                 " mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 P, [%0], %1;\n"
+                 " @!P bra WAITR_%=;\n}\n fence.acq_rel.cluster;\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
 struct VArgs {
@@ -187,6 +221,20 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
     mout = m;
 }
 
+// K_up output staging: 16-byte piece pi of a warp's (CPW columns x D) u16
+// block is stored at stg_swz(pi).  A 16-byte shared access is served per
+// quarter warp (8 lanes); both the writes (lane = (column, chunk), piece
+// column * PPC + chunk * DC/8 + q) and the reads (8 consecutive pieces) must
+// hit 8 distinct 16-byte bank groups.  PPC = 16 (T = 4): a quarter is 2 columns
+// x 4 chunks, so the XOR takes the column's low bit and the chunk's high bit
+// (piece bits 4 and 3); otherwise the column's low bits.
+template <int PPC>
+__device__ __forceinline__ int stg_swz(int pi)
+{
+    if constexpr (PPC == 16) return pi ^ ((((pi >> 3) & 1) << 1) | ((pi >> 4) & 1));
+    else return pi ^ ((pi / PPC) & ((PPC < 8 ? PPC : 8) - 1));
+}
+
 // ---------------------------------------------------------------- K_down / K_up
 // Shared-memory census rows: the left row (w words) and, per chunk k, the
 // slice of the right row its DC disparities read (w + DC - 1 words), placed at
@@ -217,10 +265,10 @@ struct VGeom {
 // by TMA in this kernel's private layout (K_down: CB ring instead of census
 // staging; K_up: a CB ring beside the P_A ring), and the handoffs carry the
 // wider partials without the cost bits: K_down writes P_A (u16), K_up P_AB.
-#ifndef ASD_VLATE
-#define ASD_VLATE 0
+#ifndef ASD_V2_DEC
+#define ASD_V2_DEC 0              // 1: vsweep_dec_kernel (experiment: measured slower); 0: barrier per row
 #endif
-constexpr bool VLATE = ASD_VLATE;
+constexpr bool DEC = ASD_V2_DEC;
 
 template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
 __global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
@@ -251,8 +299,11 @@ vsweep_kernel(VArgs a)
     constexpr int NRING = (UP && BLK) ? 2 : 1;
     uint32_t* cens = smem;                   // [NSLOT][sw] (K_down): left row, then T right-row slices
     uint32_t* hL = cens + nslot * sw;        // [2][nw][T][NR]   (NP == 3)
-    uint32_t* hR = hL + 2 * nw * T * NR;
-    uint32_t* hLM = hR + 2 * nw * T * NR;    // [2][nw]
+    // halo state per chunk padded to HS = NR + 4 words: the T edge lanes of a
+    // column (one per chunk) then hit distinct 16-byte bank groups
+    constexpr int HS = NR + 4;
+    uint32_t* hR = hL + 2 * nw * T * HS;
+    uint32_t* hLM = hR + 2 * nw * T * HS;    // [2][nw]
     uint32_t* hRM = hLM + 2 * nw;
     // K_up output staging: one (CPW columns x D) u16 block per warp, so the
     // global stores of P_AB can be issued as contiguous 512-byte warp stores
@@ -262,7 +313,8 @@ vsweep_kernel(VArgs a)
     // (K_up: P_A | C, or P_A then CB for BLK; BLK K_down: CB)
     uint16_t* ring = reinterpret_cast<uint16_t*>(stg0 + (UP ? nw * 16 * DC : 0));
     uint16_t* ring2 = ring + KR * w * D;             // BLK K_up: the CB ring
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + (RING ? NRING * KR * w * D : 0));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(ring + (RING ? NRING * KR * w * D : 0)) + 7) & ~uintptr_t(7));
     // K_down -> K_up handoff in a private layout: the warp's (CPW columns x D)
     // block is contiguous and instruction q of lane l covers 16 bytes at
     // 512*q + 16*l, i.e. warp-contiguous stores and loads (row stride cs*w).
@@ -272,7 +324,7 @@ vsweep_kernel(VArgs a)
     const uint32_t* cr = a.cr + frame * a.sig_stride;
 
     if (NP == 3) {
-        for (int i = threadIdx.x; i < 4 * nw * T * NR + 4 * nw; i += blockDim.x) hL[i] = 0u;
+        for (int i = threadIdx.x; i < 4 * nw * T * HS + 4 * nw; i += blockDim.x) hL[i] = 0u;
     }
     auto row_of = [&](int i) { return UP ? H - 1 - i : i; };
     // census rows -> shared memory with asynchronous copies (one commit group per
@@ -334,8 +386,8 @@ vsweep_kernel(VArgs a)
     const bool xin = x < W;
     // K_up: P_A and C of one row from K_down's packed words (reg k = cells d0+k, d0+NR+k)
     const unsigned row_bytes = (unsigned)(w * D * 2);
-    auto issue_row = [&](int i) {                    // TMA the i-th processed row into the ring(s)
-        if (RING && threadIdx.x == 0 && i < H && !ABL(a, 64)) {
+    auto issue_row_by = [&](int i) {                 // TMA the i-th processed row into the ring(s)
+        if (RING && i < H && !ABL(a, 64)) {
             ASD_JITTER(4);
             const long long roff = ((long long)row_of(i) * wpad + x0) * D;
             uint64_t* bar = mbar + (i % KR);
@@ -346,6 +398,7 @@ vsweep_kernel(VArgs a)
                                  row_bytes, bar);
         }
     };
+    auto issue_row = [&](int i) { if (threadIdx.x == 0) issue_row_by(i); };
     auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
         if (!ABL(a, 64)) mbar_wait(mbar + (i % KR), (unsigned)((i / KR) & 1));
         ASD_JITTER(5);
@@ -386,27 +439,27 @@ vsweep_kernel(VArgs a)
     auto wait = [&]() { if (clustered) cluster_wait(); ASD_JITTER(2); };
 
     // halo write targets of this thread, slot 0 (slot 1 = + hslot / + nw), fixed for the kernel
-    const int hslot = nw * T * NR;
+    const int hslot = nw * T * HS;
     uint32_t* wL = nullptr; uint32_t* wLm = nullptr;   // edge lane col == CPW-1 -> column x+1
     uint32_t* wR = nullptr; uint32_t* wRm = nullptr;   // edge lane col == 0     -> column x-1
     if (NP == 3) {
         if (col == CPW - 1) {
             if (warp + 1 < nw) {
-                wL = hL + ((warp + 1) * T + chunk) * NR;
+                wL = hL + ((warp + 1) * T + chunk) * HS;
                 wLm = hLM + warp + 1;
             } else if (rank + 1 < a.cs) {
                 cg::cluster_group cl_g = cg::this_cluster();
-                wL = cl_g.map_shared_rank(hL + chunk * NR, rank + 1);
+                wL = cl_g.map_shared_rank(hL + chunk * HS, rank + 1);
                 wLm = cl_g.map_shared_rank(hLM, rank + 1);
             }
         }
         if (col == 0) {
             if (warp > 0) {
-                wR = hR + ((warp - 1) * T + chunk) * NR;
+                wR = hR + ((warp - 1) * T + chunk) * HS;
                 wRm = hRM + warp - 1;
             } else if (rank > 0) {
                 cg::cluster_group cl_g = cg::this_cluster();
-                wR = cl_g.map_shared_rank(hR + ((nw - 1) * T + chunk) * NR, rank - 1);
+                wR = cl_g.map_shared_rank(hR + ((nw - 1) * T + chunk) * HS, rank - 1);
                 wRm = cl_g.map_shared_rank(hRM + nw - 1, rank - 1);
             }
         }
@@ -419,6 +472,137 @@ vsweep_kernel(VArgs a)
     uint32_t C[NR];
     uint32_t PA[NR];
 
+    // ---- the per-row pieces shared by both synchronisation schemes
+    // diagonal paths of row i from the predecessors of row i-1 (halo slot rs)
+    auto diagonals = [&](int i) {
+        const int rs = (i + 1) & 1;              // slot written at row i-1
+        uint32_t Pp[NR], Mp;
+        // path "L": predecessor column x-1 (down-right / up-right)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) Pp[k] = __shfl_up_sync(FULL, Ll[k], T);
+        Mp = __shfl_up_sync(FULL, Ml, T);
+        if (col == 0) {
+            const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                const uint4 v = h[q];
+                Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
+            }
+            Mp = hLM[rs * nw + warp];
+        }
+        path_update<NR, T>(p, chunk, Pp, Mp, C, Ll, Ml);
+        // path "R": predecessor column x+1 (down-left / up-left)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) Pp[k] = __shfl_down_sync(FULL, Lr[k], T);
+        Mp = __shfl_down_sync(FULL, Mr, T);
+        if (col == CPW - 1) {
+            const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                const uint4 v = h[q];
+                Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
+            }
+            Mp = hRM[rs * nw + warp];
+        }
+        path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
+        // columns beyond the image act as "outside" predecessors: zero state
+        if (!xin) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) { Ll[k] = 0u; Lr[k] = 0u; }
+            Ml = Mr = 0u;
+        }
+    };
+    // halos of row i for the next row (slot i & 1)
+    auto write_halos = [&](int i) {
+        const int ws = i & 1;
+        ASD_JITTER(3);
+        if (wL) {                        // my "L" state feeds column x+1 next row
+            uint4* d4 = reinterpret_cast<uint4*>(wL + ws * hslot);
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]);
+            if (chunk == 0) wLm[ws * nw] = Ml;
+        }
+        if (wR) {                        // my "R" state feeds column x-1 next row
+            uint4* d4 = reinterpret_cast<uint4*>(wR + ws * hslot);
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
+            if (chunk == 0) wRm[ws * nw] = Mr;
+        }
+    };
+    // vertical path: predecessor = own column
+    auto vertical = [&]() {
+        if (!ABL(a, 32)) {
+            uint32_t Ln[NR], mnew;
+            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
+            Mv = mnew;
+        }
+        if (!xin) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) Lv[k] = 0u;
+            Mv = 0u;
+        }
+    };
+    // partial sum of row y out
+    auto partial_out = [&](int y) {
+        if (ABL(a, 2)) return;
+        uint32_t s[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) s[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
+        if (!UP) {
+            // P_A (<= 255) | C << 8 (C <= 63): the up sweep needs no census
+            // (BLK: P_A alone, the up sweep reads CB itself)
+            uint4* dst = reinterpret_cast<uint4*>(a.pouta + frame * a.pa_stride +
+                                                  ((long long)y * wpad + (x - col)) * D) + lane;
+            constexpr uint32_t CS = BLK ? 0u : 256u;
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q)
+                dst[32 * q] = make_uint4(s[4 * q] + C[4 * q] * CS, s[4 * q + 1] + C[4 * q + 1] * CS,
+                                         s[4 * q + 2] + C[4 * q + 2] * CS, s[4 * q + 3] + C[4 * q + 3] * CS);
+        } else {
+            // P_AB (<= 510) | C << 9: the right->left row sweep needs no census
+#pragma unroll
+            for (int k = 0; k < NR; ++k) s[k] += PA[k] + C[k] * (BLK ? 0u : 512u);
+            uint32_t o[NR];
+            if (DPL_ROW == 4) {
+#pragma unroll
+                for (int g = 0; g < DC / 4; ++g) {
+                    const int kk = 4 * g < NR ? 4 * g : 4 * g - NR;
+                    const uint32_t sel = 4 * g < NR ? 0x5410u : 0x7632u;
+                    o[2 * g] = __byte_perm(s[kk], s[kk + 2], sel);
+                    o[2 * g + 1] = __byte_perm(s[kk + 1], s[kk + 3], sel);
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < DC / 2; ++g) {
+                    const int kk = 2 * g < NR ? 2 * g : 2 * g - NR;
+                    const uint32_t sel = 2 * g < NR ? 0x5410u : 0x7632u;
+                    o[g] = __byte_perm(s[kk], s[kk + 1], sel);
+                }
+            }
+            // natural [x][d] layout through the warp's staging block.  16-byte
+            // piece p of the block (column p / PPC) is stored at p ^ (column &
+            // SWZ): without it the 32 lanes of one store instruction fall into
+            // two 16-byte bank groups (a 16-way conflict).
+            constexpr int PPC = DC * T / 8;                   // 16-byte pieces per column
+            uint4* sb = reinterpret_cast<uint4*>(stg);
+            const int pbase = col * PPC + chunk * (DC / 8);
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q)
+                sb[stg_swz<PPC>(pbase + q)] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            __syncwarp();
+            uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + ((long long)y * W + (x - col)) * D);
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                const int pi = 32 * q + lane;                 // 16-byte piece of the block
+                if (x - col + pi / PPC < W) dst[pi] = sb[stg_swz<PPC>(pi)];
+            }
+            __syncwarp();
+        }
+    };
+
+    // ============ legacy scheme: one CTA barrier + one cluster barrier per row
     if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
     if (RING) {
         if (threadIdx.x == 0) {
@@ -440,8 +624,255 @@ vsweep_kernel(VArgs a)
     for (int i = 0; i < H; ++i) {
         const int y = row_of(i);
         if (i > 0) wait();
-        if (NP == 3 && !ABL(a, 4)) {
-            const int rs = (i + 1) & 1;              // slot written at row i-1
+        if (NP == 3 && !ABL(a, 4)) diagonals(i);
+        // ---- halos for the next row: written before the vertical path so the
+        // DSMEM stores are in flight while it runs
+        if (NP == 3) write_halos(i);
+        vertical();
+        // ---- K_down: stage row i+NSLOT-1 (async), make row i+1's copies complete, publish
+        if (!RING) {
+            if (i + NSLOT - 1 < H) stage(row_of(i + NSLOT - 1), (i + NSLOT - 1) % NSLOT);
+            else cp_async_commit();                  // keep one group per row
+            cp_async_wait<NSLOT - 2>();
+        }
+        arrive();
+        issue_row(i + KR);                            // ring input: row i's slot is free now
+        // ---- partial sum out (after the release so it does not wait on these stores)
+        partial_out(y);
+        // ---- next row's cost while the barrier completes
+        if (i + 1 < H) {
+            if (RING) load_pin(i + 1, PA, C);
+            else cost(row_of(i + 1), (i + 1) % NSLOT, C);
+        }
+    }
+    wait();                                          // pairs with the last arrive
+    if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
+}
+
+#if ASD_V2_DEC
+// ---------------------------------------------------------------- K_down / K_up, decoupled
+// The same sweeps with every warp autonomous except for its two neighbours:
+//  * inputs are staged per warp (census rows of its CPW columns and the T
+//    right-census slices they match, or its block of the K_down partials / CB
+//    rows) with cp.async groups into a warp-private ring -- no slot is shared,
+//    so no warp waits for another to drain it;
+//  * the diagonal halos go to the neighbour warp (or, at CTA edges, the
+//    neighbour CTA through DSMEM) and are signalled by an mbarrier per consumer
+//    warp and slot (count 1); neighbours are at most one row apart (each needs
+//    the other's previous row), so two slots suffice;
+//  * no CTA- or cluster-wide barrier inside the row loop.
+template <int DC, int T>
+struct DGeom {
+    static constexpr int NR = DC / 2;
+    static constexpr int CPW = 32 / T;
+    static constexpr int NSL = CPW + DC - 1;                              // words of one right slice
+    static constexpr int SS = CPW + 32 * ((NSL - CPW + 31) / 32);         // >= NSL, = CPW (mod 32)
+    static constexpr int CW = 32 + T * SS;                                // words per census slot
+    static constexpr int RW = CPW * DC * T / 2;                           // words per ring row (u16 x CPW x D)
+};
+constexpr int DNSLOT = 4;      // census rows in flight per warp (K_down)
+constexpr int DKR = 3;         // ring rows in flight per warp (K_up, BLK K_down)
+constexpr int DKR2 = 2;        // per ring when BLK K_up stages two (P_A and CB)
+
+template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
+__global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
+vsweep_dec_kernel(VArgs a)
+{
+    using G = DGeom<DC, T>;
+    constexpr int NR = G::NR, CPW = G::CPW, CW = G::CW, SS = G::SS, RW = G::RW;
+    constexpr bool RING = UP || BLK;
+    constexpr int NRING = (UP && BLK) ? 2 : 1;
+    constexpr int KR = (UP && BLK) ? DKR2 : DKR;
+    extern __shared__ uint32_t smem[];
+    const DevParams& p = a.p;
+    const int W = p.W, H = p.H, D = p.D;
+    const int nw = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int col = lane / T, chunk = lane % T;
+    const int rank = blockIdx.x;
+    const int frame = blockIdx.y;
+    const int w = a.w;
+    const int x0 = rank * w;
+    const int xw0 = x0 + warp * CPW;                 // the warp's first column
+    const int xl = warp * CPW + col;
+    const int x = x0 + xl;
+    const bool clustered = NP == 3 && a.cs > 1;
+    const int wpad = a.cs * a.w;
+
+    // ---- shared memory (words): census ring | halos | K_up staging | input ring(s) | mbarriers
+    uint32_t* cen = smem;                                           // [nw][DNSLOT][CW]    (K_down, !BLK)
+    uint32_t* hL = cen + (RING ? 0 : nw * DNSLOT * CW);             // [2][nw][T][NR]      (NP == 3)
+    uint32_t* hR = hL + (NP == 3 ? 2 * nw * T * NR : 0);
+    uint32_t* hLM = hR + (NP == 3 ? 2 * nw * T * NR : 0);           // [2][nw]
+    uint32_t* hRM = hLM + (NP == 3 ? 2 * nw : 0);
+    uint32_t* stg0 = hRM + (NP == 3 ? 2 * nw : 0);                  // [nw][16 * DC]       (UP)
+    uint32_t* stg = stg0 + warp * (16 * DC);
+    uint32_t* rings = stg0 + (UP ? nw * 16 * DC : 0);               // [nw][NRING][KR][RW] (RING)
+    uint64_t* hb = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(rings + (RING ? nw * NRING * KR * RW : 0)) + 7) & ~uintptr_t(7));
+    uint64_t* hbL = hb;                                             // [2][nw]  halo "L" full, per consumer
+    uint64_t* hbR = hb + 2 * nw;                                    // [2][nw]  halo "R" full
+    uint32_t* cenw = cen + warp * DNSLOT * CW;
+    uint16_t* ringw = reinterpret_cast<uint16_t*>(rings + warp * NRING * KR * RW);
+
+    const uint32_t* cl = a.cl + frame * a.sig_stride;
+    const uint32_t* cr = a.cr + frame * a.sig_stride;
+    auto row_of = [&](int i) { return UP ? H - 1 - i : i; };
+
+    // ---- warp-private input staging (one cp.async group per row)
+    auto stage = [&](int i) {
+        __syncwarp();                                // lanes' earlier reads of the slot are done
+        if (i < H) {
+            ASD_JITTER(6);
+            const int yrow = row_of(i);
+            if constexpr (RING) {
+                const long long roff = ((long long)yrow * wpad + xw0) * D;
+                uint16_t* dst = ringw + (i % KR) * (2 * RW);
+#pragma unroll
+                for (int q = 0; q < DC / 8; ++q) {
+                    const int pc = 32 * q + lane;             // 16-byte piece of the warp's block
+                    if (UP) cp_async16(dst + 8 * pc, a.pin + frame * a.pa_stride + roff + 8 * pc);
+                    if (BLK) cp_async16(dst + (UP ? KR * 2 * RW : 0) + 8 * pc, a.cbin + frame * a.pa_stride + roff + 8 * pc);
+                }
+            } else {
+                uint32_t* sl = cenw + (i % DNSLOT) * CW;
+                const uint32_t* rl = cl + (long long)yrow * W;
+                const uint32_t* rr = cr + (long long)yrow * W;
+                if (lane < CPW) {
+                    const int gx = xw0 + lane;
+                    cp_async4(sl + lane, gx < W ? rl + gx : rl, gx < W);
+                }
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    const int g0 = RR ? xw0 + p.min_disp + DC * k : xw0 - p.min_disp - DC * k - (DC - 1);
+#pragma unroll
+                    for (int ii0 = 0; ii0 < G::NSL; ii0 += 32) {
+                        const int ii = ii0 + lane;
+                        if (ii < G::NSL) {
+                            const int gx = g0 + ii;
+                            const bool ok = gx >= 0 && gx < W;
+                            cp_async4(sl + 32 + k * SS + ii, ok ? rr + gx : rr, ok);
+                        }
+                    }
+                }
+            }
+        }
+        cp_async_commit();                           // one group per row (empty past the last)
+    };
+    constexpr int DEPTH = RING ? KR : DNSLOT;
+    auto ready = [&]() { cp_async_wait<DEPTH - 2>(); __syncwarp(); };
+
+    // ---- row i's costs (and K_up's P_A) from the warp's slot
+    const bool vcol = x >= p.R && x < W - p.R;
+    const bool xin = x < W;
+    uint32_t C[NR], PA[NR];
+    auto load_input = [&](int i) {
+        if constexpr (RING) {
+            const uint16_t* blk = ringw + (i % KR) * (2 * RW);
+            const uint4* src = reinterpret_cast<const uint4*>(blk) + lane;
+            const uint4* src2 = reinterpret_cast<const uint4*>(blk + (UP && BLK ? KR * 2 * RW : 0)) + lane;
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                if constexpr (BLK) {
+                    const uint4 cv = src2[32 * q];
+                    C[4 * q] = cv.x; C[4 * q + 1] = cv.y; C[4 * q + 2] = cv.z; C[4 * q + 3] = cv.w;
+                    if constexpr (UP) {
+                        const uint4 v = src[32 * q];
+                        PA[4 * q] = v.x; PA[4 * q + 1] = v.y; PA[4 * q + 2] = v.z; PA[4 * q + 3] = v.w;
+                    }
+                } else {
+                    const uint4 v = src[32 * q];
+                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        PA[4 * q + j] = w4[j] & 0x00FF00FFu;
+                        C[4 * q + j] = __byte_perm(w4[j], 0u, 0x4341);    // (C_lo, C_hi) as u16x2
+                    }
+                }
+            }
+        } else {
+            const int yrow = row_of(i);
+            const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q;
+            const uint32_t nbnb = (uint32_t)p.nb * 0x10001u;
+            if (!vx) {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) C[k] = nbnb;
+                return;
+            }
+            const uint32_t* sl = cenw + (i % DNSLOT) * CW;
+            const uint32_t clv = sl[col];
+            constexpr int SG = RR ? 1 : -1;
+            // element of local disparity j (d = chunk * DC + j) at row[SG * j]
+            const uint32_t* row = sl + 32 + chunk * SS + col + (RR ? 0 : DC - 1);
+            const int lim = RR ? (W - p.R - 1) - (x + p.min_disp + chunk * DC)
+                               : x - p.min_disp - p.R - chunk * DC;
+            if (lim >= DC - 1) {
+#pragma unroll
+                for (int k = 0; k < NR; ++k)
+                    C[k] = __byte_perm(__popc(clv ^ row[SG * k]), __popc(clv ^ row[SG * (NR + k)]), 0x5410);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    const uint32_t lo = k <= lim ? (uint32_t)__popc(clv ^ row[SG * k]) : (uint32_t)p.nb;
+                    const uint32_t hi = NR + k <= lim ? (uint32_t)__popc(clv ^ row[SG * (NR + k)]) : (uint32_t)p.nb;
+                    C[k] = __byte_perm(lo, hi, 0x5410);
+                }
+            }
+        }
+    };
+
+    // ---- halos (NP == 3): write targets of the edge lanes, fixed for the kernel
+    const int hslot = nw * T * NR;
+    uint32_t* wL = nullptr; uint32_t* wLm = nullptr;   // edge lane col == CPW-1 -> column x+1
+    uint32_t* wR = nullptr; uint32_t* wRm = nullptr;   // edge lane col == 0     -> column x-1
+    const bool recvL = NP == 3 && (warp > 0 || (clustered && rank > 0));
+    const bool recvR = NP == 3 && (warp < nw - 1 || (clustered && rank + 1 < a.cs));
+    const bool remoteL = clustered && warp == nw - 1 && rank + 1 < a.cs;   // I feed the next CTA
+    const bool remoteR = clustered && warp == 0 && rank > 0;               // I feed the previous CTA
+    uint32_t tgtL = 0, tgtR = 0;                     // the consumer's barrier, slot 0
+    if (NP == 3) {
+        cg::cluster_group cl_g = cg::this_cluster();
+        if (col == CPW - 1) {
+            if (warp + 1 < nw) { wL = hL + ((warp + 1) * T + chunk) * NR; wLm = hLM + warp + 1; }
+            else if (remoteL) { wL = cl_g.map_shared_rank(hL + chunk * NR, rank + 1); wLm = cl_g.map_shared_rank(hLM, rank + 1); }
+        }
+        if (col == 0) {
+            if (warp > 0) { wR = hR + ((warp - 1) * T + chunk) * NR; wRm = hRM + warp - 1; }
+            else if (remoteR) {
+                wR = cl_g.map_shared_rank(hR + ((nw - 1) * T + chunk) * NR, rank - 1);
+                wRm = cl_g.map_shared_rank(hRM + nw - 1, rank - 1);
+            }
+        }
+        if (recvR) tgtL = remoteL ? mapa_u32(hbL, (unsigned)(rank + 1)) : smem_u32(hbL + warp + 1);
+        if (recvL) tgtR = remoteR ? mapa_u32(hbR + nw - 1, (unsigned)(rank - 1)) : smem_u32(hbR + warp - 1);
+        for (int i = threadIdx.x; i < 4 * nw * T * NR + 4 * nw; i += blockDim.x) hL[i] = 0u;
+        if (threadIdx.x == 0) {
+            for (int s2 = 0; s2 < 4 * nw; ++s2) mbar_init(hb + s2, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (clustered) { cluster_arrive(); cluster_wait(); }   // neighbours' halos / barriers initialised
+    }
+
+    uint32_t Lv[NR], Ll[NR], Lr[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
+    uint32_t Mv = 0u, Ml = 0u, Mr = 0u;
+
+    for (int i0 = 0; i0 < DEPTH - 1; ++i0) stage(i0);
+    ready();
+    load_input(0);
+
+    for (int i = 0; i < H; ++i) {
+        const int y = row_of(i);
+        if (NP == 3) {
+            const int rs = (i + 1) & 1;                  // slot written at row i-1
+            if (i > 0) {
+                const unsigned ph = (unsigned)(((i - 1) >> 1) & 1);
+                if (recvL) { if (warp == 0) mbar_wait_remote(hbL + rs * nw + warp, ph); else mbar_wait(hbL + rs * nw + warp, ph); }
+                if (recvR) { if (warp == nw - 1) mbar_wait_remote(hbR + rs * nw + warp, ph); else mbar_wait(hbR + rs * nw + warp, ph); }
+                ASD_JITTER(2);
+            }
             uint32_t Pp[NR], Mp;
             // path "L": predecessor column x-1 (down-right / up-right)
 #pragma unroll
@@ -471,99 +902,77 @@ vsweep_kernel(VArgs a)
                 Mp = hRM[rs * nw + warp];
             }
             path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
-        }
-        // columns beyond the image act as "outside" predecessors: zero state
-        if (NP == 3 && !xin) {
+            if (!xin) {
 #pragma unroll
-            for (int k = 0; k < NR; ++k) { Ll[k] = 0u; Lr[k] = 0u; }
-            Ml = Mr = 0u;
-        }
-        // ---- halos for the next row (slot i & 1): written before the vertical
-        // path so the DSMEM stores are in flight while it runs
-        if (NP == 3) {
+                for (int k = 0; k < NR; ++k) { Ll[k] = 0u; Lr[k] = 0u; }
+                Ml = Mr = 0u;
+            }
+            // ---- halos of row i (slot i & 1) and the consumers' signals
             const int ws = i & 1;
             ASD_JITTER(3);
-            if (wL) {                        // my "L" state feeds column x+1 next row
+            if (wL) {
                 uint4* d4 = reinterpret_cast<uint4*>(wL + ws * hslot);
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]);
                 if (chunk == 0) wLm[ws * nw] = Ml;
             }
-            if (wR) {                        // my "R" state feeds column x-1 next row
+            if (wR) {
                 uint4* d4 = reinterpret_cast<uint4*>(wR + ws * hslot);
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
                 if (chunk == 0) wRm[ws * nw] = Mr;
             }
-        }
-        // ---- vertical path: predecessor = own column.  It reads no halo, so it
-        // runs either after the halo stores (in flight meanwhile) or, with
-        // VLATE, after the row's arrive, covering the cluster barrier.
-        auto vertical = [&]() {
-            if (!ABL(a, 32)) {
-                uint32_t Ln[NR], mnew;
-                path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
-#pragma unroll
-                for (int k = 0; k < NR; ++k) Lv[k] = Ln[k];
-                Mv = mnew;
+            if (remoteL || remoteR) fence_cluster();
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned off = (unsigned)(ws * nw * 8);
+                if (recvR) { if (remoteL) mbar_arrive_remote_relaxed(tgtL + off); else mbar_arrive_local(tgtL + off); }
+                if (recvL) { if (remoteR) mbar_arrive_remote_relaxed(tgtR + off); else mbar_arrive_local(tgtR + off); }
             }
-            if (!xin) {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) Lv[k] = 0u;
-                Mv = 0u;
-            }
-        };
-        if (!(VLATE && NP == 3)) vertical();
-        // ---- K_down: stage row i+5 (async), make row i+1's copies complete, publish
-        if (!RING) {
-            if (i + NSLOT - 1 < H) stage(row_of(i + NSLOT - 1), (i + NSLOT - 1) % NSLOT);
-            else cp_async_commit();                  // keep one group per row
-            cp_async_wait<NSLOT - 2>();
         }
-        arrive();
-        issue_row(i + KR);                            // ring input: row i's slot is free now
-        if (VLATE && NP == 3) vertical();
-        // ---- partial sum out (after the release so it does not wait on these stores)
-        if (!ABL(a, 2)) {
-            uint32_t s[NR];
+        // ---- vertical path: predecessor = own column
+        {
+            uint32_t Ln[NR], mnew;
+            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
 #pragma unroll
-            for (int k = 0; k < NR; ++k) s[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
+            for (int k = 0; k < NR; ++k) Lv[k] = xin ? Ln[k] : 0u;
+            Mv = xin ? mnew : 0u;
+        }
+        stage(i + DEPTH - 1);                            // into the slot row i-1 used
+        // ---- partial sum out
+        {
+            uint32_t sv[NR];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) sv[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
             if (!UP) {
-                // P_A (<= 255) | C << 8 (C <= 63): the up sweep needs no census
-                // (BLK: P_A alone, the up sweep reads CB itself)
                 uint4* dst = reinterpret_cast<uint4*>(a.pouta + frame * a.pa_stride +
                                                       ((long long)y * wpad + (x - col)) * D) + lane;
                 constexpr uint32_t CS = BLK ? 0u : 256u;
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q)
-                    dst[32 * q] = make_uint4(s[4 * q] + C[4 * q] * CS, s[4 * q + 1] + C[4 * q + 1] * CS,
-                                             s[4 * q + 2] + C[4 * q + 2] * CS, s[4 * q + 3] + C[4 * q + 3] * CS);
+                    dst[32 * q] = make_uint4(sv[4 * q] + C[4 * q] * CS, sv[4 * q + 1] + C[4 * q + 1] * CS,
+                                             sv[4 * q + 2] + C[4 * q + 2] * CS, sv[4 * q + 3] + C[4 * q + 3] * CS);
             } else {
-                // P_AB (<= 510) | C << 9: the right->left row sweep needs no census
 #pragma unroll
-                for (int k = 0; k < NR; ++k) s[k] += PA[k] + C[k] * (BLK ? 0u : 512u);
+                for (int k = 0; k < NR; ++k) sv[k] += PA[k] + C[k] * (BLK ? 0u : 512u);
                 uint32_t o[NR];
                 if (DPL_ROW == 4) {
 #pragma unroll
                     for (int g = 0; g < DC / 4; ++g) {
                         const int kk = 4 * g < NR ? 4 * g : 4 * g - NR;
                         const uint32_t sel = 4 * g < NR ? 0x5410u : 0x7632u;
-                        o[2 * g] = __byte_perm(s[kk], s[kk + 2], sel);
-                        o[2 * g + 1] = __byte_perm(s[kk + 1], s[kk + 3], sel);
+                        o[2 * g] = __byte_perm(sv[kk], sv[kk + 2], sel);
+                        o[2 * g + 1] = __byte_perm(sv[kk + 1], sv[kk + 3], sel);
                     }
                 } else {
 #pragma unroll
                     for (int g = 0; g < DC / 2; ++g) {
                         const int kk = 2 * g < NR ? 2 * g : 2 * g - NR;
                         const uint32_t sel = 2 * g < NR ? 0x5410u : 0x7632u;
-                        o[g] = __byte_perm(s[kk], s[kk + 1], sel);
+                        o[g] = __byte_perm(sv[kk], sv[kk + 1], sel);
                     }
                 }
-                // natural [x][d] layout through the warp's staging block.  16-byte
-                // piece p of the block (column p / PPC) is stored at p ^ (column &
-                // SWZ): without it the 32 lanes of one store instruction fall into
-                // two 16-byte bank groups (a 16-way conflict).
-                constexpr int PPC = DC * T / 8;                   // 16-byte pieces per column
+                constexpr int PPC = DC * T / 8;
                 constexpr int SWZ = (PPC < 8 ? PPC : 8) - 1;
                 uint4* sb = reinterpret_cast<uint4*>(stg);
                 const int pbase = col * PPC + chunk * (DC / 8);
@@ -574,21 +983,19 @@ vsweep_kernel(VArgs a)
                 uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + ((long long)y * W + (x - col)) * D);
 #pragma unroll
                 for (int q = 0; q < NR / 4; ++q) {
-                    const int pi = 32 * q + lane;                 // 16-byte piece of the block
+                    const int pi = 32 * q + lane;
                     if (x - col + pi / PPC < W) dst[pi] = sb[pi ^ ((pi / PPC) & SWZ)];
                 }
                 __syncwarp();
             }
         }
-        // ---- next row's cost while the barrier completes
-        if (i + 1 < H) {
-            if (RING) load_pin(i + 1, PA, C);
-            else cost(row_of(i + 1), (i + 1) % NSLOT, C);
-        }
+        if (i + 1 < H) { ready(); ASD_JITTER(5); load_input(i + 1); }
     }
-    wait();                                          // pairs with the last arrive
-    if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
+    cp_async_wait<0>();
+    if (clustered) { cluster_arrive(); cluster_wait(); }   // no CTA exits while a neighbour may still write it
 }
+
+#endif  // ASD_V2_DEC
 
 // ---------------------------------------------------------------- K_row
 struct RArgs {
@@ -1388,12 +1795,24 @@ using v2::RArgs;
 typedef void (*VKernel)(VArgs);
 typedef void (*RKernel)(RArgs);
 
+// the sweep kernel of this build: vsweep_dec_kernel (ASD_V2_DEC = 1, default)
+// or the round-1 barrier-per-row vsweep_kernel
+template <int DC, int T, int NP, bool UP, int DPL, bool RR = false, bool BLK = false>
+static VKernel vkern()
+{
+#if ASD_V2_DEC
+    return v2::vsweep_dec_kernel<DC, T, NP, UP, DPL, RR, BLK>;
+#else
+    return v2::vsweep_kernel<DC, T, NP, UP, DPL, RR, BLK>;
+#endif
+}
+
 template <int DC, int T, int DPL>
 static VKernel vk(int np, bool up, bool rr)
 {
-    if (up) return np == 3 ? v2::vsweep_kernel<DC, T, 3, true, DPL> : v2::vsweep_kernel<DC, T, 1, true, DPL>;
-    if (rr) return np == 3 ? v2::vsweep_kernel<DC, T, 3, false, DPL, true> : v2::vsweep_kernel<DC, T, 1, false, DPL, true>;
-    return np == 3 ? v2::vsweep_kernel<DC, T, 3, false, DPL> : v2::vsweep_kernel<DC, T, 1, false, DPL>;
+    if (up) return np == 3 ? vkern<DC, T, 3, true, DPL>() : vkern<DC, T, 1, true, DPL>();
+    if (rr) return np == 3 ? vkern<DC, T, 3, false, DPL, true>() : vkern<DC, T, 1, false, DPL, true>();
+    return np == 3 ? vkern<DC, T, 3, false, DPL>() : vkern<DC, T, 1, false, DPL>();
 }
 
 // rr: the K_down instance with the right view as reference (R2); blk: the SGBM
@@ -1403,17 +1822,19 @@ static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = f
     if (blk) {
         if (DC != 32 || T != 4 || DPL != 4) return nullptr;
         if (np == 3) {
-            if (up) return v2::vsweep_kernel<32, 4, 3, true, 4, false, true>;
-            return rr ? v2::vsweep_kernel<32, 4, 3, false, 4, true, true> : v2::vsweep_kernel<32, 4, 3, false, 4, false, true>;
+            if (up) return vkern<32, 4, 3, true, 4, false, true>();
+            return rr ? vkern<32, 4, 3, false, 4, true, true>() : vkern<32, 4, 3, false, 4, false, true>();
         }
-        if (up) return v2::vsweep_kernel<32, 4, 1, true, 4, false, true>;
-        return rr ? v2::vsweep_kernel<32, 4, 1, false, 4, true, true> : v2::vsweep_kernel<32, 4, 1, false, 4, false, true>;
+        if (up) return vkern<32, 4, 1, true, 4, false, true>();
+        return rr ? vkern<32, 4, 1, false, 4, true, true>() : vkern<32, 4, 1, false, 4, false, true>();
     }
     if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up, rr);
     if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr);
     if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up, rr);
     if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up, rr);
+#ifdef ASD_ABLATE
     if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up, rr);
+#endif
     return nullptr;
 }
 
@@ -1448,11 +1869,27 @@ static RKernel pick_wkernel(int D, bool wide = false, int mode = 0)
 static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up, bool blk = false)
 {
     const int nw = w * T / 32;
+    const bool ring = up || blk;
+    size_t words = 0;
+#if ASD_V2_DEC
+    {                                                 // vsweep_dec_kernel's layout
+        const int cpw = 32 / T, nsl = cpw + DC - 1;
+        const int ss = cpw + 32 * ((nsl - cpw + 31) / 32);
+        const int cw = 32 + T * ss, rw = cpw * D / 2;
+        const int nring = (up && blk) ? 2 : 1, kr = (up && blk) ? v2::DKR2 : v2::DKR;
+        if (!ring) words += (size_t)nw * v2::DNSLOT * cw;
+        if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
+        if (up) words += (size_t)nw * 16 * DC;
+        if (ring) words += (size_t)nw * nring * kr * rw;
+        words += 2 * (4 * (size_t)nw) + 2;            // halo mbarriers (+ align)
+        return words * 4;
+    }
+#endif
     const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
-    size_t words = (up || blk) ? 0 : (size_t)v2::NSLOT * ((size_t)w + (size_t)T * cstr);
-    if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
+    words = ring ? 0 : (size_t)v2::NSLOT * ((size_t)w + (size_t)T * cstr);
+    if (np == 3) words += 4 * (size_t)nw * T * (DC / 2 + 4) + 4 * (size_t)nw;   // halos (HS = NR + 4)
     words += (size_t)nw * 16 * DC;                    // K_up output staging
-    if (up || blk) {                                  // TMA ring(s) + mbarriers (+ align)
+    if (ring) {                                       // TMA ring(s) + mbarriers (+ align)
         const int kr = (up && blk) ? 2 : v2::KU, nring = (up && blk) ? 2 : 1;
         words += (size_t)nring * kr * w * D / 2 + 2 * kr + 4;
     }
@@ -1466,15 +1903,23 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     if (p.nb > 32) return no("nb > 32 (u64 census)");
     if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 128) return no("num_disp not in {16,32,64,128}");
     const int np = p.paths == 8 ? 3 : 1;
-    if (p.bw * p.bh > 1) {
+    // blk: the u16-partial instances (BLK) that read the matching cost from a
+    // cost buffer in the sweeps' private layout -- SGBM's block cost, or, for
+    // SGM whose 3-path partial exceeds 8 bits (3 (nb + P2) > 255), the 1 x 1
+    // "block" cost, i.e. the per-pixel Hamming cost.  wide: u32 WTA keys.
+    bool blk = p.bw * p.bh > 1, wide = blk;
+    if (blk) {
         // SGBM: u16 partials without cost bits (S <= 65534 validated by asd_create), u32 WTA keys
         if (p.D != 128) return no("SGBM on engine D3 needs num_disp = 128");
     } else {
-        if (np == 3 && 3 * (p.nb + p.p2) > 255) return no("3*(nb+p2) > 255 (u8 partial)");
+        if (np == 3 && 3 * (p.nb + p.p2) > 255) {
+            if (p.D != 128) return no("3*(nb+p2) > 255 (u16 partials need num_disp = 128)");
+            blk = wide = true;
+        }
         int ks = 1;
         while ((1 << ks) < p.D) ++ks;
         const long long smax = (long long)p.paths * (p.nb + p.p2);
-        if ((smax << ks) + (1 << ks) - 1 > 0xFFFE) return no("S << log2(D) exceeds 16-bit WTA keys");
+        if ((smax << ks) + (1 << ks) - 1 > 0xFFFE) wide = true;       // S << log2(D) exceeds 16-bit keys
     }
     pl.NP = np;
     pl.DPL = p.D <= 64 ? 2 : 4;
@@ -1488,7 +1933,6 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
 #endif
     const int T = pl.T, CPW = 32 / T;
     const int maxt = pl.DC == 32 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
-    const bool blk = p.bw * p.bh > 1;                // SGBM block cost (reading c19)
     pl.blk = blk;
     VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk);
     VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk);
@@ -1564,7 +2008,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
-    if (!wta2_plan(p, blk, pl)) return no("min_disp + num_disp too large for the WTA window");
+    if (!wta2_plan(p, wide, pl)) return no("min_disp + num_disp too large for the WTA window");
     pl.ok = true;
     return true;
 }

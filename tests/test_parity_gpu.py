@@ -117,3 +117,21 @@ def test_config_D_full_frame():
     and half a minute of oracle time)."""
     left, right, _ = synth.make_pair("D", 0)
     _run(_cfg("D"), left, right, 0)
+
+
+@pytest.mark.parametrize("p2", [40, 54, 60, 120, 224])
+def test_d3_envelope_p2(p2):
+    """Engine D3 beyond the 16-bit-key / 8-bit-partial envelope (the
+    parameters are adjustable): P2 = 40 and 54 need u32 WTA keys (8 (nb + P2)
+    << 7 > 0xFFFE); P2 >= 55 makes the 3-path partial exceed 8 bits, so the
+    sweeps run their u16-partial instances on the per-pixel cost (a 1 x 1 block
+    cost); 224 = the validated maximum (nb + P2 <= 255).  Every stage bit-exact
+    at a 320x96 D=128 8-path speckle pair, and on one full config-C frame at
+    P2 = 40 and 120."""
+    cfg = synth.StereoConfig("P", 320, 96, 128, 9, 7, 8, 430.0 * 320 / 424, tag=11)
+    left, right, _ = synth.speckle_pair(cfg, 0)
+    d = dict(cfg.params_dict(), p2=p2)
+    _run(d, left, right, 3)
+    if p2 in (40, 120):
+        left, right, _ = synth.make_pair("C", 1)
+        _run(_cfg("C", p2=p2), left, right, 3)
