@@ -59,7 +59,8 @@ struct V2Plan {
     int DPL, nbuf, bstride;
     size_t rsmem;
     bool wide;        // WTA keys in u32 (S may exceed 2^(16 - log2 D))
-    bool blk;         // SGBM: block-cost input, u16 partials without cost bits
+    bool blk;         // u16-partial instances on a cost buffer (SGBM block cost, or SGM with 3(nb+P2) > 255)
+    bool wta_fb;      // WTA by the warp-per-pixel kernel (the ring window does not fit, D = 256)
     char why[128];
 };
 bool v2_plan(const DevParams& p, int device, V2Plan& pl);

@@ -176,6 +176,22 @@ struct VArgs {
 #endif
 
 // ---------------------------------------------------------------- helpers
+// u16x2 minimum of N registers as a balanced tree (any N: each level folds the
+// upper ceil-half onto the lower half)
+template <int N>
+__device__ __forceinline__ uint32_t tree_min(const uint32_t (&v)[N])
+{
+    uint32_t tr[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) tr[k] = v[k];
+#pragma unroll
+    for (int n = N; n > 1; n = (n + 1) / 2) {
+#pragma unroll
+        for (int k = 0; k < n / 2; ++k) tr[k] = vmin2(tr[k], tr[k + (n + 1) / 2]);
+    }
+    return tr[0];
+}
+
 // Mp is the predecessor's min over d packed in both halves (M | M << 16);
 // mout returns the new one the same way, so no scalar->packed IMAD is needed
 // and the normalisation folds into one IADD3 per register.
@@ -206,15 +222,7 @@ __device__ __forceinline__ void path_update(const DevParams& p, int chunk, const
     }
     // min over the NR registers as a balanced tree (the asm min is opaque to the
     // compiler, so a running min would be a serial chain of NR dependent ops)
-    uint32_t tr[NR];
-#pragma unroll
-    for (int k = 0; k < NR; ++k) tr[k] = Ln[k];
-#pragma unroll
-    for (int h = NR / 2; h >= 1; h >>= 1) {
-#pragma unroll
-        for (int k = 0; k < h; ++k) tr[k] = vmin2(tr[k], tr[k + h]);
-    }
-    const uint32_t macc = tr[0];
+    const uint32_t macc = tree_min<NR>(Ln);
     uint32_t m = vmin2(macc, __byte_perm(macc, macc, 0x1032));      // (min, min)
 #pragma unroll
     for (int o = 1; o < T; o <<= 1) m = vmin2(m, __shfl_xor_sync(FULL, m, o));
@@ -232,6 +240,8 @@ template <int PPC>
 __device__ __forceinline__ int stg_swz(int pi)
 {
     if constexpr (PPC == 16) return pi ^ ((((pi >> 3) & 1) << 1) | ((pi >> 4) & 1));
+    else if constexpr (PPC == 32) return pi ^ ((pi >> 3) & 3);   // T = 8: a quarter = 1 column x 8 chunks
+    else if constexpr (PPC == 12) return pi;                     // D = 96: conflict-free as laid out
     else return pi ^ ((pi / PPC) & ((PPC < 8 ? PPC : 8) - 1));
 }
 
@@ -254,7 +264,9 @@ struct VGeom {
     static constexpr int NR = DC / 2;
     static constexpr int CPW = 32 / T;
     __host__ __device__ static int cstride(int w) { return ((w + DC - 1 + 31) / 32) * 32 + 32; }
-    __host__ __device__ static int coff(int k) { return (k * (DC + 32 / T)) & 31; }
+    // chunk k's right-census slice starts at bank k * CPW: the T chunks of a
+    // column read distinct banks
+    __host__ __device__ static int coff(int k) { return (k * (32 / T)) & 31; }
     __host__ __device__ static int slot_words(int w) { return w + T * cstride(w); }
 };
 
@@ -271,7 +283,7 @@ struct VGeom {
 constexpr bool DEC = ASD_V2_DEC;
 
 template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
-__global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
+__global__ void __launch_bounds__(DC >= 24 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
 {
     using G = VGeom<DC, T>;
@@ -565,7 +577,17 @@ vsweep_kernel(VArgs a)
 #pragma unroll
             for (int k = 0; k < NR; ++k) s[k] += PA[k] + C[k] * (BLK ? 0u : 512u);
             uint32_t o[NR];
-            if (DPL_ROW == 4) {
+            if (DPL_ROW == 8) {
+                // row-kernel register order for 8 disparities per lane: word j of
+                // group g = (d 8g+j, d 8g+4+j)
+#pragma unroll
+                for (int g = 0; g < DC / 8; ++g) {
+                    const int kk = 8 * g < NR ? 8 * g : 8 * g - NR;
+                    const uint32_t sel = 8 * g < NR ? 0x5410u : 0x7632u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) o[4 * g + j] = __byte_perm(s[kk + j], s[kk + 4 + j], sel);
+                }
+            } else if (DPL_ROW == 4) {
 #pragma unroll
                 for (int g = 0; g < DC / 4; ++g) {
                     const int kk = 4 * g < NR ? 4 * g : 4 * g - NR;
@@ -1044,7 +1066,7 @@ constexpr int WTA_PAD = ASD_WTA_PAD;      // u16 of padding per window row
 constexpr int WTA_CHUNK = ASD_WTA_CHUNK;  // bytes per cp.async of the window fill
 
 template <int D> struct RowGeom {
-    static constexpr int DPL = D == 128 ? 4 : 2;     // disparities per lane
+    static constexpr int DPL = D > 128 ? 8 : D > 64 ? 4 : 2;   // disparities per lane
     static constexpr int NRR = DPL / 2;              // u16x2 registers per lane
     static constexpr int ACT = D / DPL;              // active lanes
     static constexpr int NB = D + 40;                // rows of the S window (D + 32 + one sub-group)
@@ -1058,11 +1080,53 @@ template <int D> struct RowGeom {
 // Pass 1: packed u16 keys (S << KS) | d, u16x2 min.  Pass 2: min of S with
 // d*-1..d*+1 poisoned (the row belongs to this lane alone), then restored.
 // WIDE: S may exceed 2^(16 - KS) (SGBM block costs, D1 volumes): u32 keys.
+#ifndef ASD_HROW_CFROMP
+#define ASD_HROW_CFROMP 0         // 1: the row kernel's left->right pass takes C from the P_AB | C words
+#endif
+#ifndef ASD_HROW_PF
+#define ASD_HROW_PF 0             // > 0: L2 bulk prefetch this many pixels ahead in the right->left pass
+#endif
+#ifndef ASD_WTA_LBM
+#define ASD_WTA_LBM 0             // 1: left view second-best from 8-disparity block minima (one pass)
+#endif
 template <int D, bool WIDE>
 __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, int& dstar, bool& uf, float& disp)
 {
     constexpr int KS = RowGeom<D>::KS;
     const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);     // rows are 4-byte aligned
+    if constexpr (ASD_WTA_LBM && !WIDE && D % 8 == 0) {
+        // one pass: packed keys and the minimum S of each 8-disparity block;
+        // the second best over |d - d*| >= 2 from the blocks clear of
+        // d*-1..d*+1 and, element by element, the (one or two) blocks holding them
+        uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu, bm[D / 8];
+#pragma unroll
+        for (int q = 0; q < D; q += 4) {
+            const uint32_t v0 = r32[q / 2], v1 = r32[q / 2 + 1];
+            ka = vmin2(ka, v0 * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
+            kb2 = vmin2(kb2, v1 * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
+            bm[q / 8] = (q % 8 == 0) ? vmin2(v0, v1) : vmin2(bm[q / 8], vmin2(v0, v1));
+        }
+        const uint32_t kmin = vmin2(ka, kb2);
+        const uint32_t kk = min(kmin & 0xFFFFu, kmin >> 16);
+        dstar = (int)(kk & ((1u << KS) - 1u));
+        const uint32_t s0 = kk >> KS;
+        const uint32_t cm = dstar >= 1 ? r[dstar - 1] : NONE16;
+        const uint32_t cp = dstar + 1 < D ? r[dstar + 1] : NONE16;
+        const int blo = max(dstar - 1, 0) >> 3, bhi = min(dstar + 1, D - 1) >> 3;
+        uint32_t sec = 0xFFFFFFFFu;
+#pragma unroll
+        for (int b = 0; b < D / 8; ++b)
+            if (b < blo || b > bhi) sec = vmin2(sec, bm[b]);
+        uint32_t s2 = min(sec & 0xFFFFu, sec >> 16);
+        for (int b = blo; b <= bhi; ++b)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int d = 8 * b + j;
+                if (d < dstar - 1 || d > dstar + 1) s2 = min(s2, (uint32_t)r[d]);
+            }
+        finish_wta(p, dstar, s0, s2, cm, cp, uf, disp);
+        return;
+    }
     uint32_t kb;
     if constexpr (WIDE) {
         uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
@@ -1239,7 +1303,7 @@ __device__ __forceinline__ void row_cost(const DevParams& p, int lane, uint32_t 
                                          const uint32_t (&wnd)[RowGeom<D>::DPL],
                                          uint32_t (&C)[RowGeom<D>::NRR])
 {
-    constexpr int DPL = RowGeom<D>::DPL;
+    constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR;
     const int d0 = lane * DPL;
     uint32_t c[DPL];
     if (FAST || (vx && lim >= D - 1)) {               // warp-uniform fast path: all d valid
@@ -1249,12 +1313,9 @@ __device__ __forceinline__ void row_cost(const DevParams& p, int lane, uint32_t 
 #pragma unroll
         for (int j = 0; j < DPL; ++j) c[j] = (vx && d0 + j <= lim) ? (uint32_t)__popc(clv ^ wnd[j]) : (uint32_t)p.nb;
     }
-    if constexpr (DPL == 4) {
-        C[0] = __byte_perm(c[0], c[2], 0x5410);
-        C[1] = __byte_perm(c[1], c[3], 0x5410);
-    } else {
-        C[0] = __byte_perm(c[0], c[1], 0x5410);
-    }
+    // register k = (d0 + k, d0 + NRR + k)
+#pragma unroll
+    for (int k = 0; k < NRR; ++k) C[k] = __byte_perm(c[k], c[NRR + k], 0x5410);
 }
 
 // row_rec: L_r(x) from the predecessor state Lp (zero at the line start) and
@@ -1272,34 +1333,27 @@ __device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, uint32
                                             const uint32_t (&Lp)[RowGeom<D>::NRR], uint32_t Mpk,
                                             uint32_t (&Ln)[RowGeom<D>::NRR])
 {
-    constexpr int DPL = RowGeom<D>::DPL, NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
+    constexpr int NRR = RowGeom<D>::NRR, ACT = RowGeom<D>::ACT;
     const int lane = threadIdx.x & 31;
     const uint32_t MP2 = Mpk + p2x2;
-    uint32_t mm;
-    if constexpr (DPL == 4) {
-        const uint32_t QA = Lp[0] + p1x2, QB = Lp[NRR - 1] + p1x2;
-        const uint32_t prevB = __shfl_up_sync(FULL, QB, 1) | eprev;
-        const uint32_t nextA = __shfl_down_sync(FULL, QA, 1) | enext;
-        const uint32_t dm1A = __byte_perm(prevB, QB, 0x5432);
-        const uint32_t dp1B = __byte_perm(QA, nextA, 0x5432);
-        uint32_t tA = vmin2(vmin2(dm1A, QB), Lp[0]);
-        uint32_t tB = vmin2(vmin2(QA, dp1B), Lp[NRR - 1]);
-        tA = vmin2(tA, MP2);
-        tB = vmin2(tB, MP2);
-        Ln[0] = tA + C[0] - Mpk;
-        Ln[NRR - 1] = tB + C[NRR - 1] - Mpk;
-        mm = vmin2(Ln[0], Ln[NRR - 1]);
-    } else {
-        const uint32_t Q = Lp[0] + p1x2;
-        const uint32_t prev = __shfl_up_sync(FULL, Q, 1) | eprev;
-        const uint32_t next = __shfl_down_sync(FULL, Q, 1) | enext;
-        const uint32_t dm1 = __byte_perm(prev, Q, 0x5432);
-        const uint32_t dp1 = __byte_perm(Q, next, 0x5432);
-        uint32_t t = vmin2(vmin2(dm1, dp1), Lp[0]);
+    // register k = (d0 + k, d0 + NRR + k): d-1 / d+1 are the neighbouring
+    // registers; at k = 0 the low half's d-1 is the previous lane's last
+    // register's high half, at k = NRR-1 the high half's d+1 is the next lane's
+    // first register's low half
+    uint32_t Q[NRR];
+#pragma unroll
+    for (int k = 0; k < NRR; ++k) Q[k] = Lp[k] + p1x2;
+    const uint32_t prevB = __shfl_up_sync(FULL, Q[NRR - 1], 1) | eprev;
+    const uint32_t nextA = __shfl_down_sync(FULL, Q[0], 1) | enext;
+#pragma unroll
+    for (int k = 0; k < NRR; ++k) {
+        const uint32_t dm1 = k > 0 ? Q[k - 1] : __byte_perm(prevB, Q[NRR - 1], 0x5432);
+        const uint32_t dp1 = k < NRR - 1 ? Q[k + 1] : __byte_perm(Q[0], nextA, 0x5432);
+        uint32_t t = vmin2(vmin2(dm1, dp1), Lp[k]);
         t = vmin2(t, MP2);
-        Ln[0] = t + C[0] - Mpk;
-        mm = Ln[0];
+        Ln[k] = t + C[k] - Mpk;
     }
+    const uint32_t mm = tree_min<NRR>(Ln);
     uint32_t m2 = vmin2(mm, __byte_perm(mm, mm, 0x1032));          // (min, min)
     if (ACT < 32 && lane >= ACT) m2 = 0xFFFFFFFFu;
     return __reduce_min_sync(FULL, m2);
@@ -1312,6 +1366,54 @@ __device__ __forceinline__ uint32_t row_rec(uint32_t p1x2, uint32_t p2x2, int la
                                             uint32_t (&Ln)[RowGeom<D>::NRR])
 {
     return row_rec<D>(p1x2, p2x2, lane == 0 ? INF2 : 0u, lane == RowGeom<D>::ACT - 1 ? INF2 : 0u, C, Lp, Mpk, Ln);
+}
+
+// Per-lane vectors of the row kernel in register order (register k = (d0 + k,
+// d0 + NRR + k)): the P_AB | C words K_up writes in that order (NRR words), the
+// u8 left->right stash (register k's two bytes at 2k, 2k + 1) and the S vector
+// written in natural d order for the WTA kernel.
+template <int NRR>
+__device__ __forceinline__ void ld_words(const uint16_t* src, uint32_t (&v)[NRR])
+{
+    if constexpr (NRR == 4) { const uint4 u = *reinterpret_cast<const uint4*>(src); v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; }
+    else if constexpr (NRR == 2) { const uint2 u = *reinterpret_cast<const uint2*>(src); v[0] = u.x; v[1] = u.y; }
+    else v[0] = *reinterpret_cast<const uint32_t*>(src);
+}
+template <int NRR> struct StashW { static constexpr int N = NRR >= 2 ? NRR / 2 : 1; };   // stash words per lane
+template <int NRR>
+__device__ __forceinline__ void st_stash(uint8_t* dst, const uint32_t (&Ln)[NRR])
+{
+    if constexpr (NRR == 4)
+        *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(Ln[0], Ln[1], 0x6420), __byte_perm(Ln[2], Ln[3], 0x6420));
+    else if constexpr (NRR == 2) *reinterpret_cast<uint32_t*>(dst) = __byte_perm(Ln[0], Ln[1], 0x6420);
+    else *reinterpret_cast<uint16_t*>(dst) = (uint16_t)__byte_perm(Ln[0], 0u, 0x4420);
+}
+template <int NRR>
+__device__ __forceinline__ void ld_stash(const uint8_t* src, uint32_t (&w)[StashW<NRR>::N])
+{
+    if constexpr (NRR == 4) { const uint2 u = *reinterpret_cast<const uint2*>(src); w[0] = u.x; w[1] = u.y; }
+    else if constexpr (NRR == 2) w[0] = *reinterpret_cast<const uint32_t*>(src);
+    else w[0] = *reinterpret_cast<const uint16_t*>(src);
+}
+// register k of the stash as u16x2
+template <int NRR>
+__device__ __forceinline__ uint32_t stash_reg(const uint32_t (&w)[StashW<NRR>::N], int k)
+{
+    return __byte_perm(w[k / 2], 0u, (k & 1) ? 0x4342 : 0x4140);
+}
+template <int NRR>
+__device__ __forceinline__ void st_natural(uint16_t* dst, const uint32_t (&sv)[NRR])
+{
+    if constexpr (NRR == 1) *reinterpret_cast<uint32_t*>(dst) = sv[0];
+    else {
+        uint32_t o[NRR];
+#pragma unroll
+        for (int j = 0; j < NRR; ++j)
+            o[j] = 2 * j < NRR ? __byte_perm(sv[2 * j], sv[2 * j + 1], 0x5410)
+                               : __byte_perm(sv[2 * j - NRR], sv[2 * j - NRR + 1], 0x7632);
+        if constexpr (NRR == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+        else *reinterpret_cast<uint2*>(dst) = make_uint2(o[0], o[1]);
+    }
 }
 
 // ---------------------------------------------------------------- K_row
@@ -1372,12 +1474,7 @@ hrow_kernel(RArgs a)
             for (int k = 0; k < SG; ++k) {
                 const int x = xb + k;
                 if (x < W && active) {
-                    if constexpr (DPL == 4) {
-                        const uint2 u = *reinterpret_cast<const uint2*>(pab + (long long)x * D);
-                        PP[k][0] = u.x; PP[k][NRR - 1] = u.y;
-                    } else {
-                        PP[k][0] = *reinterpret_cast<const uint32_t*>(pab + (long long)x * D);
-                    }
+                    ld_words<NRR>(pab + (long long)x * D, PP[k]);
                 } else {
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) PP[k][r] = 0u;
@@ -1395,12 +1492,7 @@ hrow_kernel(RArgs a)
                     M = row_rec<D>(a.p1x2, a.p2x2, eprev, enext, Cc, L, M, Ln);
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                    if (active) {
-                        if constexpr (DPL == 4)
-                            *reinterpret_cast<uint32_t*>(stash + (long long)x * D) = __byte_perm(Ln[0], Ln[NRR - 1], 0x6420);
-                        else
-                            *reinterpret_cast<uint16_t*>(stash + (long long)x * D) = (uint16_t)__byte_perm(Ln[0], 0u, 0x4420);
-                    }
+                    if (active) st_stash<NRR>(stash + (long long)x * D, Ln);
                 }
             }
         };
@@ -1443,12 +1535,7 @@ hrow_kernel(RArgs a)
                             M = row_rec<D>(a.p1x2, a.p2x2, eprev, enext, Cc, L, M, Ln);
 #pragma unroll
                             for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
-                            if (active) {
-                                if constexpr (DPL == 4)
-                                    *reinterpret_cast<uint32_t*>(stash + (long long)x * D) = __byte_perm(Ln[0], Ln[NRR - 1], 0x6420);
-                                else
-                                    *reinterpret_cast<uint16_t*>(stash + (long long)x * D) = (uint16_t)__byte_perm(Ln[0], 0u, 0x4420);
-                            }
+                            if (active) st_stash<NRR>(stash + (long long)x * D, Ln);
                             const uint32_t in = __shfl_up_sync(FULL, wnd[DPL - 1], 1);
 #pragma unroll
                             for (int q = DPL - 1; q > 0; --q) wnd[q] = wnd[q - 1];
@@ -1469,25 +1556,21 @@ hrow_kernel(RArgs a)
 #pragma unroll
         for (int k = 0; k < NRR; ++k) L[k] = 0u;
         uint32_t M = 0u;
-        uint32_t P[SG][NRR], Sx[SG], Pn[SG][NRR], Sn[SG];
-        auto load_sg = [&](int xb8, uint32_t (&PP)[SG][NRR], uint32_t (&SS)[SG]) {
+        constexpr int SW = StashW<NRR>::N;
+        uint32_t P[SG][NRR], Sx[SG][SW], Pn[SG][NRR], Sn[SG][SW];
+        auto load_sg = [&](int xb8, uint32_t (&PP)[SG][NRR], uint32_t (&SS)[SG][SW]) {
 #pragma unroll
             for (int k = 0; k < SG; ++k) {
                 const int x = xb8 + k;
                 if (x >= 0 && x < W && active) {
                     const long long off = (long long)x * D;
-                    if constexpr (DPL == 4) {
-                        const uint2 u = *reinterpret_cast<const uint2*>(pab + off);
-                        PP[k][0] = u.x; PP[k][NRR - 1] = u.y;
-                        SS[k] = *reinterpret_cast<const uint32_t*>(stash + off);
-                    } else {
-                        PP[k][0] = *reinterpret_cast<const uint32_t*>(pab + off);
-                        SS[k] = *reinterpret_cast<const uint16_t*>(stash + off);
-                    }
+                    ld_words<NRR>(pab + off, PP[k]);
+                    ld_stash<NRR>(stash + off, SS[k]);
                 } else {
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) PP[k][r] = 0u;
-                    SS[k] = 0u;
+#pragma unroll
+                    for (int r = 0; r < SW; ++r) SS[k][r] = 0u;
                 }
             }
         };
@@ -1499,7 +1582,7 @@ hrow_kernel(RArgs a)
         };
         // whole: all SG pixels inside the row (called with a literal, so each
         // call site inlines its own copy without the per-pixel bound test)
-        auto group = [&](const bool whole, int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG]) {
+        auto group = [&](const bool whole, int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG][SW]) {
 #pragma unroll
             for (int k = SG - 1; k >= 0; --k) {
                 const int x = xs + k;
@@ -1514,26 +1597,39 @@ hrow_kernel(RArgs a)
 #pragma unroll
                     for (int r = 0; r < NRR; ++r) L[r] = Ln[r];
                     if (active) {
-                        if constexpr (DPL == 4) {
-                            const uint32_t s0 = Pv[0] + __byte_perm(SS[k], 0u, 0x4140) + Ln[0];
-                            const uint32_t s1 = Pv[NRR - 1] + __byte_perm(SS[k], 0u, 0x4342) + Ln[NRR - 1];
-                            *reinterpret_cast<uint2*>(svec(x)) =
-                                make_uint2(__byte_perm(s0, s1, 0x5410), __byte_perm(s0, s1, 0x7632));
-                        } else {
-                            *reinterpret_cast<uint32_t*>(svec(x)) =
-                                Pv[0] + __byte_perm(SS[k], 0u, 0x4140) + Ln[0];
-                        }
+                        uint32_t sv[NRR];
+#pragma unroll
+                        for (int r = 0; r < NRR; ++r) sv[r] = Pv[r] + stash_reg<NRR>(SS[k], r) + Ln[r];
+                        st_natural<NRR>(svec(x), sv);
                     }
                 }
             }
         };
         // ping-pong between the two buffer sets (no register copies)
-        auto run_group = [&](int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG]) {
+        auto run_group = [&](int xs, const uint32_t (&PP)[SG][NRR], const uint32_t (&SS)[SG][SW]) {
             if (xs + SG <= W) group(true, xs, PP, SS);
             else group(false, xs, PP, SS);
         };
+        // bulk L2 prefetch (one lane, TMA unit) of the P_AB | C words and the
+        // stash of the 2 SG pixels ASD_HROW_PF pixels ahead of the sweep
+        const uint16_t* pab_row = a.pab + frame * a.cell_stride + (long long)y * W * D;
+        const uint8_t* st_row = a.stash + frame * a.cell_stride + (long long)y * W * D;
+        auto prefetch = [&](int xs) {
+            if (ASD_HROW_PF > 0 && lane == 0) {
+                const int hi = xs - ASD_HROW_PF + SG, lo = max(hi - 2 * SG, 0);   // pixels [lo, hi)
+                if (hi > lo) {
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n"
+                                 :: "l"(pab_row + (long long)lo * D), "r"((unsigned)((hi - lo) * D * 2)) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n"
+                                 :: "l"(st_row + (long long)lo * D), "r"((unsigned)((hi - lo) * D)) : "memory");
+                }
+            }
+        };
+        if (ASD_HROW_PF > 0 && lane == 0)
+            for (int xs = xtop; xs > xtop - ASD_HROW_PF && xs >= 0; xs -= 2 * SG) prefetch(xs + ASD_HROW_PF);
         load_sg(xtop, P, Sx);
         for (int xs = xtop; xs >= 0; xs -= 2 * SG) {
+            prefetch(xs);
             load_sg(xs - SG, Pn, Sn);
             run_group(xs, P, Sx);
             if (xs - SG < 0) break;
@@ -1832,6 +1928,8 @@ static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = f
     if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr);
     if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up, rr);
     if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up, rr);
+    if (DC == 24 && T == 4 && DPL == 4) return vk<24, 4, 4>(np, up, rr);     // D = 96
+    if (DC == 32 && T == 8 && DPL == 8) return vk<32, 8, 8>(np, up, rr);     // D = 256
 #ifdef ASD_ABLATE
     if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up, rr);
 #endif
@@ -1844,6 +1942,8 @@ static RKernel pick_rkernel(int D, bool cfromp = false)
     if (D == 32) return cfromp ? v2::hrow_kernel<32, true> : v2::hrow_kernel<32, false>;
     if (D == 64) return cfromp ? v2::hrow_kernel<64, true> : v2::hrow_kernel<64, false>;
     if (D == 128) return cfromp ? v2::hrow_kernel<128, true> : v2::hrow_kernel<128, false>;
+    if (D == 96) return cfromp ? v2::hrow_kernel<96, true> : v2::hrow_kernel<96, false>;
+    if (D == 256) return cfromp ? v2::hrow_kernel<256, true> : v2::hrow_kernel<256, false>;
     return nullptr;
 }
 
@@ -1901,7 +2001,8 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     pl = V2Plan{};
     auto no = [&](const char* why) { snprintf(pl.why, sizeof pl.why, "%s", why); pl.ok = false; return false; };
     if (p.nb > 32) return no("nb > 32 (u64 census)");
-    if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 128) return no("num_disp not in {16,32,64,128}");
+    if (p.D != 16 && p.D != 32 && p.D != 64 && p.D != 96 && p.D != 128 && p.D != 256)
+        return no("num_disp not in {16,32,64,96,128,256}");
     const int np = p.paths == 8 ? 3 : 1;
     // blk: the u16-partial instances (BLK) that read the matching cost from a
     // cost buffer in the sweeps' private layout -- SGBM's block cost, or, for
@@ -1922,8 +2023,10 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         if ((smax << ks) + (1 << ks) - 1 > 0xFFFE) wide = true;       // S << log2(D) exceeds 16-bit keys
     }
     pl.NP = np;
-    pl.DPL = p.D <= 64 ? 2 : 4;
+    pl.DPL = p.D <= 64 ? 2 : p.D <= 128 ? 4 : 8;
     if (p.D == 16) { pl.DC = 16; pl.T = 1; }
+    else if (p.D == 96) { pl.DC = 24; pl.T = 4; }
+    else if (p.D == 256) { pl.DC = 32; pl.T = 8; }
     else if (p.D == 32) { pl.DC = 32; pl.T = 1; }
     else if (p.D == 64) { pl.DC = 32; pl.T = 2; }
     else { pl.DC = 32; pl.T = 4; }
@@ -1932,7 +2035,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     if (p.D == 128 && force && force[0] == '1') { pl.DC = 16; pl.T = 8; }
 #endif
     const int T = pl.T, CPW = 32 / T;
-    const int maxt = pl.DC == 32 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
+    const int maxt = pl.DC >= 24 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
     pl.blk = blk;
     VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk);
     VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk);
@@ -2008,7 +2111,14 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
-    if (!wta2_plan(p, wide, pl)) return no("min_disp + num_disp too large for the WTA window");
+    pl.wta_fb = false;
+    if (!wta2_plan(p, wide, pl)) {
+        // the window does not fit shared memory (D = 256): the warp-per-pixel
+        // WTA kernel of engine D1 (post.cu) reads the same natural-order S
+        if (p.lr_mode == 1) return no("min_disp + num_disp too large for the WTA window (R2)");
+        pl.wta_fb = true;
+        pl.wide = wide;
+    }
     pl.ok = true;
     return true;
 }
@@ -2084,13 +2194,17 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.p2x2 = (uint32_t)p.p2 * 0x10001u;
     r.cb = cbin; r.cb_stride = (long long)p.H * pl.cs * pl.w * p.D; r.wpad = pl.cs * pl.w;
     if (stage == 2) {
-        RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1);
+        RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1 || ASD_HROW_CFROMP);
         const int hsm = pl.blk ? 0 : ASD_HROW_SMEM;
         if (hsm > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, hsm, s>>>(r);
     } else {
-        RKernel k = pick_wkernel(p.D, pl.wide, variant);
-        k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
+        if (pl.wta_fb) {
+            if (!launch_wta(p, nframes, pab, cell_stride, fs, px_stride, s)) return -1;
+        } else {
+            RKernel k = pick_wkernel(p.D, pl.wide, variant);
+            k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
+        }
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

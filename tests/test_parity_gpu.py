@@ -135,3 +135,16 @@ def test_d3_envelope_p2(p2):
     if p2 in (40, 120):
         left, right, _ = synth.make_pair("C", 1)
         _run(_cfg("C", p2=p2), left, right, 3)
+
+
+@pytest.mark.parametrize("W,H,D,paths", [(320, 96, 96, 8), (320, 96, 96, 4), (512, 96, 256, 8),
+                                         (600, 80, 256, 4), (1000, 40, 256, 8)])
+def test_d3_more_disparity_ranges(W, H, D, paths):
+    """Engine D3 at D = 96 (DC = 24 disparities per thread, T = 4) and D = 256
+    (T = 8 threads per column, 8 disparities per lane in the row kernel, the
+    warp-per-pixel WTA): Table II's other disparity ranges and
+    P:293's adjustable parameters.  8-path D = 256 needs the frame in one
+    cluster of <= 16 CTAs of 64 columns (W <= 1024).  Every stage bit-exact."""
+    cfg = synth.StereoConfig("R", W, H, D, 9, 7, paths, 430.0 * W / 424 * D / 128, tag=12)
+    left, right, _ = synth.speckle_pair(cfg, 0)
+    _run(cfg.params_dict(), left, right, 3)
