@@ -308,6 +308,10 @@ static double alg_ops_wta3(const DevParams& p) { return 3.0 * p.ncell; }
 int set_group(asd_ctx* c, int group)
 {
     if (group < 1 || group > c->max_batch) return ASD_E_INVALID_ARG;
+    // frames split over several clusters need all of a group's clusters
+    // resident at once (their boundary columns wait on each other): at most one wave
+    if (c->engine == ASD_ENGINE_D3 && c->plan.ncta > c->plan.cs &&
+        group > c->plan.active_ctas / c->plan.ncta) return ASD_E_INVALID_ARG;
     for (cudaEvent_t e : c->ev_free) if (e) cudaEventDestroy(e);
     c->ev_free.assign(c->engine == ASD_ENGINE_D3 ? c->max_batch / group : 0, nullptr);
     for (cudaEvent_t& e : c->ev_free)
@@ -350,9 +354,9 @@ int run_d3(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
     const int G = c->group;
     const int nslots = (int)c->ev_free.size();
     const int ngroups = (n + G - 1) / G;
-    const long long pa_frame = (long long)p.H * c->plan.cs * c->plan.w * p.D;   // u16 elements
+    const long long pa_frame = (long long)p.H * c->plan.ncta * c->plan.w * p.D;   // u16 elements
     const bool blk = c->cb != nullptr;             // SGBM: block cost in the private layout
-    const int wpad = c->plan.cs * c->plan.w;
+    const int wpad = c->plan.ncta * c->plan.w;
     struct Slot { void* cl; void* cr; uint8_t* pa; uint16_t* pab; uint8_t* stash; uint16_t* cb; uint16_t* cb2;
                   uint8_t* pa2; uint16_t* pab2; uint8_t* stash2; FrameScratch g; };
     const bool r2 = c->pa2 != nullptr;             // R2: a right-referenced second pass (c24)
@@ -585,7 +589,8 @@ void free_ctx(asd_ctx* c)
 {
     if (!c) return;
     void* ptrs[] = {c->census_l, c->census_r, c->S, c->SR, c->cb, c->cb2, c->dl, c->dr, c->dstar_l, c->dstar_r,
-                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->stage_in[0], c->stage_in[1], c->stage_out[0],
+                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->plan.gflag, c->plan.ghalo,
+                    c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
     for (int i = 0; i < 2; ++i) {
@@ -631,7 +636,9 @@ size_t asd_scratch_bytes(const asd_params* p, int max_batch)
         int dev = 0;
         cudaGetDevice(&dev);
         V2Plan pl;
-        if (v2_plan(d, dev, pl)) return layout(d, max_batch, ASD_ENGINE_D3, pl.cs * pl.w, pl.blk).total;
+        if (v2_plan(d, dev, pl))
+            return layout(d, max_batch, ASD_ENGINE_D3, pl.ncta * pl.w, pl.blk).total +
+                   v2_gflag_bytes(pl, max_batch) + v2_ghalo_bytes(pl, max_batch);
         cudaGetLastError();
     }
     return layout(d, max_batch, engine, d.W).total;
@@ -680,7 +687,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         if (wta2_plan(c->dp, smax >= (1ll << (16 - ks)), c->plan)) c->wta2 = true;
     }
     Layout L = layout(c->dp, max_batch, c->engine,
-                      c->engine == ASD_ENGINE_D3 ? c->plan.cs * c->plan.w : c->dp.W,
+                      c->engine == ASD_ENGINE_D3 ? c->plan.ncta * c->plan.w : c->dp.W,
                       c->engine == ASD_ENGINE_D3 && c->plan.blk);
     bool ok = true;
     auto alloc = [&](void** q, size_t bytes) {
@@ -703,6 +710,10 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         alloc((void**)&c->pa2, L.pa);
         alloc((void**)&c->pab2, L.pab);
         alloc((void**)&c->stash2, L.stash);
+    }
+    if (c->engine == ASD_ENGINE_D3 && v2_gflag_bytes(c->plan, max_batch) > 0) {
+        alloc((void**)&c->plan.gflag, v2_gflag_bytes(c->plan, max_batch));
+        alloc((void**)&c->plan.ghalo, v2_ghalo_bytes(c->plan, max_batch));
     }
     alloc((void**)&c->dl, L.px_f32); alloc((void**)&c->dr, L.px_f32);
     alloc((void**)&c->dstar_l, L.px_i16); alloc((void**)&c->dstar_r, L.px_i16);
@@ -729,7 +740,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         for (cudaEvent_t* e : {&c->ev_fork, &c->ev_sw, &c->ev_sw2, &c->ev_hi, &c->ev_lo, &c->ev_cen})
             if (ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) ok = false;
         // overlap group: one wave of sweep clusters, at most max_batch
-        const int wave = c->plan.cs > 0 ? c->plan.active_ctas / c->plan.cs : 1;
+        const int wave = c->plan.ncta > 0 ? c->plan.active_ctas / c->plan.ncta : 1;
         if (ok && set_group(c, wave < 1 ? 1 : wave > max_batch ? max_batch : wave) != ASD_OK) ok = false;
     }
     for (int i = 0; i < 2 && ok; ++i)
@@ -790,16 +801,16 @@ int asd_plan_info(const asd_ctx* ctx, char* buf, int n)
         return snprintf(buf, n, "engine D1: %d direction kernels (warp per line), WTA kernel", ctx->dp.paths);
     const V2Plan& q = ctx->plan;
     return snprintf(buf, n,
-                    "engine D3: sweeps DC=%d T=%d paths/sweep=%d cluster=%d CTA=%d cols x %d thr, "
-                    "%d resident CTAs (%d frames/wave), smem %zu B; WTA ring %d rows",
-                    q.DC, q.T, q.NP, q.cs, q.w, q.vthreads, q.active_ctas,
-                    q.NP == 3 ? q.active_ctas / q.cs : 0, q.vsmem, q.nbuf);
+                    "engine D3: sweeps DC=%d T=%d paths/sweep=%d cluster=%d x %d per frame, CTA=%d cols x %d thr, "
+                    "%d resident CTAs (%d frames/wave), smem %zu B; WTA %s %d rows",
+                    q.DC, q.T, q.NP, q.cs, q.NP == 3 ? q.ncta / q.cs : 1, q.w, q.vthreads, q.active_ctas,
+                    q.NP == 3 ? q.active_ctas / q.ncta : 0, q.vsmem, q.wta_fb ? "warp-per-pixel (no ring)" : "ring", q.nbuf);
 }
 
 int asd_frames_per_wave(const asd_ctx* ctx)
 {
     if (!ctx || ctx->engine != ASD_ENGINE_D3) return 0;
-    const int per = ctx->plan.NP == 3 ? ctx->plan.cs : 1;
+    const int per = ctx->plan.NP == 3 ? ctx->plan.ncta : 1;
     return ctx->plan.NP == 3 ? ctx->plan.active_ctas / per : 0;
 }
 

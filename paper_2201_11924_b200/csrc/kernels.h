@@ -61,12 +61,18 @@ struct V2Plan {
     bool wide;        // WTA keys in u32 (S may exceed 2^(16 - log2 D))
     bool blk;         // u16-partial instances on a cost buffer (SGBM block cost, or SGM with 3(nb+P2) > 255)
     bool wta_fb;      // WTA by the warp-per-pixel kernel (the ring window does not fit, D = 256)
+    int ncta;         // sweep CTAs per frame: cs (one cluster) or nseg * cs (frame wider than a cluster)
+    uint32_t* gflag;  // segment-boundary row counters / halos (owned by the context; nseg > 1)
+    uint32_t* ghalo;
     char why[128];
 };
 bool v2_plan(const DevParams& p, int device, V2Plan& pl);
 // The ring-window WTA kernel alone (also used by engine D1 when D is 16..128):
 // fills nbuf / bstride / rsmem / wide; false if the window does not fit.
 bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl);
+// device bytes of the segment-boundary counters / halos for nframes frames (0 if nseg == 1)
+size_t v2_gflag_bytes(const V2Plan& pl, int nframes);
+size_t v2_ghalo_bytes(const V2Plan& pl, int nframes);
 void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16_t* S, long long cell_stride,
                  const FrameScratch& fs, long long px_stride, cudaStream_t s);
 // variant: stage 0 -> 1 = right-referenced K_down (R2); stage 2 -> 1 = cost

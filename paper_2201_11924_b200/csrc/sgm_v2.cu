@@ -165,6 +165,12 @@ struct VArgs {
     long long pa_stride;      // frame stride of the P_A buffer: H * (cs*w) * D
     int ablate;               // timing experiments only (ASD_V2_ABLATE, builds with -DASD_ABLATE)
     const uint16_t* cbin;     // BLK: SGBM block cost, K_down's private layout (frame stride pa_stride)
+    // frames wider than one cluster (ncta > cs): nseg = ncta / cs clusters per
+    // frame ("segments"); the diagonal halos of the CTAs at a segment boundary
+    // go through global memory with a per-row flag (gflag, release / acquire)
+    int ncta;                 // CTAs per frame (= cs for a frame in one cluster)
+    uint32_t* gflag;          // [frames][nseg-1][2 dirs][8] row counters (zeroed before each launch)
+    uint32_t* ghalo;          // [frames][nseg-1][2 dirs][2 slots][T][NR + 4]
 };
 
 // Ablation switches exist only in experiment builds (-DASD_ABLATE); in the
@@ -282,7 +288,11 @@ struct VGeom {
 #endif
 constexpr bool DEC = ASD_V2_DEC;
 
-template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
+// SEG: the frame spans several clusters (segments) joined through global memory
+// at their boundaries -- a separate instance, so frames in one cluster carry no
+// trace of it (a data-dependent wait loop in the row loop makes the compiler
+// guard every shuffle with WARPSYNC)
+template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false, bool SEG = false>
 __global__ void __launch_bounds__(DC >= 24 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
 {
@@ -295,10 +305,12 @@ vsweep_kernel(VArgs a)
     const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int col = lane / T, chunk = lane % T;
-    const int rank = blockIdx.x;
+    const int rank = NP == 3 ? (int)(blockIdx.x % (unsigned)a.cs) : (int)blockIdx.x;   // cluster rank
+    const int seg = SEG ? (int)(blockIdx.x / (unsigned)a.cs) : 0;                       // cluster of the frame
+    const int nseg = SEG ? a.ncta / a.cs : 1;
     const int frame = blockIdx.y;
     const int w = a.w;
-    const int x0 = rank * w;
+    const int x0 = blockIdx.x * w;
     const int xl = warp * CPW + col;
     const int x = x0 + xl;
     const int cstr = G::cstride(w);
@@ -330,7 +342,7 @@ vsweep_kernel(VArgs a)
     // K_down -> K_up handoff in a private layout: the warp's (CPW columns x D)
     // block is contiguous and instruction q of lane l covers 16 bytes at
     // 512*q + 16*l, i.e. warp-contiguous stores and loads (row stride cs*w).
-    const int wpad = a.cs * a.w;
+    const int wpad = a.ncta * a.w;
 
     const uint32_t* cl = a.cl + frame * a.sig_stride;
     const uint32_t* cr = a.cr + frame * a.sig_stride;
@@ -477,6 +489,38 @@ vsweep_kernel(VArgs a)
         }
     }
 
+    // segment boundaries (nseg > 1): the last CTA of segment s and the first of
+    // s+1 exchange their edge columns' diagonal states through global memory;
+    // boundary b = (s, s+1); the consumer is at most one row behind or ahead
+    // (each needs the other's previous row), so two slots suffice
+    const int nb = nseg - 1;
+    auto gh = [&](int b, int dir) {               // halo block of boundary b, direction 0 = L, 1 = R
+        return a.ghalo + ((((long long)frame * nb + b) * 2 + dir) * 2) * T * HS;
+    };
+    auto gf = [&](int b, int dir) { return a.gflag + (((long long)frame * nb + b) * 2 + dir) * 8; };
+    const bool gsendL = SEG && NP == 3 && nseg > 1 && rank == a.cs - 1 && seg + 1 < nseg && warp == nw - 1 && col == CPW - 1;
+    const bool gsendR = SEG && NP == 3 && nseg > 1 && rank == 0 && seg > 0 && warp == 0 && col == 0;
+    // warp-uniform: this warp receives a boundary halo (all its lanes wait, the
+    // edge lanes read), so the shuffles after the wait stay convergent
+    const bool gwL = SEG && NP == 3 && nseg > 1 && rank == 0 && seg > 0 && warp == 0;
+    const bool gwR = SEG && NP == 3 && nseg > 1 && rank == a.cs - 1 && seg + 1 < nseg && warp == nw - 1;
+    // spin until the producer published row `need` - 1 (flag >= need); a trap
+    // instead of a hang if it never comes
+    // Every warp of a SEG instance runs the same poll (one asm loop, relaxed
+    // generic loads): the boundary warps on the global row counter, the others
+    // on a shared-memory word that is always 0 -- so no branch encloses the
+    // loop (a loop under a warp-dependent branch makes the compiler guard every
+    // later shuffle of the row with WARPSYNC); the boundary warps then fence.
+    __shared__ uint32_t gzero;
+    if (SEG && threadIdx.x == 0) gzero = 0u;
+    auto gpoll = [&](const uint32_t* f, int need) {
+        asm volatile("{\n .reg .pred P, Q;\n .reg .u32 V;\n GWAIT_%=:\n"
+                     " ld.relaxed.gpu.u32 V, [%0];\n"
+                     " setp.lt.s32 P, V, %1;\n"
+                     " vote.sync.any.pred Q, P, 0xffffffff;\n"
+                     " @Q bra.uni GWAIT_%=;\n}\n" :: "l"(f), "r"(need) : "memory");
+    };
+
     uint32_t Lv[NR], Ll[NR], Lr[NR];
 #pragma unroll
     for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
@@ -488,12 +532,31 @@ vsweep_kernel(VArgs a)
     // diagonal paths of row i from the predecessors of row i-1 (halo slot rs)
     auto diagonals = [&](int i) {
         const int rs = (i + 1) & 1;              // slot written at row i-1
+        if (SEG) {                               // segment boundary: row i-1 published?
+            gpoll(gwL ? gf(seg - 1, 0) : &gzero, gwL ? i : 0);
+            gpoll(gwR ? gf(seg, 1) : &gzero, gwR ? i : 0);
+            if (gwL || gwR) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+        }
         uint32_t Pp[NR], Mp;
         // path "L": predecessor column x-1 (down-right / up-right)
 #pragma unroll
         for (int k = 0; k < NR; ++k) Pp[k] = __shfl_up_sync(FULL, Ll[k], T);
         Mp = __shfl_up_sync(FULL, Ml, T);
-        if (col == 0) {
+        if (gwL && col == 0) {                   // from the previous segment, row i-1
+            if (i > 0) {
+                const uint32_t* h = gh(seg - 1, 0) + (rs * T + chunk) * HS;
+#pragma unroll
+                for (int q = 0; q < NR / 4; ++q) {
+                    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(h) + q);
+                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
+                }
+                Mp = __ldcg(gh(seg - 1, 0) + (rs * T) * HS + NR);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) Pp[k] = 0u;
+                Mp = 0u;
+            }
+        } else if (col == 0) {
             const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
 #pragma unroll
             for (int q = 0; q < NR / 4; ++q) {
@@ -507,7 +570,21 @@ vsweep_kernel(VArgs a)
 #pragma unroll
         for (int k = 0; k < NR; ++k) Pp[k] = __shfl_down_sync(FULL, Lr[k], T);
         Mp = __shfl_down_sync(FULL, Mr, T);
-        if (col == CPW - 1) {
+        if (gwR && col == CPW - 1) {             // from the next segment, row i-1
+            if (i > 0) {
+                const uint32_t* h = gh(seg, 1) + (rs * T + chunk) * HS;
+#pragma unroll
+                for (int q = 0; q < NR / 4; ++q) {
+                    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(h) + q);
+                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
+                }
+                Mp = __ldcg(gh(seg, 1) + (rs * T) * HS + NR);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) Pp[k] = 0u;
+                Mp = 0u;
+            }
+        } else if (col == CPW - 1) {
             const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
 #pragma unroll
             for (int q = 0; q < NR / 4; ++q) {
@@ -539,6 +616,30 @@ vsweep_kernel(VArgs a)
 #pragma unroll
             for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
             if (chunk == 0) wRm[ws * nw] = Mr;
+        }
+        if (SEG && nseg > 1 && (warp == 0 || warp == nw - 1)) {
+            // segment boundary: halo to global memory, fence, then the row
+            // counter (one lane per direction, after the warp's stores)
+            if (gsendL) {
+                uint32_t* h = gh(seg, 0) + (ws * T + chunk) * HS;
+#pragma unroll
+                for (int q = 0; q < NR / 4; ++q)
+                    __stcg(reinterpret_cast<uint4*>(h) + q, make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]));
+                if (chunk == 0) __stcg(h + NR, Ml);
+            }
+            if (gsendR) {
+                uint32_t* h = gh(seg - 1, 1) + (ws * T + chunk) * HS;
+#pragma unroll
+                for (int q = 0; q < NR / 4; ++q)
+                    __stcg(reinterpret_cast<uint4*>(h) + q, make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]));
+                if (chunk == 0) __stcg(h + NR, Mr);
+            }
+            if (gsendL || gsendR) __threadfence();
+            __syncwarp();
+            if (chunk == 0 && gsendL)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" :: "l"(gf(seg, 0)), "r"((unsigned)(i + 1)) : "memory");
+            if (chunk == 0 && gsendR)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" :: "l"(gf(seg - 1, 1)), "r"((unsigned)(i + 1)) : "memory");
         }
     };
     // vertical path: predecessor = own column
@@ -1893,30 +1994,43 @@ typedef void (*RKernel)(RArgs);
 
 // the sweep kernel of this build: vsweep_dec_kernel (ASD_V2_DEC = 1, default)
 // or the round-1 barrier-per-row vsweep_kernel
-template <int DC, int T, int NP, bool UP, int DPL, bool RR = false, bool BLK = false>
+template <int DC, int T, int NP, bool UP, int DPL, bool RR = false, bool BLK = false, bool SEG = false>
 static VKernel vkern()
 {
 #if ASD_V2_DEC
     return v2::vsweep_dec_kernel<DC, T, NP, UP, DPL, RR, BLK>;
 #else
-    return v2::vsweep_kernel<DC, T, NP, UP, DPL, RR, BLK>;
+    return v2::vsweep_kernel<DC, T, NP, UP, DPL, RR, BLK, SEG>;
 #endif
 }
 
-template <int DC, int T, int DPL>
-static VKernel vk(int np, bool up, bool rr)
+template <int DC, int T, int DPL, bool SEG>
+static VKernel vk3(bool up, bool rr)
 {
-    if (up) return np == 3 ? vkern<DC, T, 3, true, DPL>() : vkern<DC, T, 1, true, DPL>();
-    if (rr) return np == 3 ? vkern<DC, T, 3, false, DPL, true>() : vkern<DC, T, 1, false, DPL, true>();
-    return np == 3 ? vkern<DC, T, 3, false, DPL>() : vkern<DC, T, 1, false, DPL>();
+    if (up) return vkern<DC, T, 3, true, DPL, false, false, SEG>();
+    if (rr) return vkern<DC, T, 3, false, DPL, true, false, SEG>();
+    return vkern<DC, T, 3, false, DPL, false, false, SEG>();
+}
+template <int DC, int T, int DPL>
+static VKernel vk(int np, bool up, bool rr, bool seg)
+{
+    if (np == 3) return seg ? vk3<DC, T, DPL, true>(up, rr) : vk3<DC, T, DPL, false>(up, rr);
+    if (up) return vkern<DC, T, 1, true, DPL>();
+    if (rr) return vkern<DC, T, 1, false, DPL, true>();
+    return vkern<DC, T, 1, false, DPL>();
 }
 
 // rr: the K_down instance with the right view as reference (R2); blk: the SGBM
 // instances (D = 128: DC = 32, T = 4, 8 paths only)
-static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = false, bool blk = false)
+static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = false, bool blk = false,
+                            bool seg = false)
 {
     if (blk) {
         if (DC != 32 || T != 4 || DPL != 4) return nullptr;
+        if (np == 3 && seg) {
+            if (up) return vkern<32, 4, 3, true, 4, false, true, true>();
+            return rr ? vkern<32, 4, 3, false, 4, true, true, true>() : vkern<32, 4, 3, false, 4, false, true, true>();
+        }
         if (np == 3) {
             if (up) return vkern<32, 4, 3, true, 4, false, true>();
             return rr ? vkern<32, 4, 3, false, 4, true, true>() : vkern<32, 4, 3, false, 4, false, true>();
@@ -1924,14 +2038,14 @@ static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = f
         if (up) return vkern<32, 4, 1, true, 4, false, true>();
         return rr ? vkern<32, 4, 1, false, 4, true, true>() : vkern<32, 4, 1, false, 4, false, true>();
     }
-    if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up, rr);
-    if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr);
-    if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up, rr);
-    if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up, rr);
-    if (DC == 24 && T == 4 && DPL == 4) return vk<24, 4, 4>(np, up, rr);     // D = 96
-    if (DC == 32 && T == 8 && DPL == 8) return vk<32, 8, 8>(np, up, rr);     // D = 256
+    if (DC == 16 && T == 1 && DPL == 2) return vk<16, 1, 2>(np, up, rr, seg);
+    if (DC == 32 && T == 1 && DPL == 2) return vk<32, 1, 2>(np, up, rr, seg);
+    if (DC == 32 && T == 2 && DPL == 2) return vk<32, 2, 2>(np, up, rr, seg);
+    if (DC == 32 && T == 4 && DPL == 4) return vk<32, 4, 4>(np, up, rr, seg);
+    if (DC == 24 && T == 4 && DPL == 4) return vk<24, 4, 4>(np, up, rr, seg);     // D = 96
+    if (DC == 32 && T == 8 && DPL == 8) return vk<32, 8, 8>(np, up, rr, seg);     // D = 256
 #ifdef ASD_ABLATE
-    if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up, rr);
+    if (DC == 16 && T == 8 && DPL == 4) return vk<16, 8, 4>(np, up, rr, seg);
 #endif
     return nullptr;
 }
@@ -1996,6 +2110,9 @@ static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up, bool blk
     return words * 4;
 }
 
+#ifndef ASD_V2_SEGSEARCH
+#define ASD_V2_SEGSEARCH 0        // 1: also try more segments per frame when one cluster fits
+#endif
 bool v2_plan(const DevParams& p, int device, V2Plan& pl)
 {
     pl = V2Plan{};
@@ -2040,6 +2157,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk);
     VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk);
     if (!kd || !ku) return no(blk ? "SGBM on engine D3 needs num_disp = 128" : "no sweep kernel instance");
+    VKernel kd1 = kd, ku1 = ku;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     double best = -1.0;
@@ -2049,11 +2167,20 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
 #else
     const int force_cs = 0;
 #endif
+    // nseg > 1: a frame wider than one cluster is covered by nseg clusters of cs
+    // CTAs (8 paths only), joined through global memory at the boundaries; all
+    // nseg clusters of a frame must be co-resident, so a wave is
+    // floor(active clusters / nseg) frames.  One segment is preferred.
+    for (int nseg = 1; nseg <= (np == 3 ? 4 : 1); ++nseg) {
+    kd = nseg > 1 ? pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk, true) : kd1;
+    ku = nseg > 1 ? pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk, true) : ku1;
     for (int cs = 1; cs <= 16; ++cs) {
         if (force_cs > 0 && cs != force_cs) continue;
-        int w = (p.W + cs - 1) / cs;
+        if (nseg > 1 && cs < 2) continue;
+        const int n = cs * nseg;
+        int w = (p.W + n - 1) / n;
         w = (w + CPW - 1) / CPW * CPW;
-        if ((long long)w * (cs - 1) >= p.W && cs > 1) continue;     // last CTA would be empty
+        if ((long long)w * (n - 1) >= p.W && n > 1) continue;      // last CTA would be empty
         const int threads = w * T;
         if (threads > maxt) continue;
         if (np == 1 && cs > 1 && threads < 128) continue;
@@ -2076,22 +2203,30 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
             cfg.attrs = at; cfg.numAttrs = 1;
             int nc = 0;
             if (cudaOccupancyMaxActiveClusters(&nc, (const void*)ku, &cfg) != cudaSuccess) { cudaGetLastError(); continue; }
-            active = nc * cs;
+            active = (nc / nseg) * nseg * cs;                         // whole frames only
         } else {
             int nb = 0;
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)ku, threads, sm) != cudaSuccess) { cudaGetLastError(); continue; }
             active = nb * nsm;
         }
         if (active <= 0) continue;
-        // throughput proxy: resident threads, penalising clusters that leave SMs idle
-        const double score = (double)active * threads;
+        // throughput proxy: resident threads, penalising clusters that leave SMs
+        // idle and (2 % per extra segment) the boundary exchange
+        const double score = (double)active * threads / (1.0 + 0.02 * (nseg - 1));
         if (score > best * 1.02) {
             best = score; pl.cs = cs; pl.w = w; pl.vthreads = threads; pl.vsmem = smd; pl.vsmem_up = sm;
-            pl.active_ctas = active;
+            pl.active_ctas = active; pl.ncta = n;
         }
         if (np == 1) break;
     }
+    // one cluster per frame when it fits (measured: config C 1937 frames/s as
+    // 10 x 1 vs 1390 as 5 x 4); otherwise the best-scoring segment count
+    if (nseg == 1 && best >= 0 && !ASD_V2_SEGSEARCH) break;
+    }
     if (best < 0) return no("no feasible cluster configuration");
+    const bool segs = np == 3 && pl.ncta > pl.cs;
+    kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk, segs);
+    ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk, segs);
     cudaFuncSetAttribute((const void*)kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
     cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     if (np == 1) {
@@ -2100,6 +2235,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         if (w > (p.W + CPW - 1) / CPW * CPW) w = (p.W + CPW - 1) / CPW * CPW;
         pl.w = w;
         pl.cs = (p.W + w - 1) / w;
+        pl.ncta = pl.cs;
         pl.vthreads = w * T;
         pl.vsmem = vsmem_bytes(w, p.D, T, pl.DC, np, false, blk);
         pl.vsmem_up = vsmem_bytes(w, p.D, T, pl.DC, np, true, blk);
@@ -2107,7 +2243,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         cudaFuncSetAttribute((const void*)ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem_up);
     }
     if (p.lr_mode == 1) {                            // R2: the right-referenced K_down
-        VKernel kr = pick_vkernel(pl.DC, T, pl.DPL, np, false, true, blk);
+        VKernel kr = pick_vkernel(pl.DC, T, pl.DPL, np, false, true, blk, segs);
         cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.vsmem);
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
@@ -2121,6 +2257,18 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     }
     pl.ok = true;
     return true;
+}
+
+// Segment-boundary exchange buffers (nseg > 1) for nframes frames in flight.
+size_t v2_gflag_bytes(const V2Plan& pl, int nframes)
+{
+    const int nb = pl.ncta / (pl.cs > 0 ? pl.cs : 1) - 1;
+    return nb > 0 ? (size_t)nframes * nb * 2 * 8 * sizeof(uint32_t) : 0;
+}
+size_t v2_ghalo_bytes(const V2Plan& pl, int nframes)
+{
+    const int nb = pl.ncta / (pl.cs > 0 ? pl.cs : 1) - 1;
+    return nb > 0 ? (size_t)nframes * nb * 2 * 2 * pl.T * (pl.DC / 2 + 4) * sizeof(uint32_t) : 0;
 }
 
 // The WTA kernel's window: rows [256t, 256t + 255 + min + D - 1] of stage t.
@@ -2152,7 +2300,7 @@ void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16
 static cudaError_t launch_vsweep(VKernel k, const V2Plan& pl, int nframes, const VArgs& a, bool up, cudaStream_t s)
 {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(pl.cs, nframes);
+    cfg.gridDim = dim3(pl.ncta, nframes);
     cfg.blockDim = dim3(pl.vthreads);
     cfg.dynamicSmemBytes = up ? pl.vsmem_up : pl.vsmem;
     cfg.stream = s;
@@ -2172,17 +2320,21 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
 {
     if (stage == 0 || stage == 1) {
         VArgs a{};
-        a.p = p; a.w = pl.w; a.cs = pl.cs;
+        a.p = p; a.w = pl.w; a.cs = pl.cs; a.ncta = pl.ncta;
+        a.gflag = pl.gflag; a.ghalo = pl.ghalo;
+        if (pl.ncta > pl.cs && pl.NP == 3)       // segment-boundary row counters start at 0 each launch
+            cudaMemsetAsync(pl.gflag, 0, v2_gflag_bytes(pl, nframes), s);
         a.cl = (const uint32_t*)cl; a.cr = (const uint32_t*)cr; a.sig_stride = sig_stride;
 #ifdef ASD_ABLATE
         static const int ablate = getenv("ASD_V2_ABLATE") ? atoi(getenv("ASD_V2_ABLATE")) : 0;
         a.ablate = ablate;
 #endif
         a.pin = reinterpret_cast<const uint16_t*>(pa); a.pouta = reinterpret_cast<uint16_t*>(pa);
-        a.pa_stride = (long long)p.H * pl.cs * pl.w * p.D;
+        a.pa_stride = (long long)p.H * pl.ncta * pl.w * p.D;
         a.pout16 = pab; a.cell_stride = cell_stride;
         a.cbin = cbin;
-        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1, pl.blk);
+        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1, pl.blk,
+                                 pl.NP == 3 && pl.ncta > pl.cs);
         return launch_vsweep(k, pl, nframes, a, stage == 1, s) == cudaSuccess ? 0 : -1;
     }
     (void)agg;
@@ -2192,7 +2344,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.nbuf = pl.nbuf; r.bstride = pl.bstride;
     r.p1x2 = (uint32_t)p.p1 * 0x10001u;
     r.p2x2 = (uint32_t)p.p2 * 0x10001u;
-    r.cb = cbin; r.cb_stride = (long long)p.H * pl.cs * pl.w * p.D; r.wpad = pl.cs * pl.w;
+    r.cb = cbin; r.cb_stride = (long long)p.H * pl.ncta * pl.w * p.D; r.wpad = pl.ncta * pl.w;
     if (stage == 2) {
         RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1 || ASD_HROW_CFROMP);
         const int hsm = pl.blk ? 0 : ASD_HROW_SMEM;

@@ -110,13 +110,15 @@ def test_config_C_full_frame(engine):
     _run(_cfg("C"), left, right, engine)
 
 
-def test_config_D_full_frame():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config_D_full_frame(engine):
     """One full 1920x1080 D256 8-path frame (BASELINE.json configs[3]), every
     stage against the full oracle: census, cost, S, d* of both views, masks and
     sub-pixel disparities bit-exact, depth to 1e-5 (about 9 GB of host memory
-    and half a minute of oracle time)."""
+    and half a minute of oracle time).  On D3 the frame spans two clusters of
+    15 CTAs joined through global memory."""
     left, right, _ = synth.make_pair("D", 0)
-    _run(_cfg("D"), left, right, 0)
+    _run(_cfg("D"), left, right, engine)
 
 
 @pytest.mark.parametrize("p2", [40, 54, 60, 120, 224])
@@ -138,13 +140,16 @@ def test_d3_envelope_p2(p2):
 
 
 @pytest.mark.parametrize("W,H,D,paths", [(320, 96, 96, 8), (320, 96, 96, 4), (512, 96, 256, 8),
-                                         (600, 80, 256, 4), (1000, 40, 256, 8)])
+                                         (600, 80, 256, 4), (1000, 40, 256, 8),
+                                         (1100, 48, 256, 8), (2100, 40, 128, 8)])
 def test_d3_more_disparity_ranges(W, H, D, paths):
     """Engine D3 at D = 96 (DC = 24 disparities per thread, T = 4) and D = 256
     (T = 8 threads per column, 8 disparities per lane in the row kernel, the
     warp-per-pixel WTA): Table II's other disparity ranges and
-    P:293's adjustable parameters.  8-path D = 256 needs the frame in one
-    cluster of <= 16 CTAs of 64 columns (W <= 1024).  Every stage bit-exact."""
+    P:293's adjustable parameters.  An 8-path frame wider than one cluster
+    (16 CTAs of 64 columns at D = 256, of 128 at D = 128: the last two cases)
+    runs as two clusters joined through global memory at the boundary.
+    Every stage bit-exact."""
     cfg = synth.StereoConfig("R", W, H, D, 9, 7, paths, 430.0 * W / 424 * D / 128, tag=12)
     left, right, _ = synth.speckle_pair(cfg, 0)
     _run(cfg.params_dict(), left, right, 3)
