@@ -256,6 +256,19 @@ __device__ __forceinline__ int stg_swz(int pi)
 // slice of the right row its DC disparities read (w + DC - 1 words), placed at
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
+// experiment switches (A/B builds, tools/ab_bench.sh); production uses the defaults
+#ifndef ASD_HROW_SG
+#define ASD_HROW_SG 8             // pixels per register-buffered load group in the row kernel
+#endif
+#ifndef ASD_HALO_SEL
+#define ASD_HALO_SEL 0            // 1: branch-free halo reads (all lanes load, the edge lanes select)
+#endif
+#ifndef ASD_WTA_FB256
+#define ASD_WTA_FB256 0           // 1: D = 256 WTA by the warp-per-pixel kernel even when the ring fits
+#endif
+#ifndef ASD_V2_SEGSEARCH
+#define ASD_V2_SEGSEARCH 0        // 1: also try more segments per frame when one cluster fits
+#endif
 #ifndef ASD_NSLOT
 #define ASD_NSLOT 4               // 6 and 8 measured no faster (tools/runs/d3ab.sh)
 #endif
@@ -556,6 +569,19 @@ vsweep_kernel(VArgs a)
                 for (int k = 0; k < NR; ++k) Pp[k] = 0u;
                 Mp = 0u;
             }
+        } else if (ASD_HALO_SEL) {
+            // every lane reads its chunk's halo (one address per chunk: broadcast),
+            // the column-0 lanes select it -- no divergent branch in the row loop
+            const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
+            const bool e = col == 0;
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                const uint4 v = h[q];
+                Pp[4 * q] = e ? v.x : Pp[4 * q]; Pp[4 * q + 1] = e ? v.y : Pp[4 * q + 1];
+                Pp[4 * q + 2] = e ? v.z : Pp[4 * q + 2]; Pp[4 * q + 3] = e ? v.w : Pp[4 * q + 3];
+            }
+            const uint32_t hm = hLM[rs * nw + warp];
+            Mp = e ? hm : Mp;
         } else if (col == 0) {
             const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
 #pragma unroll
@@ -584,6 +610,17 @@ vsweep_kernel(VArgs a)
                 for (int k = 0; k < NR; ++k) Pp[k] = 0u;
                 Mp = 0u;
             }
+        } else if (ASD_HALO_SEL) {
+            const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
+            const bool e = col == CPW - 1;
+#pragma unroll
+            for (int q = 0; q < NR / 4; ++q) {
+                const uint4 v = h[q];
+                Pp[4 * q] = e ? v.x : Pp[4 * q]; Pp[4 * q + 1] = e ? v.y : Pp[4 * q + 1];
+                Pp[4 * q + 2] = e ? v.z : Pp[4 * q + 2]; Pp[4 * q + 3] = e ? v.w : Pp[4 * q + 3];
+            }
+            const uint32_t hm = hRM[rs * nw + warp];
+            Mp = e ? hm : Mp;
         } else if (col == CPW - 1) {
             const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
 #pragma unroll
@@ -1537,7 +1574,7 @@ hrow_kernel(RArgs a)
 {
     using G = RowGeom<D>;
     constexpr int DPL = G::DPL, NRR = G::NRR, ACT = G::ACT;
-    constexpr int SG = 8;
+    constexpr int SG = ASD_HROW_SG;
     const DevParams& p = a.p;
     const int W = p.W, H = p.H;
     const int frame = blockIdx.y;
@@ -2110,9 +2147,6 @@ static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up, bool blk
     return words * 4;
 }
 
-#ifndef ASD_V2_SEGSEARCH
-#define ASD_V2_SEGSEARCH 0        // 1: also try more segments per frame when one cluster fits
-#endif
 bool v2_plan(const DevParams& p, int device, V2Plan& pl)
 {
     pl = V2Plan{};
@@ -2213,6 +2247,11 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         // throughput proxy: resident threads, penalising clusters that leave SMs
         // idle and (2 % per extra segment) the boundary exchange
         const double score = (double)active * threads / (1.0 + 0.02 * (nseg - 1));
+#ifdef ASD_ABLATE
+        if (getenv("ASD_PLAN_DEBUG"))
+            fprintf(stderr, "plan nseg=%d cs=%d w=%d threads=%d smem=%zu/%zu active=%d score=%.0f\n",
+                    nseg, cs, w, threads, smd, sm, active, score);
+#endif
         if (score > best * 1.02) {
             best = score; pl.cs = cs; pl.w = w; pl.vthreads = threads; pl.vsmem = smd; pl.vsmem_up = sm;
             pl.active_ctas = active; pl.ncta = n;
@@ -2248,7 +2287,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
     pl.wta_fb = false;
-    if (!wta2_plan(p, wide, pl)) {
+    if ((ASD_WTA_FB256 && p.D > 128 && p.lr_mode == 0) || !wta2_plan(p, wide, pl)) {
         // the window does not fit shared memory (D = 256): the warp-per-pixel
         // WTA kernel of engine D1 (post.cu) reads the same natural-order S
         if (p.lr_mode == 1) return no("min_disp + num_disp too large for the WTA window (R2)");
