@@ -156,11 +156,17 @@ def oracle_workers():
     return max(1, min(cores, mem_frames, 32)), cores
 
 
+def oracle_params(params: dict):
+    """oracle.Params of a run's parameters (the engine choice is the GPU's alone)."""
+    import oracle
+    return oracle.Params(**{k: v for k, v in params.items() if k != "engine"})
+
+
 def oracle_frames_parallel(params, Ls, Rs, nworkers):
     """The oracle as it stands: one full frame per worker thread (ctypes releases
     the GIL, so the C oracle runs on nworkers host cores)."""
     import oracle
-    p = oracle.Params(**params)
+    p = oracle_params(params)
     oracle.lib()
     out = [None] * nworkers
 
@@ -206,7 +212,7 @@ def oracle_pool_sigs(params, Ls, Rs, have: dict | None = None) -> dict:
     if not todo:
         return sigs
     nworkers, _ = oracle_workers()
-    p = oracle.Params(**params)
+    p = oracle_params(params)
     oracle.lib()
     for k in range(0, len(todo), nworkers):
         part = todo[k:k + nworkers]

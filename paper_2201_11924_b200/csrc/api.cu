@@ -684,7 +684,7 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
          c->dp.D == 256)) {
         const int ks = c->dp.D <= 16 ? 4 : c->dp.D <= 32 ? 5 : c->dp.D <= 64 ? 6 : c->dp.D <= 128 ? 7 : 8;
         const long long smax = (long long)c->dp.paths * ((long long)c->dp.bw * c->dp.bh * c->dp.nb + c->dp.p2);
-        if (wta2_plan(c->dp, smax >= (1ll << (16 - ks)), c->plan)) c->wta2 = true;
+        if (wta2_plan(c->dp, smax >= (1ll << (16 - ks)), c->plan, true)) c->wta2 = true;
     }
     Layout L = layout(c->dp, max_batch, c->engine,
                       c->engine == ASD_ENGINE_D3 ? c->plan.ncta * c->plan.w : c->dp.W,

@@ -60,7 +60,8 @@ struct V2Plan {
     size_t rsmem;
     bool wide;        // WTA keys in u32 (S may exceed 2^(16 - log2 D))
     bool blk;         // u16-partial instances on a cost buffer (SGBM block cost, or SGM with 3(nb+P2) > 255)
-    bool wta_fb;      // WTA by the warp-per-pixel kernel (the ring window does not fit, D = 256)
+    bool wta_fb;      // WTA by the warp-per-pixel kernel (the ring window does not fit)
+    bool halves;      // D = 256 (R1): wta_halves_kernel, three passes over half-width windows
     int ncta;         // sweep CTAs per frame: cs (one cluster) or nseg * cs (frame wider than a cluster)
     uint32_t* gflag;  // segment-boundary row counters / halos (owned by the context; nseg > 1)
     uint32_t* ghalo;
@@ -69,7 +70,7 @@ struct V2Plan {
 bool v2_plan(const DevParams& p, int device, V2Plan& pl);
 // The ring-window WTA kernel alone (also used by engine D1 when D is 16..128):
 // fills nbuf / bstride / rsmem / wide; false if the window does not fit.
-bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl);
+bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl, bool halves_ok = false);
 // device bytes of the segment-boundary counters / halos for nframes frames (0 if nseg == 1)
 size_t v2_gflag_bytes(const V2Plan& pl, int nframes);
 size_t v2_ghalo_bytes(const V2Plan& pl, int nframes);

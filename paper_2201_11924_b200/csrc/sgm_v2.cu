@@ -257,6 +257,9 @@ __device__ __forceinline__ int stg_swz(int pi)
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
 // experiment switches (A/B builds, tools/ab_bench.sh); production uses the defaults
+#ifndef ASD_WTA_HALVES
+#define ASD_WTA_HALVES 1          // D = 256 (R1): the three-pass half-width-window WTA kernel
+#endif
 #ifndef ASD_HROW_SG
 #define ASD_HROW_SG 8             // pixels per register-buffered load group in the row kernel
 #endif
@@ -2020,6 +2023,198 @@ wta2_kernel(RArgs a)
     }
 }
 
+// ---------------------------------------------------------------- K_wta, D = 256 in halves
+// The D = 256 window (384 rows x 516 B) would leave one 4-warp CTA per SM.
+// Here every stage of 256 pixels runs three passes over half-width windows
+// (rows of 128 disparities, 384 x 260 B = 100 KB: two 8-warp CTAs per SM):
+//   A  rows [x0, x0 + 256 + min + 127) of d 0..127: left and right view, low half
+//   B  rows [x0, x0 + 256)             of d 128..255: left view, high half
+//   C  rows [x0 + min + 128, +256+127) of d 128..255: right view, high half
+// Each pass leaves per lane the half's best key (S << 8 | d), its neighbours,
+// its own second best (|d - d*| >= 2 within the half), the half's minimum, the
+// minimum without the element next to the other half, and that element; the
+// merge then gives exactly the full-range d*, S(d* +- 1) and second best
+// (K4 semantics, readings c8, c9, c13).
+struct HalfSt { uint32_t key, cm, cp, s2, mall, medge, sedge; };
+constexpr uint32_t NOKEY = 0xFFFFFFFFu;
+
+// all 128 elements defined; e(j) = S(dbase + j), ep(j) = e(j) | e(j + 1) << 16 (j even)
+template <bool LOW, class E, class EP>
+__device__ __forceinline__ HalfSt half_scan_full(E e, EP ep, int dbase)
+{
+    uint32_t k0 = NOKEY, k1 = NOKEY, bm[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        uint32_t m = 0xFFFFu;
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+            const int j = 8 * b + t;
+            const uint32_t pr = ep(j);
+            const uint32_t v0 = pr & 0xFFFFu, v1 = pr >> 16;
+            k0 = min(k0, (v0 << 8) | (uint32_t)(dbase + j));
+            k1 = min(k1, (v1 << 8) | (uint32_t)(dbase + j + 1));
+            m = min(m, min(v0, v1));
+        }
+        bm[b] = m;
+    }
+    HalfSt h;
+    h.key = min(k0, k1);
+    const int js = (int)(h.key & 255u) - dbase;
+    h.cm = js > 0 ? e(js - 1) : NONE16;
+    h.cp = js < 127 ? e(js + 1) : NONE16;
+    const int blo = max(js - 1, 0) >> 3, bhi = min(js + 1, 127) >> 3;
+    uint32_t sec = 0xFFFFu, mall = 0xFFFFu, medge = 0xFFFFu;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        if (b < blo || b > bhi) sec = min(sec, bm[b]);
+        mall = min(mall, bm[b]);
+        if (LOW ? b < 15 : b > 0) medge = min(medge, bm[b]);
+    }
+    for (int b = blo; b <= bhi; ++b)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int j = 8 * b + t;
+            if (j < js - 1 || j > js + 1) sec = min(sec, e(j));
+        }
+#pragma unroll
+    for (int t = 0; t < 7; ++t) medge = min(medge, e(LOW ? 120 + t : 1 + t));   // the edge block minus the edge
+    h.s2 = sec; h.mall = mall; h.medge = medge;
+    h.sedge = e(LOW ? 127 : 0);
+    return h;
+}
+
+// the first nh (0..128) elements defined (right view near the right border)
+template <bool LOW, class E>
+__device__ __forceinline__ HalfSt half_scan_part(E e, int dbase, int nh)
+{
+    HalfSt h{NOKEY, NONE16, NONE16, NONE16, NONE16, NONE16, NONE16};
+    if (nh <= 0) return h;
+    uint32_t key = NOKEY;
+    for (int j = 0; j < nh; ++j) key = min(key, (e(j) << 8) | (uint32_t)(dbase + j));
+    const int js = (int)(key & 255u) - dbase;
+    h.key = key;
+    h.cm = js > 0 ? e(js - 1) : NONE16;
+    h.cp = js + 1 < nh ? e(js + 1) : NONE16;
+    uint32_t sec = NONE16, mall = NONE16, medge = NONE16;
+    for (int j = 0; j < nh; ++j) {
+        const uint32_t v = e(j);
+        if (j < js - 1 || j > js + 1) sec = min(sec, v);
+        mall = min(mall, v);
+        if (LOW ? j < 127 : j > 0) medge = min(medge, v);
+    }
+    h.s2 = sec; h.mall = mall; h.medge = medge;
+    h.sedge = LOW ? (nh == 128 ? e(127) : NONE16) : e(0);
+    return h;
+}
+
+__device__ __forceinline__ void merge_halves(const DevParams& p, const HalfSt& A, const HalfSt& B,
+                                             int& dstar, bool& uf, float& disp)
+{
+    uint32_t s0, cm, cp, s2;
+    if (A.key <= B.key) {                       // ties: the smaller d (A) wins, as in K4
+        dstar = (int)(A.key & 255u); s0 = A.key >> 8; cm = A.cm;
+        cp = dstar == 127 ? B.sedge : A.cp;
+        s2 = min(A.s2, dstar == 127 ? B.medge : B.mall);
+    } else {
+        dstar = (int)(B.key & 255u); s0 = B.key >> 8; cp = B.cp;
+        cm = dstar == 128 ? A.sedge : B.cm;
+        s2 = min(B.s2, dstar == 128 ? A.medge : A.mall);
+    }
+    finish_wta(p, dstar, s0, s2, cm, cp, uf, disp);
+}
+
+constexpr int WH_BS = 128 + WTA_PAD;       // u16 per half-window row (odd word stride)
+
+__global__ void __launch_bounds__(256)
+wta_halves_kernel(RArgs a)
+{
+    constexpr int D = 256, TX = 256, BS = WH_BS, STEP = BS + 1;
+    extern __shared__ __align__(16) uint16_t sbuf[];   // [nbuf][BS]
+    const DevParams& p = a.p;
+    const int W = p.W, md = p.min_disp;
+    const int y = blockIdx.x, frame = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint16_t* S = a.pab + frame * a.cell_stride + (long long)y * W * D;
+    const bool vrow = y >= p.Q && y < p.H - p.Q;
+    for (int xr = max(0, W - md) + tid; xr < W; xr += blockDim.x) {   // no disparity defined
+        const long long o = frame * a.px_stride + (long long)y * W + xr;
+        a.fs.dstar_r[o] = -1;
+        a.fs.mask_r[o] = MASK_BORDER;
+        a.fs.dr[o] = 0.0f;
+    }
+    // rows [r0, r1) of half h into window rows 0.. (4-byte cp.async, 64 per row)
+    auto fill = [&](int r0, int r1, int h) {
+        __syncthreads();                              // previous pass done with the window
+        constexpr int CH = 64, RSTEP = TX / CH;
+        const int c = tid % CH;
+        for (int r = r0 + tid / CH; r < r1; r += RSTEP)
+            cp_async4(reinterpret_cast<uint32_t*>(sbuf + (r - r0) * BS) + c,
+                      reinterpret_cast<const uint32_t*>(S + (long long)r * D + 128 * h) + c, true);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+    };
+    const int nstage = (W + TX - 1) / TX;
+    for (int t = 0; t < nstage; ++t) {
+        const int x0 = t * TX;
+        const int xp = x0 + tid;                      // this lane's left pixel and right pixel
+        const int nd = min(D, W - md - xp);           // defined disparities of right pixel xp
+        const bool fast = x0 + warp * 32 + 31 + md + D - 1 < W;   // warp-uniform: all defined
+        HalfSt LA, RA;
+        // ---- pass A: d 0..127, left and right
+        fill(x0, min(W, x0 + TX + md + 127), 0);
+        if (xp < W) {
+            const uint16_t* r = sbuf + (xp - x0) * BS;
+            const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);
+            LA = half_scan_full<true>([&](int j) { return (uint32_t)r[j]; }, [&](int j) { return r32[j / 2]; }, 0);
+        }
+        if (xp < W && nd > 0) {
+            const uint16_t* b0 = sbuf + (xp + md - x0) * BS;
+            if (fast) RA = half_scan_full<true>([&](int j) { return (uint32_t)b0[j * STEP]; },
+                                                [&](int j) { return __byte_perm(b0[j * STEP], b0[(j + 1) * STEP], 0x5410); }, 0);
+            else RA = half_scan_part<true>([&](int j) { return (uint32_t)b0[j * STEP]; }, 0, min(nd, 128));
+        }
+        // ---- pass B: d 128..255, left view
+        fill(x0, min(W, x0 + TX), 1);
+        if (xp < W) {
+            const uint16_t* r = sbuf + (xp - x0) * BS;
+            const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);
+            const HalfSt LB = half_scan_full<false>([&](int j) { return (uint32_t)r[j]; },
+                                                    [&](int j) { return r32[j / 2]; }, 128);
+            int ds; bool uf; float disp;
+            merge_halves(p, LA, LB, ds, uf, disp);
+            const long long o = frame * a.px_stride + (long long)y * W + xp;
+            uint8_t m = 0;
+            if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
+            if (uf) m |= MASK_UNIQUE;
+            a.fs.dstar_l[o] = (int16_t)ds;
+            a.fs.mask_l[o] = m;
+            a.fs.dl[o] = disp;
+        }
+        // ---- pass C: d 128..255, right view
+        const int c0 = x0 + md + 128;
+        fill(c0, min(W, c0 + TX + 127), 1);
+        if (xp < W && nd > 0) {
+            HalfSt RB{NOKEY, NONE16, NONE16, NONE16, NONE16, NONE16, NONE16};
+            if (nd > 128) {
+                const uint16_t* b0 = sbuf + (xp - x0) * BS;       // row xp + md + 128 + j of the window
+                if (fast) RB = half_scan_full<false>([&](int j) { return (uint32_t)b0[j * STEP]; },
+                                                     [&](int j) { return __byte_perm(b0[j * STEP], b0[(j + 1) * STEP], 0x5410); }, 128);
+                else RB = half_scan_part<false>([&](int j) { return (uint32_t)b0[j * STEP]; }, 128, nd - 128);
+            }
+            int ds; bool uf; float disp;
+            merge_halves(p, RA, RB, ds, uf, disp);
+            const long long o = frame * a.px_stride + (long long)y * W + xp;
+            uint8_t m = 0;
+            if (!(vrow && xp >= p.R && xp < W - p.R)) m |= MASK_BORDER;
+            if (uf) m |= MASK_UNIQUE;
+            a.fs.dstar_r[o] = (int16_t)ds;
+            a.fs.mask_r[o] = m;
+            a.fs.dr[o] = disp;
+        }
+    }
+}
+
 }  // namespace v2
 
 // ======================================================================== host
@@ -2311,9 +2506,24 @@ size_t v2_ghalo_bytes(const V2Plan& pl, int nframes)
 }
 
 // The WTA kernel's window: rows [256t, 256t + 255 + min + D - 1] of stage t.
-bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl)
+bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl, bool halves_ok)
 {
     if (!pick_wkernel(p.D, wide)) return false;
+    // wta_halves_kernel (half-width windows): engine D1 only -- in the D3
+    // pipeline its 2 x 100 KB CTAs per SM delay the sweep clusters (config D
+    // 297 vs 307 frames/s), while D1 runs its stages one after another (233 -> 246)
+    pl.halves = ASD_WTA_HALVES && halves_ok && p.D == 256 && p.lr_mode == 0;
+    if (pl.halves) {
+        pl.nbuf = ((256 + p.min_disp + 128 + 31) / 32) * 32;
+        pl.bstride = v2::WH_BS;
+        pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
+        if (pl.rsmem > 200 * 1024) return false;
+        cudaFuncSetAttribute((const void*)v2::wta_halves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pl.rsmem);
+        cudaGetLastError();
+        pl.wide = true;
+        return true;
+    }
     pl.nbuf = ((32 * v2::wta_warps(p.D) + p.min_disp + p.D + 31) / 32) * 32;
     pl.bstride = p.D + v2::WTA_PAD;     // RowGeom<D>::BS
     pl.rsmem = (size_t)pl.nbuf * pl.bstride * 2;
@@ -2332,6 +2542,7 @@ void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16
     RArgs r{};
     r.p = p; r.pab = const_cast<uint16_t*>(S); r.cell_stride = cell_stride; r.fs = fs; r.px_stride = px_stride;
     r.nbuf = pl.nbuf; r.bstride = pl.bstride;
+    if (pl.halves) { v2::wta_halves_kernel<<<dim3(p.H, nframes), 256, pl.rsmem, s>>>(r); return; }
     RKernel k = pick_wkernel(p.D, pl.wide);
     k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
 }
@@ -2392,6 +2603,8 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     } else {
         if (pl.wta_fb) {
             if (!launch_wta(p, nframes, pab, cell_stride, fs, px_stride, s)) return -1;
+        } else if (pl.halves && variant == 0) {
+            v2::wta_halves_kernel<<<dim3(p.H, nframes), 256, pl.rsmem, s>>>(r);
         } else {
             RKernel k = pick_wkernel(p.D, pl.wide, variant);
             k<<<dim3(p.H, nframes), 32 * v2::wta_warps(p.D), pl.rsmem, s>>>(r);
