@@ -132,6 +132,53 @@ def run_params(cfg, block: int, lr_mode: int = 0, median: int = 0, engine: int =
     return d
 
 
+def bench_config(args, world: int) -> dict:
+    """The `config` object, identical in both arms (GPU and reference) of the
+    same command line: the workload and the L2 statement (run details go under
+    `run`)."""
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    B = args.job // max(1, world) if args.job else args.frames
+    return {"workload": workload(args.block, args.lr_mode, args.median, args.config)
+                        + (f" (P2={args.p2})" if args.p2 else "")
+                        + (f"; E: job of {args.job} frames per step sharded over {world} GPU(s)" if args.job else ""),
+            "l2": f"inputs larger than L2 ({2 * B * cfg.height * cfg.width / 1e6:.0f} MB/step/GPU) "
+                  "+ per-frame scratch > L2"}
+
+
+def host_context(params, cpu) -> dict:
+    """SURVEY §8(d)'s oracle context in the same run: the host CPU, the oracle's
+    single-frame latency per config (A and B timed here on one core; C from the
+    cpu_baseline run, one frame per thread), and the paper's Table II numbers
+    with their hardware (another workload and GPU: context only)."""
+    import oracle
+    import synth
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    lat = {}
+    for name in ("A", "B"):
+        c = synth.CONFIGS[name]
+        L, R, _ = synth.make_pair(name, 0)
+        t0 = time.perf_counter()
+        oracle.compute(oracle.Params(**c.params_dict()), L, R)
+        lat[name] = round(time.perf_counter() - t0, 3)
+    if cpu:
+        lat["C"] = cpu.get("frame_latency_s")
+    return {"cpu_model": model, "host_cores": len(os.sched_getaffinity(0)),
+            "oracle_single_frame_latency_s": lat,
+            "paper_table2": {"hardware": "1x RTX 4090 (P:296); OpenCV SGBM on i5-10400",
+                             "workload": "960x540 -> 1920x1080, 4-path, median 3 (not config C)",
+                             "sgm_fps": {str(k): v[0] for k, v in TABLE2_FPS.items()},
+                             "sgbm_fps": {str(k): v[1] for k, v in TABLE2_FPS.items()},
+                             "source": "PAPER.md Table II, BASELINE.md §1"}}
+
+
 def workload(block: int, lr_mode: int = 0, median: int = 0, cfg_name: str = "C") -> str:
     extra = (", R2 right view" if lr_mode else "") + (f", median {median}" if median else "")
     if cfg_name == "D":
@@ -197,7 +244,7 @@ def cpu_baseline(params, Ls, Rs, cfg_name="C"):
     wall, outs = oracle_frames_parallel(params, Ls, Rs, nworkers)
     sigs = {i % len(Ls): _oracle_sig(o) for i, o in enumerate(outs)}
     return {"value": round(nworkers / wall, 4), "unit": "frames/s", "cores": nworkers,
-            "kind": "oracle",
+            "kind": "oracle", "frame_latency_s": round(wall, 2),
             "sample": f"{nworkers} full config-{cfg_name} frames"
                       f"{' (SGBM block)' if params.get('block_w', 1) > 1 else ''}, one per host thread "
                       f"on {nworkers} of {cores} cores, plain-C oracle (gcc -O2), wall {wall:.1f} s"}, sigs
@@ -248,8 +295,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = synth.CONFIGS[CONFIG]
+    cfg = synth.CONFIGS[args.config]
     params = run_params(cfg, args.block, args.lr_mode, args.median)
+    if args.p2:
+        params["p2"] = args.p2
     Ls, Rs = synth.frame_pool(cfg, min(POOL, 4))
     nworkers, cores = oracle_workers()
     for _ in range(args.warmup):
@@ -260,14 +309,14 @@ def run_reference(args):
         tot += w
     frames = nworkers * args.steps
     value = frames / tot
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "frames/s",
+    line = {"impl": "reference", "metric": METRIC if args.config == "C" else METRIC_D, "value": round(value, 4), "unit": "frames/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000 * tot / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 6),
-            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config)
-                                   + (f"; E: job of {args.job} frames per step (CPU oracle: a bounded sample)" if args.job else ""),
-                       "frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)"},
+            "config": bench_config(args, int(os.environ.get("WORLD_SIZE", str(args.gpus)))),
+            "run": {"frames_per_step": nworkers, "impl": "CPU oracle (oracle/asd_oracle.c)",
+                    "note": "each step: one full frame of the workload per host thread (a bounded sample)"},
             "cpu_baseline": {"value": round(value, 4), "unit": "frames/s", "cores": nworkers,
                              "kind": "oracle",
                              "sample": f"{nworkers} full config-C frames per step, one per thread "
@@ -715,13 +764,9 @@ def main():
             "dtype": "u16",
             "data": "synthetic",
             "gcells_per_s": round(value * cfg.cells / 1e9, 3),
-            "config": {"workload": workload(args.block, args.lr_mode, args.median, args.config)
-                                   + (f" (P2={args.p2})" if args.p2 else "")
-                                   + (f"; E: job of {args.job} frames per step sharded over {world} GPU(s)" if args.job else ""),
-                       "frames_per_step_per_gpu": B, "max_batch": args.max_batch,
-                       "distinct_frames": POOL,
-                       "l2": f"inputs larger than L2 ({2 * B * H * W / 1e6:.0f} MB/step/GPU) + per-frame scratch > L2",
-                       "engine": st.plan_info},
+            "config": bench_config(args, world),
+            "run": {"frames_per_step_per_gpu": B, "max_batch": args.max_batch,
+                    "distinct_frames": POOL, "engine": st.plan_info},
             "roofline": roof,
             "parity": parity if not args.no_parity else None,
             "stage_ms": {k: round(prof[k]["ms"] / psteps, 3) for k in asd.abi.STAGES if prof[k]["launches"]},
@@ -740,6 +785,10 @@ def main():
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+            try:
+                line["context"] = host_context(params, cpu)
+            except Exception as exc:             # context only: never fail the line for it
+                line["context"] = {"error": str(exc)[:200]}
         print(json.dumps(line), flush=True)
         bad = (0 if args.no_parity else parity["mismatches"] + (parity_e2e["mismatches"] if parity_e2e else 0))
         if bad:
