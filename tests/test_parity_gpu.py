@@ -153,3 +153,16 @@ def test_d3_more_disparity_ranges(W, H, D, paths):
     cfg = synth.StereoConfig("R", W, H, D, 9, 7, paths, 430.0 * W / 424 * D / 128, tag=12)
     left, right, _ = synth.speckle_pair(cfg, 0)
     _run(cfg.params_dict(), left, right, 3)
+
+
+@pytest.mark.parametrize("variant", ["sgbm3", "r2", "p2_100", "median5"])
+def test_d3_two_segment_variants(variant):
+    """The engine's other instances on a frame spanning two clusters (2100 x 40,
+    D = 128, 8 paths): SGBM 3x3 and SGM with P2 = 100 (u16-partial BLK sweeps),
+    the R2 right view (right-referenced down sweep), median 5.  Bit-exact."""
+    cfg = synth.StereoConfig("S2", 2100, 40, 128, 9, 7, 8, 430.0 * 2100 / 424, tag=13)
+    left, right, _ = synth.speckle_pair(cfg, 0)
+    d = cfg.params_dict()
+    d.update({"sgbm3": dict(block_w=3, block_h=3, p1=72, p2=288), "r2": dict(lr_mode=1),
+              "p2_100": dict(p2=100), "median5": dict(median_ksize=5)}[variant])
+    _run(d, left, right, 3)
