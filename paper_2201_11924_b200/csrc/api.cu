@@ -30,6 +30,9 @@ struct asd_ctx {
     int max_batch = 1;
     size_t sig_bytes = 4;
     // scratch (max_batch frame slots)
+    void* census_l_base = nullptr;   // allocations (guard band before and after)
+    void* census_r_base = nullptr;
+    size_t cen_guard = 0;
     void* census_l = nullptr;
     void* census_r = nullptr;
     uint16_t* S = nullptr;
@@ -588,7 +591,7 @@ int run_chunk(asd_ctx* c, int n, const uint8_t* left, const uint8_t* right,
 void free_ctx(asd_ctx* c)
 {
     if (!c) return;
-    void* ptrs[] = {c->census_l, c->census_r, c->S, c->SR, c->cb, c->cb2, c->dl, c->dr, c->dstar_l, c->dstar_r,
+    void* ptrs[] = {c->census_l_base, c->census_r_base, c->S, c->SR, c->cb, c->cb2, c->dl, c->dr, c->dstar_l, c->dstar_r,
                     c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->plan.gflag, c->plan.ghalo,
                     c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
@@ -638,7 +641,8 @@ size_t asd_scratch_bytes(const asd_params* p, int max_batch)
         V2Plan pl;
         if (v2_plan(d, dev, pl))
             return layout(d, max_batch, ASD_ENGINE_D3, pl.ncta * pl.w, pl.blk).total +
-                   v2_gflag_bytes(pl, max_batch) + v2_ghalo_bytes(pl, max_batch);
+                   v2_gflag_bytes(pl, max_batch) + v2_ghalo_bytes(pl, max_batch) +
+                   4 * align_up((size_t)4 * ((size_t)d.min_disp + d.D + 1024 + 64));   // census guards
         cudaGetLastError();
     }
     return layout(d, max_batch, engine, d.W).total;
@@ -698,7 +702,14 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         if (ok) cudaMemset(*q, 0xA5, bytes);
 #endif
     };
-    alloc(&c->census_l, L.sig); alloc(&c->census_r, L.sig);
+    // census buffers with guard bands: the D3 down sweep's TMA staging copies
+    // from 16-byte aligned starts up to min_disp + D + w columns outside a row
+    c->cen_guard = align_up((size_t)4 * ((size_t)c->dp.min_disp + c->dp.D + 1024 + 64));
+    alloc(&c->census_l_base, L.sig + 2 * c->cen_guard); alloc(&c->census_r_base, L.sig + 2 * c->cen_guard);
+    if (ok) {
+        c->census_l = (char*)c->census_l_base + c->cen_guard;
+        c->census_r = (char*)c->census_r_base + c->cen_guard;
+    }
     if (L.s) alloc((void**)&c->S, L.s);
     if (L.cb) alloc((void**)&c->cb, L.cb);
     if (L.sr) alloc((void**)&c->SR, L.sr);

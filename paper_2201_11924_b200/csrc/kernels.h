@@ -62,6 +62,7 @@ struct V2Plan {
     bool blk;         // u16-partial instances on a cost buffer (SGBM block cost, or SGM with 3(nb+P2) > 255)
     bool wta_fb;      // WTA by the warp-per-pixel kernel (the ring window does not fit)
     bool halves;      // D = 256 (R1): wta_halves_kernel, three passes over half-width windows
+    bool tma_cen;     // K_down stages census rows with TMA bulk copies (needs guarded census buffers)
     int ncta;         // sweep CTAs per frame: cs (one cluster) or nseg * cs (frame wider than a cluster)
     uint32_t* gflag;  // segment-boundary row counters / halos (owned by the context; nseg > 1)
     uint32_t* ghalo;

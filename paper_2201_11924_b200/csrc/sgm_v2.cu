@@ -169,6 +169,7 @@ struct VArgs {
     // frame ("segments"); the diagonal halos of the CTAs at a segment boundary
     // go through global memory with a per-row flag (gflag, release / acquire)
     int ncta;                 // CTAs per frame (= cs for a frame in one cluster)
+    int tma_cen;              // K_down: census rows staged by TMA bulk copies (guarded census buffers)
     uint32_t* gflag;          // [frames][nseg-1][2 dirs][8] row counters (zeroed before each launch)
     uint32_t* ghalo;          // [frames][nseg-1][2 dirs][2 slots][T][NR + 4]
 };
@@ -257,6 +258,9 @@ __device__ __forceinline__ int stg_swz(int pi)
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
 // experiment switches (A/B builds, tools/ab_bench.sh); production uses the defaults
+#ifndef ASD_CEN_TMA
+#define ASD_CEN_TMA 1             // K_down census rows by TMA bulk copies (one thread) instead of cp.async
+#endif
 #ifndef ASD_WTA_HALVES
 #define ASD_WTA_HALVES 1          // D = 256 (R1): the three-pass half-width-window WTA kernel
 #endif
@@ -355,6 +359,14 @@ vsweep_kernel(VArgs a)
     uint16_t* ring2 = ring + KR * w * D;             // BLK K_up: the CB ring
     uint64_t* mbar = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(ring + (RING ? NRING * KR * w * D : 0)) + 7) & ~uintptr_t(7));
+    uint64_t* cbar = mbar + (RING ? KR : 0);         // [NSLOT] census full (K_down, tma_cen)
+    // TMA census: the right slices are copied from 16-byte aligned starts,
+    // cshift words before their first column (the same for every chunk and row)
+    const int cshift = (!RING && a.tma_cen)
+        ? (RR ? ((x0 + p.min_disp) & 3) : ((x0 - p.min_disp - (DC - 1)) & 3)) : 0;
+    auto cen_ready = [&](int j) {                    // census row j landed (TMA staging)
+        if (!RING && a.tma_cen) mbar_wait(cbar + j % NSLOT, (unsigned)((j / NSLOT) & 1));
+    };
     // K_down -> K_up handoff in a private layout: the warp's (CPW columns x D)
     // block is contiguous and instruction q of lane l covers 16 bytes at
     // 512*q + 16*l, i.e. warp-contiguous stores and loads (row stride cs*w).
@@ -376,6 +388,25 @@ vsweep_kernel(VArgs a)
         uint32_t* sl = cens + slot * sw;
         const uint32_t* rl = cl + (long long)yrow * W;
         const uint32_t* rr = cr + (long long)yrow * W;
+        if (a.tma_cen) {
+            // one thread: the left row and the T right slices as bulk copies from
+            // 16-byte aligned starts (the slices from cshift words before their
+            // first column; columns outside the image are read from the guard
+            // bands / neighbouring rows and never used: the cost masks them)
+            if (threadIdx.x == 0) {
+                const unsigned nal = (unsigned)((w + DC - 1 + cshift + 3) & ~3);
+                uint64_t* bar = cbar + slot;
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                mbar_arrive_expect(bar, (unsigned)(w * 4) + (unsigned)T * nal * 4u);
+                bulk_g2s_tx(sl, rl + x0, (unsigned)(w * 4), bar);
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    const int g0 = RR ? x0 + p.min_disp + DC * k : x0 - p.min_disp - DC * k - (DC - 1);
+                    bulk_g2s_tx(sl + w + k * cstr + G::coff(k), rr + (g0 - cshift), nal * 4u, bar);
+                }
+            }
+            return;
+        }
         for (int i = threadIdx.x; i < w; i += blockDim.x) {
             const int gx = x0 + i;
             cp_async4(sl + i, gx < W ? rl + gx : rl, gx < W);
@@ -406,7 +437,7 @@ vsweep_kernel(VArgs a)
         const uint32_t clv = sl[xl];
         // element for local disparity j (d = chunk*DC + j) at row[-j] (RR: row[+j])
         constexpr int SG = RR ? 1 : -1;
-        const uint32_t* row = sl + w + chunk * cstr + G::coff(chunk) + xl + (RR ? 0 : DC - 1);
+        const uint32_t* row = sl + w + chunk * cstr + G::coff(chunk) + xl + (RR ? 0 : DC - 1) + cshift;
         // local j valid iff j <= lim (the matched census window lies inside the image)
         const int lim = RR ? (W - p.R - 1) - (x + p.min_disp + chunk * DC)
                            : x - p.min_disp - p.R - chunk * DC;
@@ -774,6 +805,14 @@ vsweep_kernel(VArgs a)
         }
         __syncthreads();
         for (int i0 = 0; i0 < KR; ++i0) issue_row(i0);
+    } else if (a.tma_cen) {
+        if (threadIdx.x == 0) {
+            for (int s2 = 0; s2 < NSLOT; ++s2) mbar_init(cbar + s2, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        for (int i0 = 0; i0 < NSLOT - 1; ++i0)
+            if (i0 < H) stage(row_of(i0), i0);
     } else {
         for (int i0 = 0; i0 < NSLOT - 1; ++i0)
             if (i0 < H) stage(row_of(i0), i0);
@@ -782,7 +821,7 @@ vsweep_kernel(VArgs a)
     arrive();
     wait();
     if (RING) load_pin(0, PA, C);
-    else cost(row_of(0), 0, C);
+    else { cen_ready(0); cost(row_of(0), 0, C); }
 
     for (int i = 0; i < H; ++i) {
         const int y = row_of(i);
@@ -795,8 +834,8 @@ vsweep_kernel(VArgs a)
         // ---- K_down: stage row i+NSLOT-1 (async), make row i+1's copies complete, publish
         if (!RING) {
             if (i + NSLOT - 1 < H) stage(row_of(i + NSLOT - 1), (i + NSLOT - 1) % NSLOT);
-            else cp_async_commit();                  // keep one group per row
-            cp_async_wait<NSLOT - 2>();
+            else if (!a.tma_cen) cp_async_commit();  // keep one group per row
+            if (!a.tma_cen) cp_async_wait<NSLOT - 2>();
         }
         arrive();
         issue_row(i + KR);                            // ring input: row i's slot is free now
@@ -805,7 +844,7 @@ vsweep_kernel(VArgs a)
         // ---- next row's cost while the barrier completes
         if (i + 1 < H) {
             if (RING) load_pin(i + 1, PA, C);
-            else cost(row_of(i + 1), (i + 1) % NSLOT, C);
+            else { cen_ready(i + 1); cost(row_of(i + 1), (i + 1) % NSLOT, C); }
         }
     }
     wait();                                          // pairs with the last arrive
@@ -2338,6 +2377,8 @@ static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up, bool blk
     if (ring) {                                       // TMA ring(s) + mbarriers (+ align)
         const int kr = (up && blk) ? 2 : v2::KU, nring = (up && blk) ? 2 : 1;
         words += (size_t)nring * kr * w * D / 2 + 2 * kr + 4;
+    } else {
+        words += 2 * v2::NSLOT + 4;                   // census-row mbarriers (TMA staging)
     }
     return words * 4;
 }
@@ -2383,6 +2424,9 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     const int T = pl.T, CPW = 32 / T;
     const int maxt = pl.DC >= 24 ? 512 : 1024;      // __launch_bounds__ of vsweep_kernel
     pl.blk = blk;
+    // census rows by TMA bulk copies: 16-byte aligned rows and slice starts
+    // (the context allocates guard bands around the census buffers)
+    pl.tma_cen = ASD_CEN_TMA && !blk && p.W % 4 == 0 && p.min_disp % 4 == 0;
     VKernel kd = pick_vkernel(pl.DC, T, pl.DPL, np, false, false, blk);
     VKernel ku = pick_vkernel(pl.DC, T, pl.DPL, np, true, false, blk);
     if (!kd || !ku) return no(blk ? "SGBM on engine D3 needs num_disp = 128" : "no sweep kernel instance");
@@ -2572,6 +2616,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         VArgs a{};
         a.p = p; a.w = pl.w; a.cs = pl.cs; a.ncta = pl.ncta;
         a.gflag = pl.gflag; a.ghalo = pl.ghalo;
+        a.tma_cen = stage == 0 && pl.tma_cen;
         if (pl.ncta > pl.cs && pl.NP == 3)       // segment-boundary row counters start at 0 each launch
             cudaMemsetAsync(pl.gflag, 0, v2_gflag_bytes(pl, nframes), s);
         a.cl = (const uint32_t*)cl; a.cr = (const uint32_t*)cr; a.sig_stride = sig_stride;
