@@ -61,11 +61,6 @@ __device__ __forceinline__ void cp_async4(uint32_t* sdst, const uint32_t* gsrc, 
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" :: "r"(sa), "l"(gsrc), "r"(valid ? 4 : 0) : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc)
-{
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(gsrc) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
@@ -120,35 +115,6 @@ __device__ __forceinline__ void fence_cluster()
 __device__ __forceinline__ void cluster_wait()
 {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-// Decoupled sweeps (vsweep_dec_kernel): point-to-point mbarrier signals
-// between neighbouring warps instead of a CTA / cluster barrier per row.
-__device__ __forceinline__ uint32_t mapa_u32(const void* p, unsigned rank)
-{
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-    return r;
-}
-// arrive with CTA-scope release: orders this warp's halo stores (the writing
-// lanes synchronise with the arriving lane through __syncwarp first)
-__device__ __forceinline__ void mbar_arrive_local(uint32_t addr)
-{
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" :: "r"(addr) : "memory");
-}
-// arrive on a neighbouring CTA's barrier; the writing lanes fenced at cluster
-// scope before (fence.acq_rel.cluster), so the arrive itself is relaxed
-__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr)
-{
-    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" :: "r"(cluster_addr) : "memory");
-}
-// wait for a phase completed by a remote arrive: poll relaxed, then one
-// cluster-scope acquire fence (an acquire poll would invalidate L1 per try)
-__device__ __forceinline__ void mbar_wait_remote(uint64_t* bar, unsigned parity)
-{
-    asm volatile("{\n .reg .pred P;\n WAITR_%=:\n"
-                 " mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 P, [%0], %1;\n"
-                 " @!P bra WAITR_%=;\n}\n fence.acq_rel.cluster;\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
 struct VArgs {
@@ -267,15 +233,6 @@ __device__ __forceinline__ int stg_swz(int pi)
 #ifndef ASD_HROW_SG
 #define ASD_HROW_SG 8             // pixels per register-buffered load group in the row kernel
 #endif
-#ifndef ASD_HALO_SEL
-#define ASD_HALO_SEL 0            // 1: branch-free halo reads (all lanes load, the edge lanes select)
-#endif
-#ifndef ASD_WTA_FB256
-#define ASD_WTA_FB256 0           // 1: D = 256 WTA by the warp-per-pixel kernel even when the ring fits
-#endif
-#ifndef ASD_V2_SEGSEARCH
-#define ASD_V2_SEGSEARCH 0        // 1: also try more segments per frame when one cluster fits
-#endif
 #ifndef ASD_NSLOT
 #define ASD_NSLOT 4               // 6 and 8 measured no faster (tools/runs/d3ab.sh)
 #endif
@@ -303,10 +260,6 @@ struct VGeom {
 // by TMA in this kernel's private layout (K_down: CB ring instead of census
 // staging; K_up: a CB ring beside the P_A ring), and the handoffs carry the
 // wider partials without the cost bits: K_down writes P_A (u16), K_up P_AB.
-#ifndef ASD_V2_DEC
-#define ASD_V2_DEC 0              // 1: vsweep_dec_kernel (experiment: measured slower); 0: barrier per row
-#endif
-constexpr bool DEC = ASD_V2_DEC;
 
 // SEG: the frame spans several clusters (segments) joined through global memory
 // at their boundaries -- a separate instance, so frames in one cluster carry no
@@ -603,19 +556,6 @@ vsweep_kernel(VArgs a)
                 for (int k = 0; k < NR; ++k) Pp[k] = 0u;
                 Mp = 0u;
             }
-        } else if (ASD_HALO_SEL) {
-            // every lane reads its chunk's halo (one address per chunk: broadcast),
-            // the column-0 lanes select it -- no divergent branch in the row loop
-            const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
-            const bool e = col == 0;
-#pragma unroll
-            for (int q = 0; q < NR / 4; ++q) {
-                const uint4 v = h[q];
-                Pp[4 * q] = e ? v.x : Pp[4 * q]; Pp[4 * q + 1] = e ? v.y : Pp[4 * q + 1];
-                Pp[4 * q + 2] = e ? v.z : Pp[4 * q + 2]; Pp[4 * q + 3] = e ? v.w : Pp[4 * q + 3];
-            }
-            const uint32_t hm = hLM[rs * nw + warp];
-            Mp = e ? hm : Mp;
         } else if (col == 0) {
             const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
 #pragma unroll
@@ -644,17 +584,6 @@ vsweep_kernel(VArgs a)
                 for (int k = 0; k < NR; ++k) Pp[k] = 0u;
                 Mp = 0u;
             }
-        } else if (ASD_HALO_SEL) {
-            const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
-            const bool e = col == CPW - 1;
-#pragma unroll
-            for (int q = 0; q < NR / 4; ++q) {
-                const uint4 v = h[q];
-                Pp[4 * q] = e ? v.x : Pp[4 * q]; Pp[4 * q + 1] = e ? v.y : Pp[4 * q + 1];
-                Pp[4 * q + 2] = e ? v.z : Pp[4 * q + 2]; Pp[4 * q + 3] = e ? v.w : Pp[4 * q + 3];
-            }
-            const uint32_t hm = hRM[rs * nw + warp];
-            Mp = e ? hm : Mp;
         } else if (col == CPW - 1) {
             const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
 #pragma unroll
@@ -851,353 +780,6 @@ vsweep_kernel(VArgs a)
     if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
 }
 
-#if ASD_V2_DEC
-// ---------------------------------------------------------------- K_down / K_up, decoupled
-// The same sweeps with every warp autonomous except for its two neighbours:
-//  * inputs are staged per warp (census rows of its CPW columns and the T
-//    right-census slices they match, or its block of the K_down partials / CB
-//    rows) with cp.async groups into a warp-private ring -- no slot is shared,
-//    so no warp waits for another to drain it;
-//  * the diagonal halos go to the neighbour warp (or, at CTA edges, the
-//    neighbour CTA through DSMEM) and are signalled by an mbarrier per consumer
-//    warp and slot (count 1); neighbours are at most one row apart (each needs
-//    the other's previous row), so two slots suffice;
-//  * no CTA- or cluster-wide barrier inside the row loop.
-template <int DC, int T>
-struct DGeom {
-    static constexpr int NR = DC / 2;
-    static constexpr int CPW = 32 / T;
-    static constexpr int NSL = CPW + DC - 1;                              // words of one right slice
-    static constexpr int SS = CPW + 32 * ((NSL - CPW + 31) / 32);         // >= NSL, = CPW (mod 32)
-    static constexpr int CW = 32 + T * SS;                                // words per census slot
-    static constexpr int RW = CPW * DC * T / 2;                           // words per ring row (u16 x CPW x D)
-};
-constexpr int DNSLOT = 4;      // census rows in flight per warp (K_down)
-constexpr int DKR = 3;         // ring rows in flight per warp (K_up, BLK K_down)
-constexpr int DKR2 = 2;        // per ring when BLK K_up stages two (P_A and CB)
-
-template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false>
-__global__ void __launch_bounds__(DC == 32 ? 512 : 1024, 1)
-vsweep_dec_kernel(VArgs a)
-{
-    using G = DGeom<DC, T>;
-    constexpr int NR = G::NR, CPW = G::CPW, CW = G::CW, SS = G::SS, RW = G::RW;
-    constexpr bool RING = UP || BLK;
-    constexpr int NRING = (UP && BLK) ? 2 : 1;
-    constexpr int KR = (UP && BLK) ? DKR2 : DKR;
-    extern __shared__ uint32_t smem[];
-    const DevParams& p = a.p;
-    const int W = p.W, H = p.H, D = p.D;
-    const int nw = blockDim.x >> 5;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int col = lane / T, chunk = lane % T;
-    const int rank = blockIdx.x;
-    const int frame = blockIdx.y;
-    const int w = a.w;
-    const int x0 = rank * w;
-    const int xw0 = x0 + warp * CPW;                 // the warp's first column
-    const int xl = warp * CPW + col;
-    const int x = x0 + xl;
-    const bool clustered = NP == 3 && a.cs > 1;
-    const int wpad = a.cs * a.w;
-
-    // ---- shared memory (words): census ring | halos | K_up staging | input ring(s) | mbarriers
-    uint32_t* cen = smem;                                           // [nw][DNSLOT][CW]    (K_down, !BLK)
-    uint32_t* hL = cen + (RING ? 0 : nw * DNSLOT * CW);             // [2][nw][T][NR]      (NP == 3)
-    uint32_t* hR = hL + (NP == 3 ? 2 * nw * T * NR : 0);
-    uint32_t* hLM = hR + (NP == 3 ? 2 * nw * T * NR : 0);           // [2][nw]
-    uint32_t* hRM = hLM + (NP == 3 ? 2 * nw : 0);
-    uint32_t* stg0 = hRM + (NP == 3 ? 2 * nw : 0);                  // [nw][16 * DC]       (UP)
-    uint32_t* stg = stg0 + warp * (16 * DC);
-    uint32_t* rings = stg0 + (UP ? nw * 16 * DC : 0);               // [nw][NRING][KR][RW] (RING)
-    uint64_t* hb = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(rings + (RING ? nw * NRING * KR * RW : 0)) + 7) & ~uintptr_t(7));
-    uint64_t* hbL = hb;                                             // [2][nw]  halo "L" full, per consumer
-    uint64_t* hbR = hb + 2 * nw;                                    // [2][nw]  halo "R" full
-    uint32_t* cenw = cen + warp * DNSLOT * CW;
-    uint16_t* ringw = reinterpret_cast<uint16_t*>(rings + warp * NRING * KR * RW);
-
-    const uint32_t* cl = a.cl + frame * a.sig_stride;
-    const uint32_t* cr = a.cr + frame * a.sig_stride;
-    auto row_of = [&](int i) { return UP ? H - 1 - i : i; };
-
-    // ---- warp-private input staging (one cp.async group per row)
-    auto stage = [&](int i) {
-        __syncwarp();                                // lanes' earlier reads of the slot are done
-        if (i < H) {
-            ASD_JITTER(6);
-            const int yrow = row_of(i);
-            if constexpr (RING) {
-                const long long roff = ((long long)yrow * wpad + xw0) * D;
-                uint16_t* dst = ringw + (i % KR) * (2 * RW);
-#pragma unroll
-                for (int q = 0; q < DC / 8; ++q) {
-                    const int pc = 32 * q + lane;             // 16-byte piece of the warp's block
-                    if (UP) cp_async16(dst + 8 * pc, a.pin + frame * a.pa_stride + roff + 8 * pc);
-                    if (BLK) cp_async16(dst + (UP ? KR * 2 * RW : 0) + 8 * pc, a.cbin + frame * a.pa_stride + roff + 8 * pc);
-                }
-            } else {
-                uint32_t* sl = cenw + (i % DNSLOT) * CW;
-                const uint32_t* rl = cl + (long long)yrow * W;
-                const uint32_t* rr = cr + (long long)yrow * W;
-                if (lane < CPW) {
-                    const int gx = xw0 + lane;
-                    cp_async4(sl + lane, gx < W ? rl + gx : rl, gx < W);
-                }
-#pragma unroll
-                for (int k = 0; k < T; ++k) {
-                    const int g0 = RR ? xw0 + p.min_disp + DC * k : xw0 - p.min_disp - DC * k - (DC - 1);
-#pragma unroll
-                    for (int ii0 = 0; ii0 < G::NSL; ii0 += 32) {
-                        const int ii = ii0 + lane;
-                        if (ii < G::NSL) {
-                            const int gx = g0 + ii;
-                            const bool ok = gx >= 0 && gx < W;
-                            cp_async4(sl + 32 + k * SS + ii, ok ? rr + gx : rr, ok);
-                        }
-                    }
-                }
-            }
-        }
-        cp_async_commit();                           // one group per row (empty past the last)
-    };
-    constexpr int DEPTH = RING ? KR : DNSLOT;
-    auto ready = [&]() { cp_async_wait<DEPTH - 2>(); __syncwarp(); };
-
-    // ---- row i's costs (and K_up's P_A) from the warp's slot
-    const bool vcol = x >= p.R && x < W - p.R;
-    const bool xin = x < W;
-    uint32_t C[NR], PA[NR];
-    auto load_input = [&](int i) {
-        if constexpr (RING) {
-            const uint16_t* blk = ringw + (i % KR) * (2 * RW);
-            const uint4* src = reinterpret_cast<const uint4*>(blk) + lane;
-            const uint4* src2 = reinterpret_cast<const uint4*>(blk + (UP && BLK ? KR * 2 * RW : 0)) + lane;
-#pragma unroll
-            for (int q = 0; q < NR / 4; ++q) {
-                if constexpr (BLK) {
-                    const uint4 cv = src2[32 * q];
-                    C[4 * q] = cv.x; C[4 * q + 1] = cv.y; C[4 * q + 2] = cv.z; C[4 * q + 3] = cv.w;
-                    if constexpr (UP) {
-                        const uint4 v = src[32 * q];
-                        PA[4 * q] = v.x; PA[4 * q + 1] = v.y; PA[4 * q + 2] = v.z; PA[4 * q + 3] = v.w;
-                    }
-                } else {
-                    const uint4 v = src[32 * q];
-                    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        PA[4 * q + j] = w4[j] & 0x00FF00FFu;
-                        C[4 * q + j] = __byte_perm(w4[j], 0u, 0x4341);    // (C_lo, C_hi) as u16x2
-                    }
-                }
-            }
-        } else {
-            const int yrow = row_of(i);
-            const bool vx = vcol && yrow >= p.Q && yrow < H - p.Q;
-            const uint32_t nbnb = (uint32_t)p.nb * 0x10001u;
-            if (!vx) {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) C[k] = nbnb;
-                return;
-            }
-            const uint32_t* sl = cenw + (i % DNSLOT) * CW;
-            const uint32_t clv = sl[col];
-            constexpr int SG = RR ? 1 : -1;
-            // element of local disparity j (d = chunk * DC + j) at row[SG * j]
-            const uint32_t* row = sl + 32 + chunk * SS + col + (RR ? 0 : DC - 1);
-            const int lim = RR ? (W - p.R - 1) - (x + p.min_disp + chunk * DC)
-                               : x - p.min_disp - p.R - chunk * DC;
-            if (lim >= DC - 1) {
-#pragma unroll
-                for (int k = 0; k < NR; ++k)
-                    C[k] = __byte_perm(__popc(clv ^ row[SG * k]), __popc(clv ^ row[SG * (NR + k)]), 0x5410);
-            } else {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) {
-                    const uint32_t lo = k <= lim ? (uint32_t)__popc(clv ^ row[SG * k]) : (uint32_t)p.nb;
-                    const uint32_t hi = NR + k <= lim ? (uint32_t)__popc(clv ^ row[SG * (NR + k)]) : (uint32_t)p.nb;
-                    C[k] = __byte_perm(lo, hi, 0x5410);
-                }
-            }
-        }
-    };
-
-    // ---- halos (NP == 3): write targets of the edge lanes, fixed for the kernel
-    const int hslot = nw * T * NR;
-    uint32_t* wL = nullptr; uint32_t* wLm = nullptr;   // edge lane col == CPW-1 -> column x+1
-    uint32_t* wR = nullptr; uint32_t* wRm = nullptr;   // edge lane col == 0     -> column x-1
-    const bool recvL = NP == 3 && (warp > 0 || (clustered && rank > 0));
-    const bool recvR = NP == 3 && (warp < nw - 1 || (clustered && rank + 1 < a.cs));
-    const bool remoteL = clustered && warp == nw - 1 && rank + 1 < a.cs;   // I feed the next CTA
-    const bool remoteR = clustered && warp == 0 && rank > 0;               // I feed the previous CTA
-    uint32_t tgtL = 0, tgtR = 0;                     // the consumer's barrier, slot 0
-    if (NP == 3) {
-        cg::cluster_group cl_g = cg::this_cluster();
-        if (col == CPW - 1) {
-            if (warp + 1 < nw) { wL = hL + ((warp + 1) * T + chunk) * NR; wLm = hLM + warp + 1; }
-            else if (remoteL) { wL = cl_g.map_shared_rank(hL + chunk * NR, rank + 1); wLm = cl_g.map_shared_rank(hLM, rank + 1); }
-        }
-        if (col == 0) {
-            if (warp > 0) { wR = hR + ((warp - 1) * T + chunk) * NR; wRm = hRM + warp - 1; }
-            else if (remoteR) {
-                wR = cl_g.map_shared_rank(hR + ((nw - 1) * T + chunk) * NR, rank - 1);
-                wRm = cl_g.map_shared_rank(hRM + nw - 1, rank - 1);
-            }
-        }
-        if (recvR) tgtL = remoteL ? mapa_u32(hbL, (unsigned)(rank + 1)) : smem_u32(hbL + warp + 1);
-        if (recvL) tgtR = remoteR ? mapa_u32(hbR + nw - 1, (unsigned)(rank - 1)) : smem_u32(hbR + warp - 1);
-        for (int i = threadIdx.x; i < 4 * nw * T * NR + 4 * nw; i += blockDim.x) hL[i] = 0u;
-        if (threadIdx.x == 0) {
-            for (int s2 = 0; s2 < 4 * nw; ++s2) mbar_init(hb + s2, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        }
-        __syncthreads();
-        if (clustered) { cluster_arrive(); cluster_wait(); }   // neighbours' halos / barriers initialised
-    }
-
-    uint32_t Lv[NR], Ll[NR], Lr[NR];
-#pragma unroll
-    for (int k = 0; k < NR; ++k) { Lv[k] = 0u; Ll[k] = 0u; Lr[k] = 0u; }
-    uint32_t Mv = 0u, Ml = 0u, Mr = 0u;
-
-    for (int i0 = 0; i0 < DEPTH - 1; ++i0) stage(i0);
-    ready();
-    load_input(0);
-
-    for (int i = 0; i < H; ++i) {
-        const int y = row_of(i);
-        if (NP == 3) {
-            const int rs = (i + 1) & 1;                  // slot written at row i-1
-            if (i > 0) {
-                const unsigned ph = (unsigned)(((i - 1) >> 1) & 1);
-                if (recvL) { if (warp == 0) mbar_wait_remote(hbL + rs * nw + warp, ph); else mbar_wait(hbL + rs * nw + warp, ph); }
-                if (recvR) { if (warp == nw - 1) mbar_wait_remote(hbR + rs * nw + warp, ph); else mbar_wait(hbR + rs * nw + warp, ph); }
-                ASD_JITTER(2);
-            }
-            uint32_t Pp[NR], Mp;
-            // path "L": predecessor column x-1 (down-right / up-right)
-#pragma unroll
-            for (int k = 0; k < NR; ++k) Pp[k] = __shfl_up_sync(FULL, Ll[k], T);
-            Mp = __shfl_up_sync(FULL, Ml, T);
-            if (col == 0) {
-                const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * NR);
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) {
-                    const uint4 v = h[q];
-                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
-                }
-                Mp = hLM[rs * nw + warp];
-            }
-            path_update<NR, T>(p, chunk, Pp, Mp, C, Ll, Ml);
-            // path "R": predecessor column x+1 (down-left / up-left)
-#pragma unroll
-            for (int k = 0; k < NR; ++k) Pp[k] = __shfl_down_sync(FULL, Lr[k], T);
-            Mp = __shfl_down_sync(FULL, Mr, T);
-            if (col == CPW - 1) {
-                const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * NR);
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) {
-                    const uint4 v = h[q];
-                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
-                }
-                Mp = hRM[rs * nw + warp];
-            }
-            path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
-            if (!xin) {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) { Ll[k] = 0u; Lr[k] = 0u; }
-                Ml = Mr = 0u;
-            }
-            // ---- halos of row i (slot i & 1) and the consumers' signals
-            const int ws = i & 1;
-            ASD_JITTER(3);
-            if (wL) {
-                uint4* d4 = reinterpret_cast<uint4*>(wL + ws * hslot);
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]);
-                if (chunk == 0) wLm[ws * nw] = Ml;
-            }
-            if (wR) {
-                uint4* d4 = reinterpret_cast<uint4*>(wR + ws * hslot);
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
-                if (chunk == 0) wRm[ws * nw] = Mr;
-            }
-            if (remoteL || remoteR) fence_cluster();
-            __syncwarp();
-            if (lane == 0) {
-                const unsigned off = (unsigned)(ws * nw * 8);
-                if (recvR) { if (remoteL) mbar_arrive_remote_relaxed(tgtL + off); else mbar_arrive_local(tgtL + off); }
-                if (recvL) { if (remoteR) mbar_arrive_remote_relaxed(tgtR + off); else mbar_arrive_local(tgtR + off); }
-            }
-        }
-        // ---- vertical path: predecessor = own column
-        {
-            uint32_t Ln[NR], mnew;
-            path_update<NR, T>(p, chunk, Lv, Mv, C, Ln, mnew);
-#pragma unroll
-            for (int k = 0; k < NR; ++k) Lv[k] = xin ? Ln[k] : 0u;
-            Mv = xin ? mnew : 0u;
-        }
-        stage(i + DEPTH - 1);                            // into the slot row i-1 used
-        // ---- partial sum out
-        {
-            uint32_t sv[NR];
-#pragma unroll
-            for (int k = 0; k < NR; ++k) sv[k] = NP == 3 ? Lv[k] + Ll[k] + Lr[k] : Lv[k];
-            if (!UP) {
-                uint4* dst = reinterpret_cast<uint4*>(a.pouta + frame * a.pa_stride +
-                                                      ((long long)y * wpad + (x - col)) * D) + lane;
-                constexpr uint32_t CS = BLK ? 0u : 256u;
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q)
-                    dst[32 * q] = make_uint4(sv[4 * q] + C[4 * q] * CS, sv[4 * q + 1] + C[4 * q + 1] * CS,
-                                             sv[4 * q + 2] + C[4 * q + 2] * CS, sv[4 * q + 3] + C[4 * q + 3] * CS);
-            } else {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) sv[k] += PA[k] + C[k] * (BLK ? 0u : 512u);
-                uint32_t o[NR];
-                if (DPL_ROW == 4) {
-#pragma unroll
-                    for (int g = 0; g < DC / 4; ++g) {
-                        const int kk = 4 * g < NR ? 4 * g : 4 * g - NR;
-                        const uint32_t sel = 4 * g < NR ? 0x5410u : 0x7632u;
-                        o[2 * g] = __byte_perm(sv[kk], sv[kk + 2], sel);
-                        o[2 * g + 1] = __byte_perm(sv[kk + 1], sv[kk + 3], sel);
-                    }
-                } else {
-#pragma unroll
-                    for (int g = 0; g < DC / 2; ++g) {
-                        const int kk = 2 * g < NR ? 2 * g : 2 * g - NR;
-                        const uint32_t sel = 2 * g < NR ? 0x5410u : 0x7632u;
-                        o[g] = __byte_perm(sv[kk], sv[kk + 1], sel);
-                    }
-                }
-                constexpr int PPC = DC * T / 8;
-                constexpr int SWZ = (PPC < 8 ? PPC : 8) - 1;
-                uint4* sb = reinterpret_cast<uint4*>(stg);
-                const int pbase = col * PPC + chunk * (DC / 8);
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q)
-                    sb[(pbase + q) ^ (col & SWZ)] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-                __syncwarp();
-                uint4* dst = reinterpret_cast<uint4*>(a.pout16 + frame * a.cell_stride + ((long long)y * W + (x - col)) * D);
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) {
-                    const int pi = 32 * q + lane;
-                    if (x - col + pi / PPC < W) dst[pi] = sb[pi ^ ((pi / PPC) & SWZ)];
-                }
-                __syncwarp();
-            }
-        }
-        if (i + 1 < H) { ready(); ASD_JITTER(5); load_input(i + 1); }
-    }
-    cp_async_wait<0>();
-    if (clustered) { cluster_arrive(); cluster_wait(); }   // no CTA exits while a neighbour may still write it
-}
-
-#endif  // ASD_V2_DEC
 
 // ---------------------------------------------------------------- K_row
 struct RArgs {
@@ -1263,50 +845,11 @@ template <int D> struct RowGeom {
 #ifndef ASD_HROW_CFROMP
 #define ASD_HROW_CFROMP 0         // 1: the row kernel's left->right pass takes C from the P_AB | C words
 #endif
-#ifndef ASD_HROW_PF
-#define ASD_HROW_PF 0             // > 0: L2 bulk prefetch this many pixels ahead in the right->left pass
-#endif
-#ifndef ASD_WTA_LBM
-#define ASD_WTA_LBM 0             // 1: left view second-best from 8-disparity block minima (one pass)
-#endif
 template <int D, bool WIDE>
 __device__ __forceinline__ void wta_left_lane(const DevParams& p, uint16_t* r, int& dstar, bool& uf, float& disp)
 {
     constexpr int KS = RowGeom<D>::KS;
     const uint32_t* r32 = reinterpret_cast<const uint32_t*>(r);     // rows are 4-byte aligned
-    if constexpr (ASD_WTA_LBM && !WIDE && D % 8 == 0) {
-        // one pass: packed keys and the minimum S of each 8-disparity block;
-        // the second best over |d - d*| >= 2 from the blocks clear of
-        // d*-1..d*+1 and, element by element, the (one or two) blocks holding them
-        uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu, bm[D / 8];
-#pragma unroll
-        for (int q = 0; q < D; q += 4) {
-            const uint32_t v0 = r32[q / 2], v1 = r32[q / 2 + 1];
-            ka = vmin2(ka, v0 * (1u << KS) + ((uint32_t)q | ((uint32_t)(q + 1) << 16)));
-            kb2 = vmin2(kb2, v1 * (1u << KS) + ((uint32_t)(q + 2) | ((uint32_t)(q + 3) << 16)));
-            bm[q / 8] = (q % 8 == 0) ? vmin2(v0, v1) : vmin2(bm[q / 8], vmin2(v0, v1));
-        }
-        const uint32_t kmin = vmin2(ka, kb2);
-        const uint32_t kk = min(kmin & 0xFFFFu, kmin >> 16);
-        dstar = (int)(kk & ((1u << KS) - 1u));
-        const uint32_t s0 = kk >> KS;
-        const uint32_t cm = dstar >= 1 ? r[dstar - 1] : NONE16;
-        const uint32_t cp = dstar + 1 < D ? r[dstar + 1] : NONE16;
-        const int blo = max(dstar - 1, 0) >> 3, bhi = min(dstar + 1, D - 1) >> 3;
-        uint32_t sec = 0xFFFFFFFFu;
-#pragma unroll
-        for (int b = 0; b < D / 8; ++b)
-            if (b < blo || b > bhi) sec = vmin2(sec, bm[b]);
-        uint32_t s2 = min(sec & 0xFFFFu, sec >> 16);
-        for (int b = blo; b <= bhi; ++b)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int d = 8 * b + j;
-                if (d < dstar - 1 || d > dstar + 1) s2 = min(s2, (uint32_t)r[d]);
-            }
-        finish_wta(p, dstar, s0, s2, cm, cp, uf, disp);
-        return;
-    }
     uint32_t kb;
     if constexpr (WIDE) {
         uint32_t ka = 0xFFFFFFFFu, kb2 = 0xFFFFFFFFu;
@@ -1790,26 +1333,8 @@ hrow_kernel(RArgs a)
             if (xs + SG <= W) group(true, xs, PP, SS);
             else group(false, xs, PP, SS);
         };
-        // bulk L2 prefetch (one lane, TMA unit) of the P_AB | C words and the
-        // stash of the 2 SG pixels ASD_HROW_PF pixels ahead of the sweep
-        const uint16_t* pab_row = a.pab + frame * a.cell_stride + (long long)y * W * D;
-        const uint8_t* st_row = a.stash + frame * a.cell_stride + (long long)y * W * D;
-        auto prefetch = [&](int xs) {
-            if (ASD_HROW_PF > 0 && lane == 0) {
-                const int hi = xs - ASD_HROW_PF + SG, lo = max(hi - 2 * SG, 0);   // pixels [lo, hi)
-                if (hi > lo) {
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n"
-                                 :: "l"(pab_row + (long long)lo * D), "r"((unsigned)((hi - lo) * D * 2)) : "memory");
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n"
-                                 :: "l"(st_row + (long long)lo * D), "r"((unsigned)((hi - lo) * D)) : "memory");
-                }
-            }
-        };
-        if (ASD_HROW_PF > 0 && lane == 0)
-            for (int xs = xtop; xs > xtop - ASD_HROW_PF && xs >= 0; xs -= 2 * SG) prefetch(xs + ASD_HROW_PF);
         load_sg(xtop, P, Sx);
         for (int xs = xtop; xs >= 0; xs -= 2 * SG) {
-            prefetch(xs);
             load_sg(xs - SG, Pn, Sn);
             run_group(xs, P, Sx);
             if (xs - SG < 0) break;
@@ -2263,16 +1788,10 @@ using v2::RArgs;
 typedef void (*VKernel)(VArgs);
 typedef void (*RKernel)(RArgs);
 
-// the sweep kernel of this build: vsweep_dec_kernel (ASD_V2_DEC = 1, default)
-// or the round-1 barrier-per-row vsweep_kernel
 template <int DC, int T, int NP, bool UP, int DPL, bool RR = false, bool BLK = false, bool SEG = false>
 static VKernel vkern()
 {
-#if ASD_V2_DEC
-    return v2::vsweep_dec_kernel<DC, T, NP, UP, DPL, RR, BLK>;
-#else
     return v2::vsweep_kernel<DC, T, NP, UP, DPL, RR, BLK, SEG>;
-#endif
 }
 
 template <int DC, int T, int DPL, bool SEG>
@@ -2356,20 +1875,6 @@ static size_t vsmem_bytes(int w, int D, int T, int DC, int np, bool up, bool blk
     const int nw = w * T / 32;
     const bool ring = up || blk;
     size_t words = 0;
-#if ASD_V2_DEC
-    {                                                 // vsweep_dec_kernel's layout
-        const int cpw = 32 / T, nsl = cpw + DC - 1;
-        const int ss = cpw + 32 * ((nsl - cpw + 31) / 32);
-        const int cw = 32 + T * ss, rw = cpw * D / 2;
-        const int nring = (up && blk) ? 2 : 1, kr = (up && blk) ? v2::DKR2 : v2::DKR;
-        if (!ring) words += (size_t)nw * v2::DNSLOT * cw;
-        if (np == 3) words += 4 * (size_t)nw * T * (DC / 2) + 4 * (size_t)nw;
-        if (up) words += (size_t)nw * 16 * DC;
-        if (ring) words += (size_t)nw * nring * kr * rw;
-        words += 2 * (4 * (size_t)nw) + 2;            // halo mbarriers (+ align)
-        return words * 4;
-    }
-#endif
     const int cstr = ((w + DC - 1 + 31) / 32) * 32 + 32;
     words = ring ? 0 : (size_t)v2::NSLOT * ((size_t)w + (size_t)T * cstr);
     if (np == 3) words += 4 * (size_t)nw * T * (DC / 2 + 4) + 4 * (size_t)nw;   // halos (HS = NR + 4)
@@ -2499,7 +2004,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     }
     // one cluster per frame when it fits (measured: config C 1937 frames/s as
     // 10 x 1 vs 1390 as 5 x 4); otherwise the best-scoring segment count
-    if (nseg == 1 && best >= 0 && !ASD_V2_SEGSEARCH) break;
+    if (nseg == 1 && best >= 0) break;
     }
     if (best < 0) return no("no feasible cluster configuration");
     const bool segs = np == 3 && pl.ncta > pl.cs;
@@ -2526,7 +2031,7 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
     pl.wta_fb = false;
-    if ((ASD_WTA_FB256 && p.D > 128 && p.lr_mode == 0) || !wta2_plan(p, wide, pl)) {
+    if (!wta2_plan(p, wide, pl)) {
         // the window does not fit shared memory (D = 256): the warp-per-pixel
         // WTA kernel of engine D1 (post.cu) reads the same natural-order S
         if (p.lr_mode == 1) return no("min_disp + num_disp too large for the WTA window (R2)");
