@@ -60,6 +60,10 @@ FUZZ = [
     (200, 9, 128, 2, 9, 7, 8, 32, 8, 10, 1.0, 1),
     (33, 64, 112, 0, 3, 5, 1, 2, 4, 100, 0.0, 1),
     (16, 16, 16, 0, 15, 1, 200, 248, 8, 10, 1.0, 1),      # nb = 7, p2 near the u8 bound
+    (160, 40, 64, 8, 7, 7, 8, 32, 8, 10, 1.0, 1),          # TMA census staging with min_disp > 0
+    (264, 24, 128, 12, 9, 7, 8, 32, 8, 10, 1.0, 1),        # the same at D = 128, two CTAs
+    (96, 20, 96, 4, 9, 7, 10, 50, 8, 15, 1.5, 1),          # D = 96, P2 = 50 (u32 keys)
+    (300, 20, 256, 20, 5, 5, 8, 32, 4, 10, 1.0, 1),        # D = 256, 4 paths, min_disp 20
 ]
 
 
