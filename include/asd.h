@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define ASD_VERSION 2
+#define ASD_VERSION 3
 
 #define ASD_OK              0
 #define ASD_E_INVALID_ARG  (-1)  /* bad parameter, NULL required pointer, n out of range */
@@ -76,8 +76,8 @@ extern "C" {
  *       the hamming distance between the local regions of the two pixels";
  *       SPEC S:258; reading c19): odd, 1..15; 0 is read as 1.
  *       1 x 1 = plain SGM.  The cost becomes CB(x,y,d) = sum over the block
- *       of C(x+u, y+v, d), nb for block positions off the image.  A block
- *       larger than 1 x 1 runs on engine D1 (the D3 packing holds 8-bit costs).
+ *       of C(x+u, y+v, d), nb for block positions off the image.  Engine D3
+ *       runs SGBM at num_disp = 128 (u16-partial sweeps on CB), D1 otherwise.
  *   median_ksize: 0, 3 or 5 ("median filtering"; SPEC S:342-347;
  *       reading c20): after the LR check, a pixel with no BORDER/UNIQUE/LR bit
  *       takes the lower median of dl over the valid k x k neighbours (itself
@@ -85,17 +85,19 @@ extern "C" {
  *   lr_mode: right-view disparity for the LR check.  0 = R1 (reading c10,
  *       S:389): WTA on the re-indexed left aggregate S(x + delta, d).  1 = R2
  *       (reading c24): the right view runs its own SGM on
- *       C_R = hamming(cr(x), cl(x + delta)) (twice the aggregation work; engine
- *       D1). */
+ *       C_R = hamming(cr(x), cl(x + delta)) (twice the aggregation work; both
+ *       engines). */
 /* Aggregation designs:
  *   ASD_ENGINE_D1  one warp-per-line kernel per path direction, u16 S volume
  *                  read-modify-written in HBM (any configuration above)
  *   ASD_ENGINE_D3  grouped sweeps: cluster kernels for the 3 downward and 3
- *                  upward paths, a warp-per-row kernel for the 2 horizontal
- *                  paths fused with WTA/uniqueness/sub-pixel; the cost volume
- *                  and S are never materialised.  Envelope: nb <= 32,
- *                  num_disp in {16,32,64,128}, 3*(nb+p2) <= 255 (8-path),
- *                  paths*(nb+p2)*2^ceil(log2 num_disp) < 65535.
+ *                  upward paths (frames wider than one cluster span several,
+ *                  joined through global memory), a warp-per-row kernel for
+ *                  the 2 horizontal paths, a shared-memory window WTA; the cost
+ *                  volume is never materialised.  Envelope: nb <= 32,
+ *                  num_disp in {16,32,64,96,128,256}; 8-path with
+ *                  3*(nb+p2) > 255 (u16 partials) and SGBM only at
+ *                  num_disp = 128.  WTA keys widen to u32 automatically.
  *   ASD_ENGINE_AUTO D3 inside its envelope, else D1.                      */
 #define ASD_ENGINE_AUTO 0
 #define ASD_ENGINE_D1   1
@@ -169,12 +171,20 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out);
 /* Free the context and its scratch (synchronises the device first).  NULL ok. */
 void asd_destroy(asd_ctx* ctx);
 
-/* One frame: left/right u8 [H][W] -> out_disp, out_depth f32 [H][W].
- * Either output may be NULL (not written). */
+/* One frame: left/right u8 [H][W] -> out_disp, out_depth f32 [H][W] -- the
+ * whole path of PAPER.md P:289 (census, Hamming cost, SGM, WTA + uniqueness,
+ * sub-pixel, LR check, depth) with SPEC S:366-368's compute_depth semantics
+ * (disparity NaN where any mask bit is set; depth NaN where the disparity is
+ * invalid or <= 0).  Pointers: device memory, no alignment requirement.
+ * Either output may be NULL (not written).  ASD_E_INVALID_ARG for a NULL
+ * context or input. */
 int asd_depth(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
               float* out_disp, float* out_depth, void* cuda_stream);
 
-/* n frames (n >= 0), [n][H][W] each; stats ([n] asd_frame_stats) may be NULL. */
+/* n frames (n >= 0), [n][H][W] each, frames contiguous -- asd_depth per frame
+ * (P:289 stage list; datagen batches, BASELINE.json north_star), pipelined on
+ * the D3 engine; stats ([n] asd_frame_stats) may be NULL.
+ * Frames beyond max_batch run in chunks.  n = 0 enqueues nothing. */
 int asd_depth_batch(asd_ctx* ctx, int n, const uint8_t* left, const uint8_t* right,
                     float* out_disp, float* out_depth, asd_frame_stats* stats,
                     void* cuda_stream);
@@ -187,8 +197,10 @@ int asd_depth_batch_host(asd_ctx* ctx, int n, const uint8_t* left_host, const ui
                          float* out_disp_host, float* out_depth_host,
                          asd_frame_stats* stats_host, void* cuda_stream);
 
-/* One frame with stage outputs (see asd_debug_out); out_disp/out_depth via
- * asd_depth semantics may additionally be requested. */
+/* One frame with every stage's output (see asd_debug_out: the census of P:289 /
+ * S:291, the cost of S:300, S of S:309, the WTA maps of S:318-332, the LR mask
+ * of S:336-341); out_disp/out_depth via asd_depth semantics may additionally
+ * be requested.  For parity tests; not a fast path. */
 int asd_depth_debug(asd_ctx* ctx, const uint8_t* left, const uint8_t* right,
                     const asd_debug_out* outs, float* out_disp, float* out_depth,
                     void* cuda_stream);
@@ -208,8 +220,10 @@ int asd_frames_per_wave(const asd_ctx* ctx);
  * max_batch / group scratch slots; the cluster sweeps of one group overlap the
  * row/WTA/LR passes of the previous one on the SMs the clusters leave free.
  * Default: one wave (asd_frames_per_wave, capped at max_batch).  group must be
- * in [1, max_batch]; asd_set_group synchronises the device first.  Returns
- * ASD_OK or ASD_E_INVALID_ARG / ASD_E_CUDA.  D1 ignores it. */
+ * in [1, max_batch] -- and at most one wave when a frame spans several
+ * clusters (their boundary columns wait on each other, so every cluster of a
+ * group must be resident at once); asd_set_group synchronises the device
+ * first.  Returns ASD_OK or ASD_E_INVALID_ARG / ASD_E_CUDA.  D1 ignores it. */
 int asd_set_group(asd_ctx* ctx, int group);
 int asd_group(const asd_ctx* ctx);
 

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_version_and_strerror(lib):
-    assert lib.asd_version() == 2
+    assert lib.asd_version() == 3
     assert lib.asd_strerror(0) == b"ok"
     assert lib.asd_strerror(-2) == b"unsupported configuration"
 
