@@ -151,18 +151,36 @@ struct VArgs {
 // ---------------------------------------------------------------- helpers
 // u16x2 minimum of N registers as a balanced tree (any N: each level folds the
 // upper ceil-half onto the lower half)
+#ifndef ASD_TREE3
+#define ASD_TREE3 1
+#endif
 template <int N>
 __device__ __forceinline__ uint32_t tree_min(const uint32_t (&v)[N])
 {
-    uint32_t tr[N];
+    if constexpr (N == 1) {
+        return v[0];
+    } else if constexpr (ASD_TREE3 && N > 2) {
+        // three-input levels (VIMNMX3): 16 registers in 5 + 2 + 1 = 8 minima
+        constexpr int M = (N + 2) / 3;
+        uint32_t t[M];
 #pragma unroll
-    for (int k = 0; k < N; ++k) tr[k] = v[k];
+        for (int i = 0; i < M; ++i) {
+            if (3 * i + 2 < N) t[i] = vmin2(vmin2(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+            else if (3 * i + 1 < N) t[i] = vmin2(v[3 * i], v[3 * i + 1]);
+            else t[i] = v[3 * i];
+        }
+        return tree_min<M>(t);
+    } else {
+        uint32_t tr[N];
 #pragma unroll
-    for (int n = N; n > 1; n = (n + 1) / 2) {
+        for (int k = 0; k < N; ++k) tr[k] = v[k];
 #pragma unroll
-        for (int k = 0; k < n / 2; ++k) tr[k] = vmin2(tr[k], tr[k + (n + 1) / 2]);
+        for (int n = N; n > 1; n = (n + 1) / 2) {
+#pragma unroll
+            for (int k = 0; k < n / 2; ++k) tr[k] = vmin2(tr[k], tr[k + (n + 1) / 2]);
+        }
+        return tr[0];
     }
-    return tr[0];
 }
 
 // Mp is the predecessor's min over d packed in both halves (M | M << 16);
