@@ -36,7 +36,7 @@ METRIC_D = "frames/s and Gcell/s (W·H·D) at 1920×1080×D256 8-path (config D)
 FRAMES_PER_STEP = 128          # inputs 128 x 2 x 0.92 MB = 236 MB per step > 126 MB L2
 POOL = 8                       # distinct synthetic frames (kernels are data-oblivious)
 CRITICAL = ("census", "block", "down", "up")   # D3 stages on the high-priority streams (s_cen, s_hi)
-MAX_BATCH = 32                 # frames in flight per asd_depth_batch chunk
+MAX_BATCH = 33                 # frames in flight: three D3 waves (three scratch slots: e2e 1836 -> 1900 vs two)
 
 
 KERNEL_NAMES = {"census": "census_kernel (K1)", "dir": "sgm_dir_kernel (D1, one path direction)",
@@ -511,7 +511,7 @@ def main():
     ap.add_argument("--impl", default="asd", choices=["asd", "reference"])
     ap.add_argument("--frames", type=int, default=FRAMES_PER_STEP, help="frames per step per GPU")
     ap.add_argument("--max-batch", type=int, default=0,
-                    help="frames per asd_depth_batch chunk (0: a whole number of cluster waves, ~32)")
+                    help="frames in flight (0: a whole number of cluster waves, ~33 = 3 slots at config C)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gate", action="store_true", help="skip the D1 aggregation-kernel HBM gate measurement")
