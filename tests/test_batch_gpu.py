@@ -74,18 +74,18 @@ def test_host_path_matches_device_path():
 
 
 def test_config_C_batch_launch_config():
-    """Config C in bench.py's launch configuration: max_batch 22 = two scratch
-    slots of one 11-frame cluster wave each, so a 35-frame batch runs 4 groups
-    (11, 11, 11, 2: both slots reused, the last group ragged) through the
+    """Config C in bench.py's launch configuration: max_batch 33 = three scratch
+    slots of one 11-frame cluster wave each, so a 46-frame batch runs 5 groups
+    (11, 11, 11, 11, 2: slots reused, the last group ragged) through the
     three-stream pipeline with event-ordered slot recycling.  Every frame's
     (checksum, valid) is compared with the oracle (frame i = pool[i % 8], as in
-    bench.py); frames 0, 11, 22 and 34 (the first of each slot use and the
+    bench.py); frames 0, 11, 33 and 45 (first uses, a reused slot and the
     ragged tail) also bit for bit on disp and to 1e-5 on depth."""
     import torch
     from tests.gpu_util import oracle_frames, oracle_sig
     cfg = synth.CONFIGS["C"]
     d = cfg.params_dict()
-    n, mb, pool = 35, 22, 8
+    n, mb, pool = 46, 33, 8
     PL, PR = synth.frame_pool(cfg, pool)
     idx = [i % pool for i in range(n)]
     L, R = torch.from_numpy(PL[idx]).cuda(), torch.from_numpy(PR[idx]).cuda()
@@ -102,7 +102,7 @@ def test_config_C_batch_launch_config():
     s = stats.cpu().numpy()
     bad = [i for i in range(n) if (int(s[i, 0]) & 0xFFFFFFFF, int(s[i, 1])) != sigs[i % pool]]
     assert not bad, f"frames differing from the oracle: {bad}"
-    for i in (0, 11, 22, 34):
+    for i in (0, 11, 33, 45):
         o = outs[i % pool]
         assert_bits_equal(disp[i].cpu().numpy(), o["disp"], f"disp frame {i}")
         assert_depth_close(depth[i].cpu().numpy(), o["depth"])
@@ -110,7 +110,7 @@ def test_config_C_batch_launch_config():
 
 def test_config_E_job_checksums():
     """Config E: a 4096-frame job of config-C frames (frame f = pool[f % 8]) in
-    chunks of bench.py's max_batch (22, two slots) -- every frame's (checksum,
+    chunks of bench.py's max_batch (33, three slots) -- every frame's (checksum,
     valid) against the oracle (SURVEY §8(d) E, §8(e) checksum)."""
     import torch
     from tests.gpu_util import oracle_frames, oracle_sig
@@ -121,7 +121,7 @@ def test_config_E_job_checksums():
     idx = [i % pool for i in range(n)]
     L, R = torch.from_numpy(PL[idx]).cuda(), torch.from_numpy(PR[idx]).cuda()
     stats = torch.zeros(n, 4, dtype=torch.int32, device="cuda")
-    with asd.Stereo(asd.Params(**d), 0, 22) as st:
+    with asd.Stereo(asd.Params(**d), 0, 33) as st:
         st.asd_depth_batch(L, R, None, None, stats)
         torch.cuda.synchronize()
     sigs = [oracle_sig(o) for o in oracle_frames(d, PL, PR)]
