@@ -1489,8 +1489,7 @@ constexpr int WTA_WARPS = ASD_WTA_WARPS;
 #define ASD_WTA_SPLIT 1
 #endif
 constexpr bool WTA_SPLIT = ASD_WTA_SPLIT;
-constexpr int WTA_TX = 32 * WTA_WARPS;
-// D = 256 (engine D1 only): stages of 128 pixels (4 warps) so the window fits
+// D = 256: stages of 128 pixels (4 warps) so the full-width window fits
 __host__ __device__ constexpr int wta_warps(int D) { return D > 128 ? (WTA_WARPS < 4 ? WTA_WARPS : 4) : WTA_WARPS; }
 
 
@@ -1715,7 +1714,7 @@ wta_halves_kernel(RArgs a)
     const DevParams& p = a.p;
     const int W = p.W, md = p.min_disp;
     const int y = blockIdx.x, frame = blockIdx.y;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const uint16_t* S = a.pab + frame * a.cell_stride + (long long)y * W * D;
     const bool vrow = y >= p.Q && y < p.H - p.Q;
     for (int xr = max(0, W - md) + tid; xr < W; xr += blockDim.x) {   // no disparity defined
