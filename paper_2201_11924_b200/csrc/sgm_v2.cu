@@ -2048,7 +2048,10 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
         if (pl.cs > 8) cudaFuncSetAttribute((const void*)kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
     pl.wta_fb = false;
-    if (!wta2_plan(p, wide, pl)) {
+    // the half-window D = 256 WTA also on D3 when the sweeps use no clusters
+    // (4 paths: Table II D = 256 1851 -> 2001); with 15-CTA clusters it
+    // delays their placement (config D 297 vs 307)
+    if (!wta2_plan(p, wide, pl, np == 1)) {
         // the window does not fit shared memory (D = 256): the warp-per-pixel
         // WTA kernel of engine D1 (post.cu) reads the same natural-order S
         if (p.lr_mode == 1) return no("min_disp + num_disp too large for the WTA window (R2)");
@@ -2075,9 +2078,9 @@ size_t v2_ghalo_bytes(const V2Plan& pl, int nframes)
 bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl, bool halves_ok)
 {
     if (!pick_wkernel(p.D, wide)) return false;
-    // wta_halves_kernel (half-width windows): engine D1 only -- in the D3
-    // pipeline its 2 x 100 KB CTAs per SM delay the sweep clusters (config D
-    // 297 vs 307 frames/s), while D1 runs its stages one after another (233 -> 246)
+    // wta_halves_kernel (half-width windows): engine D1 and 4-path D3 -- in the
+    // 8-path D3 pipeline its 2 x 100 KB CTAs per SM delay the sweep clusters
+    // (config D 297 vs 307 frames/s); D1 runs its stages one after another (233 -> 246)
     pl.halves = ASD_WTA_HALVES && halves_ok && p.D == 256 && p.lr_mode == 0;
     if (pl.halves) {
         pl.nbuf = ((256 + p.min_disp + 128 + 31) / 32) * 32;
