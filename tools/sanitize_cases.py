@@ -68,6 +68,12 @@ def cases():
         # config C in bench.py's pipeline: 24 frames over two 11-frame slots
         # (groups 11, 11, 2), 4 distinct frames
         "C_d3": (_cfg("C", engine=3), 24, 22, None),
+        # frames wider than one cluster: two clusters joined through global
+        # memory (segment-boundary counters), D = 128 and D = 256
+        "seg128_d3": ({**_cfg("C"), "width": 2100, "height": 40, "focal_px": 430.0 * 2100 / 424,
+                       "engine": 3}, 4, 4, None),
+        "seg256_d3": ({**_cfg("C"), "width": 1100, "height": 48, "num_disp": 256,
+                       "focal_px": 430.0 * 1100 / 424 * 2, "engine": 3}, 4, 4, None),
     }
 
 
