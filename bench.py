@@ -193,11 +193,17 @@ def workload(block: int, lr_mode: int = 0, median: int = 0, cfg_name: str = "C")
 
 
 # ----------------------------------------------------------------- oracle (CPU)
-def oracle_workers():
+def oracle_workers(params: dict | None = None):
+    """Host threads for the oracle: all cores, at most 32, and as many frames as
+    fit in half the free host memory (the oracle holds ~13 B per cell: the u8
+    cost, u32 block cost and u32 aggregate volumes)."""
     cores = len(os.sched_getaffinity(0))
+    cells = 1280 * 720 * 128
+    if params:
+        cells = params["width"] * params["height"] * params["num_disp"]
     try:
         import psutil
-        mem_frames = int(psutil.virtual_memory().available // (1.6e9))
+        mem_frames = int(0.5 * psutil.virtual_memory().available // (13.0 * cells + 64e6))
     except Exception:
         mem_frames = 8
     return max(1, min(cores, mem_frames, 32)), cores
@@ -240,7 +246,7 @@ def cpu_baseline(params, Ls, Rs, cfg_name="C"):
     """The oracle timed on the host cores (one full frame per thread); also
     returns the (checksum, valid) of every pool frame it computed, which the
     parity check of the GPU frames reuses."""
-    nworkers, cores = oracle_workers()
+    nworkers, cores = oracle_workers(params)
     wall, outs = oracle_frames_parallel(params, Ls, Rs, nworkers)
     sigs = {i % len(Ls): _oracle_sig(o) for i, o in enumerate(outs)}
     return {"value": round(nworkers / wall, 4), "unit": "frames/s", "cores": nworkers,
@@ -258,7 +264,7 @@ def oracle_pool_sigs(params, Ls, Rs, have: dict | None = None) -> dict:
     todo = [i for i in range(len(Ls)) if i not in sigs]
     if not todo:
         return sigs
-    nworkers, _ = oracle_workers()
+    nworkers, _ = oracle_workers(params)
     p = oracle_params(params)
     oracle.lib()
     for k in range(0, len(todo), nworkers):
@@ -300,7 +306,7 @@ def run_reference(args):
     if args.p2:
         params["p2"] = args.p2
     Ls, Rs = synth.frame_pool(cfg, min(POOL, 4))
-    nworkers, cores = oracle_workers()
+    nworkers, cores = oracle_workers(params)
     for _ in range(args.warmup):
         oracle_frames_parallel(params, Ls, Rs, nworkers)
     tot = 0.0
