@@ -37,6 +37,9 @@ CASES = [
     (260, 15, 144, 20, 9, 7, 8, 1, 0, 0),     # D = 144: 8 per lane, 18 active lanes, min_disp 20
     (60, 12, 240, 0, 5, 5, 4, 1, 0, 1),       # D = 240 > W: every matched window range is partial
     (75, 14, 112, 33, 7, 5, 8, 3, 0, 0),      # D = 112 SGBM (cost from CB), min_disp 33
+    # round 2: D3 at D = 256 with R2 + median, and SGBM + median + R2 on a frame spanning two clusters
+    (200, 20, 256, 0, 9, 7, 8, 1, 3, 1),
+    (2100, 9, 128, 0, 9, 7, 8, 3, 5, 1),
 ]
 
 
