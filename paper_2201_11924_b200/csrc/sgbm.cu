@@ -17,7 +17,10 @@
 
 namespace asd {
 
-constexpr int SB_RY = 16;            // rows per CTA (the block sum slides down them)
+#ifndef ASD_BC_RY
+#define ASD_BC_RY 32              // rows per CTA (16: 1285, 8: 1259 frames/s SGBM 3x3)
+#endif
+constexpr int SB_RY = ASD_BC_RY;     // rows per CTA (the block sum slides down them)
 
 // RR: the right view is the reference (R2, reading c24): cl_base / cr_base are
 // then the reference and matched census and the matched column is x' + delta.
@@ -36,8 +39,14 @@ constexpr int SB_RY = 16;            // rows per CTA (the block sum slides down 
 // then lives in registers (fully unrolled over the TX + BW - 1 block columns)
 // and invalid census words carry bit 31 (MARK; needs nb <= 31) instead of
 // separate validity flags.  BW == 0: the generic form.
+#ifndef ASD_BC_MINB
+#define ASD_BC_MINB 1             // min resident CTAs (of D threads) per SM for the block cost kernel
+#endif
+#ifndef ASD_BC_TX
+#define ASD_BC_TX 16              // pixels per CTA row (the CB accumulators per thread; 32: 1162 vs 1275 frames/s SGBM 3x3)
+#endif
 template <typename SigT, bool RR, int TX, bool PRIV, int BW = 0>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, ASD_BC_MINB)
 block_cost_kernel(DevParams p, const SigT* __restrict__ cl_base, const SigT* __restrict__ cr_base,
                   long long sig_stride, uint16_t* __restrict__ cb_base, long long cell_stride, int wpad)
 {
@@ -189,7 +198,7 @@ template <typename SigT, bool RR, bool PRIV>
 static void launch_bc_tx(const DevParams& p, int nframes, const void* ref, const void* mat,
                          long long sig_stride, uint16_t* cb, long long cell_stride, int wpad, cudaStream_t s)
 {
-    if (!launch_bc<SigT, RR, 32, PRIV>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wpad, s))
+    if (!launch_bc<SigT, RR, ASD_BC_TX, PRIV>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wpad, s))
         launch_bc<SigT, RR, 8, PRIV>(p, nframes, ref, mat, sig_stride, cb, cell_stride, wpad, s);
 }
 

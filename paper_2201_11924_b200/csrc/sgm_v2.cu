@@ -242,6 +242,9 @@ __device__ __forceinline__ int stg_swz(int pi)
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
 // experiment switches (A/B builds, tools/ab_bench.sh); production uses the defaults
+#ifndef ASD_HROWB_SG
+#define ASD_HROWB_SG 4            // SGBM row pass: pixels per register-buffered load group
+#endif
 #ifndef ASD_CEN_TMA
 #define ASD_CEN_TMA 1             // K_down census rows by TMA bulk copies (one thread) instead of cp.async
 #endif
@@ -1372,7 +1375,7 @@ __global__ void __launch_bounds__(32 * HROW_WARPS, 4)
 hrow_blk_kernel(RArgs a)
 {
     static_assert(D == 128, "SGBM row pass: D = 128 only");
-    constexpr int NRR = 2, SG = 4;
+    constexpr int NRR = 2, SG = ASD_HROWB_SG;
     const DevParams& p = a.p;
     const int W = p.W, H = p.H;
     const int frame = blockIdx.y;
