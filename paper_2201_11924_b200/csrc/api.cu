@@ -592,7 +592,7 @@ void free_ctx(asd_ctx* c)
 {
     if (!c) return;
     void* ptrs[] = {c->census_l_base, c->census_r_base, c->S, c->SR, c->cb, c->cb2, c->dl, c->dr, c->dstar_l, c->dstar_r,
-                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->plan.gflag, c->plan.ghalo,
+                    c->mask_l, c->mask_r, c->pa, c->pab, c->stash, c->pa2, c->pab2, c->stash2, c->plan.ghalo,
                     c->stage_in[0], c->stage_in[1], c->stage_out[0],
                     c->stage_out[1], c->stage_stats[0], c->stage_stats[1]};
     for (void* q : ptrs) if (q) cudaFree(q);
@@ -641,7 +641,7 @@ size_t asd_scratch_bytes(const asd_params* p, int max_batch)
         V2Plan pl;
         if (v2_plan(d, dev, pl))
             return layout(d, max_batch, ASD_ENGINE_D3, pl.ncta * pl.w, pl.blk).total +
-                   v2_gflag_bytes(pl, max_batch) + v2_ghalo_bytes(pl, max_batch) +
+                   v2_ghalo_bytes(pl, max_batch) +
                    4 * align_up((size_t)4 * ((size_t)d.min_disp + d.D + 1024 + 64));   // census guards
         cudaGetLastError();
     }
@@ -722,10 +722,8 @@ int asd_create(const asd_params* p, int device, int max_batch, asd_ctx** out)
         alloc((void**)&c->pab2, L.pab);
         alloc((void**)&c->stash2, L.stash);
     }
-    if (c->engine == ASD_ENGINE_D3 && v2_gflag_bytes(c->plan, max_batch) > 0) {
-        alloc((void**)&c->plan.gflag, v2_gflag_bytes(c->plan, max_batch));
+    if (c->engine == ASD_ENGINE_D3 && v2_ghalo_bytes(c->plan, max_batch) > 0)
         alloc((void**)&c->plan.ghalo, v2_ghalo_bytes(c->plan, max_batch));
-    }
     alloc((void**)&c->dl, L.px_f32); alloc((void**)&c->dr, L.px_f32);
     alloc((void**)&c->dstar_l, L.px_i16); alloc((void**)&c->dstar_r, L.px_i16);
     alloc((void**)&c->mask_l, L.px_u8); alloc((void**)&c->mask_r, L.px_u8);

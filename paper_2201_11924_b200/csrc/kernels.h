@@ -64,16 +64,14 @@ struct V2Plan {
     bool halves;      // D = 256 (R1): wta_halves_kernel, three passes over half-width windows
     bool tma_cen;     // K_down stages census rows with TMA bulk copies (needs guarded census buffers)
     int ncta;         // sweep CTAs per frame: cs (one cluster) or nseg * cs (frame wider than a cluster)
-    uint32_t* gflag;  // segment-boundary row counters / halos (owned by the context; nseg > 1)
-    uint32_t* ghalo;
+    unsigned long long* ghalo;   // segment-boundary tagged halos (owned by the context; nseg > 1)
     char why[128];
 };
 bool v2_plan(const DevParams& p, int device, V2Plan& pl);
 // The ring-window WTA kernel alone (also used by engine D1 when D is 16..128):
 // fills nbuf / bstride / rsmem / wide; false if the window does not fit.
 bool wta2_plan(const DevParams& p, bool wide, V2Plan& pl, bool halves_ok = false);
-// device bytes of the segment-boundary counters / halos for nframes frames (0 if nseg == 1)
-size_t v2_gflag_bytes(const V2Plan& pl, int nframes);
+// device bytes of the segment-boundary halos for nframes frames (0 if nseg == 1)
 size_t v2_ghalo_bytes(const V2Plan& pl, int nframes);
 void launch_wta2(const DevParams& p, const V2Plan& pl, int nframes, const uint16_t* S, long long cell_stride,
                  const FrameScratch& fs, long long px_stride, cudaStream_t s);

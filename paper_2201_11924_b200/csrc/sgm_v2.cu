@@ -133,11 +133,12 @@ struct VArgs {
     const uint16_t* cbin;     // BLK: SGBM block cost, K_down's private layout (frame stride pa_stride)
     // frames wider than one cluster (ncta > cs): nseg = ncta / cs clusters per
     // frame ("segments"); the diagonal halos of the CTAs at a segment boundary
-    // go through global memory with a per-row flag (gflag, release / acquire)
+    // go through global memory as tagged words (ghalo: each u64 = the row
+    // number + 1 in the high half, a 32-bit state word in the low half; zeroed
+    // before each launch), so neither side needs a fence or a flag
     int ncta;                 // CTAs per frame (= cs for a frame in one cluster)
     int tma_cen;              // K_down: census rows staged by TMA bulk copies (guarded census buffers)
-    uint32_t* gflag;          // [frames][nseg-1][2 dirs][8] row counters (zeroed before each launch)
-    uint32_t* ghalo;          // [frames][nseg-1][2 dirs][2 slots][T][NR + 4]
+    unsigned long long* ghalo;   // [frames][nseg-1][2 dirs][2 slots][T][NR + 2]
 };
 
 // Ablation switches exist only in experiment builds (-DASD_ABLATE); in the
@@ -286,6 +287,245 @@ struct VGeom {
 // at their boundaries -- a separate instance, so frames in one cluster carry no
 // trace of it (a data-dependent wait loop in the row loop makes the compiler
 // guard every shuffle with WARPSYNC)
+// Segment-boundary receive (SEG instances, every warp calls it; gw is
+// warp-uniform): the receiving lanes copy NQ pairs of tagged words from src
+// to a private shared stage with cp.async (all in flight at once, no
+// registers held), then move their low halves to dst; the warp retries until
+// every tag equals `tag` (and traps after 2^24 tries instead of hanging).  The loop lives in one asm block (uniform branches
+// only), so no data-dependent loop encloses the row's shuffles.
+template <int NQ> struct GsegRecv;
+template <> struct GsegRecv<5> {
+    static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
+                                               unsigned tag, unsigned stage)
+    {
+        asm volatile("{\n"
+                     " .reg .pred R, P, Q;\n"
+                     " .reg .b64 A, B;\n"
+                     " .reg .b32 a0, a1, b0, b1, N;\n"
+                     " setp.eq.u32 Q, %0, 0;\n"
+                     " @Q bra.uni GD_%=;\n"
+                     " setp.ne.u32 R, %1, 0;\n"
+                     " mov.b32 N, 0;\n"
+                     "GR_%=:\n"
+                     " @R cp.async.cg.shared.global [%5+0], [%2+0], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+16], [%2+16], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+32], [%2+32], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+48], [%2+48], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+64], [%2+64], 16;\n"
+                     " cp.async.commit_group;\n"
+                     " cp.async.wait_group 0;\n"
+                     " setp.ne.u32 P, %1, %1;\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+0];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+0], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+16];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+8], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+32];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+16], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+48];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+24], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+64];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+32], {a0, b0};\n"
+                     " vote.sync.any.pred Q, P, 0xffffffff;\n"
+                     " add.u32 N, N, 1;\n"
+                     " setp.gt.and.u32 P, N, 16777216, Q;\n"
+                     " @P trap;\n"
+                     " @Q bra.uni GR_%=;\n"
+                     "GD_%=:\n"
+                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage)
+                     : "memory");
+    }
+};
+template <> struct GsegRecv<7> {
+    static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
+                                               unsigned tag, unsigned stage)
+    {
+        asm volatile("{\n"
+                     " .reg .pred R, P, Q;\n"
+                     " .reg .b64 A, B;\n"
+                     " .reg .b32 a0, a1, b0, b1, N;\n"
+                     " setp.eq.u32 Q, %0, 0;\n"
+                     " @Q bra.uni GD_%=;\n"
+                     " setp.ne.u32 R, %1, 0;\n"
+                     " mov.b32 N, 0;\n"
+                     "GR_%=:\n"
+                     " @R cp.async.cg.shared.global [%5+0], [%2+0], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+16], [%2+16], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+32], [%2+32], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+48], [%2+48], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+64], [%2+64], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+80], [%2+80], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+96], [%2+96], 16;\n"
+                     " cp.async.commit_group;\n"
+                     " cp.async.wait_group 0;\n"
+                     " setp.ne.u32 P, %1, %1;\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+0];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+0], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+16];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+8], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+32];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+16], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+48];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+24], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+64];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+32], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+80];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+40], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+96];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+48], {a0, b0};\n"
+                     " vote.sync.any.pred Q, P, 0xffffffff;\n"
+                     " add.u32 N, N, 1;\n"
+                     " setp.gt.and.u32 P, N, 16777216, Q;\n"
+                     " @P trap;\n"
+                     " @Q bra.uni GR_%=;\n"
+                     "GD_%=:\n"
+                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage)
+                     : "memory");
+    }
+};
+template <> struct GsegRecv<9> {
+    static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
+                                               unsigned tag, unsigned stage)
+    {
+        asm volatile("{\n"
+                     " .reg .pred R, P, Q;\n"
+                     " .reg .b64 A, B;\n"
+                     " .reg .b32 a0, a1, b0, b1, N;\n"
+                     " setp.eq.u32 Q, %0, 0;\n"
+                     " @Q bra.uni GD_%=;\n"
+                     " setp.ne.u32 R, %1, 0;\n"
+                     " mov.b32 N, 0;\n"
+                     "GR_%=:\n"
+                     " @R cp.async.cg.shared.global [%5+0], [%2+0], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+16], [%2+16], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+32], [%2+32], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+48], [%2+48], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+64], [%2+64], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+80], [%2+80], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+96], [%2+96], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+112], [%2+112], 16;\n"
+                     " @R cp.async.cg.shared.global [%5+128], [%2+128], 16;\n"
+                     " cp.async.commit_group;\n"
+                     " cp.async.wait_group 0;\n"
+                     " setp.ne.u32 P, %1, %1;\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+0];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+0], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+16];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+8], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+32];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+16], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+48];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+24], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+64];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+32], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+80];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+40], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+96];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+48], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+112];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+56], {a0, b0};\n"
+                     " @R ld.shared.v2.b64 {A, B}, [%5+128];\n"
+                     " @R mov.b64 {a0, a1}, A;\n"
+                     " @R mov.b64 {b0, b1}, B;\n"
+                     " @R setp.ne.or.u32 P, a1, %4, P;\n"
+                     " @R setp.ne.or.u32 P, b1, %4, P;\n"
+                     " @R st.shared.v2.b32 [%3+64], {a0, b0};\n"
+                     " vote.sync.any.pred Q, P, 0xffffffff;\n"
+                     " add.u32 N, N, 1;\n"
+                     " setp.gt.and.u32 P, N, 16777216, Q;\n"
+                     " @P trap;\n"
+                     " @Q bra.uni GR_%=;\n"
+                     "GD_%=:\n"
+                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage)
+                     : "memory");
+    }
+};
+template <int NQ>
+__device__ __forceinline__ void gseg_recv(bool gw, bool recv, const unsigned long long* src, unsigned dst,
+                                          unsigned tag, unsigned stage)
+{
+    GsegRecv<NQ>::run(gw, recv, src, dst, tag, stage);
+}
+
 template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false, bool SEG = false>
 __global__ void __launch_bounds__(DC >= 24 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
@@ -312,6 +552,9 @@ vsweep_kernel(VArgs a)
     const bool clustered = NP == 3 && a.cs > 1 && !ABL(a, 1);
 
     const int nslot = (UP || BLK) ? 0 : NSLOT;
+    // the TMA-issuing thread (a middle warp instead measured slower: config C
+    // 1821 vs 1956 frames/s, and no faster with segments)
+    constexpr int tma_thread = 0;
     constexpr bool RING = UP || BLK;                 // TMA ring(s) of per-row input blocks
     constexpr int KR = (UP && BLK) ? 2 : KU;         // ring depth (two rings in BLK K_up)
     constexpr int NRING = (UP && BLK) ? 2 : 1;
@@ -329,7 +572,9 @@ vsweep_kernel(VArgs a)
     uint32_t* stg = stg0 + warp * (16 * DC);
     // input ring(s): KR rows of this CTA's (w columns x D) u16 block, TMA-loaded
     // (K_up: P_A | C, or P_A then CB for BLK; BLK K_down: CB)
-    uint16_t* ring = reinterpret_cast<uint16_t*>(stg0 + (UP ? nw * 16 * DC : 0));
+    // (after the staging blocks in every instance: the blocks double as the
+    // segment-boundary receive stage, also in K_down)
+    uint16_t* ring = reinterpret_cast<uint16_t*>(stg0 + nw * 16 * DC);
     uint16_t* ring2 = ring + KR * w * D;             // BLK K_up: the CB ring
     uint64_t* mbar = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(ring + (RING ? NRING * KR * w * D : 0)) + 7) & ~uintptr_t(7));
@@ -367,7 +612,7 @@ vsweep_kernel(VArgs a)
             // 16-byte aligned starts (the slices from cshift words before their
             // first column; columns outside the image are read from the guard
             // bands / neighbouring rows and never used: the cost masks them)
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == tma_thread) {
                 const unsigned nal = (unsigned)((w + DC - 1 + cshift + 3) & ~3);
                 uint64_t* bar = cbar + slot;
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -443,7 +688,7 @@ vsweep_kernel(VArgs a)
                                  row_bytes, bar);
         }
     };
-    auto issue_row = [&](int i) { if (threadIdx.x == 0) issue_row_by(i); };
+    auto issue_row = [&](int i) { if (threadIdx.x == tma_thread) issue_row_by(i); };
     auto load_pin = [&](int i, uint32_t (&pa)[NR], uint32_t (&c)[NR]) {
         if (!ABL(a, 64)) mbar_wait(mbar + (i % KR), (unsigned)((i / KR) & 1));
         ASD_JITTER(5);
@@ -513,33 +758,47 @@ vsweep_kernel(VArgs a)
     // segment boundaries (nseg > 1): the last CTA of segment s and the first of
     // s+1 exchange their edge columns' diagonal states through global memory;
     // boundary b = (s, s+1); the consumer is at most one row behind or ahead
-    // (each needs the other's previous row), so two slots suffice
+    // (each needs the other's previous row), so two slots suffice.  Each word
+    // travels with its row tag (row + 1) in one 8-byte store, so a receiver that
+    // sees every tag of the slot has the whole state: no release fence on the
+    // sender (it would wait for the row's partial stores), no acquire fence.
     const int nb = nseg - 1;
+    constexpr int GQ = NR + 2;                    // tagged words per chunk and slot (state, M, pad)
     auto gh = [&](int b, int dir) {               // halo block of boundary b, direction 0 = L, 1 = R
-        return a.ghalo + ((((long long)frame * nb + b) * 2 + dir) * 2) * T * HS;
+        return a.ghalo + ((((long long)frame * nb + b) * 2 + dir) * 2) * T * GQ;
     };
-    auto gf = [&](int b, int dir) { return a.gflag + (((long long)frame * nb + b) * 2 + dir) * 8; };
     const bool gsendL = SEG && NP == 3 && nseg > 1 && rank == a.cs - 1 && seg + 1 < nseg && warp == nw - 1 && col == CPW - 1;
     const bool gsendR = SEG && NP == 3 && nseg > 1 && rank == 0 && seg > 0 && warp == 0 && col == 0;
     // warp-uniform: this warp receives a boundary halo (all its lanes wait, the
     // edge lanes read), so the shuffles after the wait stay convergent
     const bool gwL = SEG && NP == 3 && nseg > 1 && rank == 0 && seg > 0 && warp == 0;
     const bool gwR = SEG && NP == 3 && nseg > 1 && rank == a.cs - 1 && seg + 1 < nseg && warp == nw - 1;
-    // spin until the producer published row `need` - 1 (flag >= need); a trap
-    // instead of a hang if it never comes
-    // Every warp of a SEG instance runs the same poll (one asm loop, relaxed
-    // generic loads): the boundary warps on the global row counter, the others
-    // on a shared-memory word that is always 0 -- so no branch encloses the
-    // loop (a loop under a warp-dependent branch makes the compiler guard every
-    // later shuffle of the row with WARPSYNC); the boundary warps then fence.
-    __shared__ uint32_t gzero;
-    if (SEG && threadIdx.x == 0) gzero = 0u;
-    auto gpoll = [&](const uint32_t* f, int need) {
-        asm volatile("{\n .reg .pred P, Q;\n .reg .u32 V;\n GWAIT_%=:\n"
-                     " ld.relaxed.gpu.u32 V, [%0];\n"
-                     " setp.lt.s32 P, V, %1;\n"
-                     " vote.sync.any.pred Q, P, 0xffffffff;\n"
-                     " @Q bra.uni GWAIT_%=;\n}\n" :: "l"(f), "r"(need) : "memory");
+    // Segment boundary, row i (i >= 1): row i-1 of the neighbouring segment's
+    // edge column into this warp's own (otherwise unused) halo slot (i + 1) & 1
+    // -- received at the end of row i-1, before the cluster wait, so its L2
+    // round trip overlaps the barrier; at i = 0 the slot holds its initial
+    // zeros (outside predecessor).
+    auto grecv = [&](int i) {
+        const int rs = (i + 1) & 1;
+        const bool gw = (gwL || gwR) && i > 0 && i < H;
+        const bool rcv = gw && ((gwL && col == 0) || (gwR && col == CPW - 1));
+        const unsigned long long* src = (gwL ? gh(seg - 1, 0) : gh(seg, 1)) + (rs * T + chunk) * GQ;
+        uint32_t* dst = (gwL ? hL : hR) + ((rs * nw + warp) * T + chunk) * HS;
+        // stage: the warp's K_up output block (free between partial_out and
+        // the next row's), GQ tagged words per chunk
+        gseg_recv<GQ / 2>(gw, rcv, src, smem_u32(dst), (unsigned)i, smem_u32(stg) + chunk * GQ * 8);
+        ASD_JITTER(9);
+    };
+    // tagged 8-byte stores of one chunk's state (row i, tag i + 1)
+    auto gsend = [&](unsigned long long* h, const uint32_t (&Lx)[NR], uint32_t Mx, int i) {
+        const unsigned long long t = (unsigned long long)(unsigned)(i + 1) << 32;
+#pragma unroll
+        for (int q = 0; q < GQ / 2; ++q) {
+            const uint32_t lo = 2 * q < NR ? Lx[2 * q] : Mx;
+            const uint32_t hi = 2 * q + 1 < NR ? Lx[2 * q + 1] : Mx;
+            asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};\n"
+                         :: "l"(h + 2 * q), "l"(t | lo), "l"(t | hi) : "memory");
+        }
     };
 
     uint32_t Lv[NR], Ll[NR], Lr[NR];
@@ -553,66 +812,35 @@ vsweep_kernel(VArgs a)
     // diagonal paths of row i from the predecessors of row i-1 (halo slot rs)
     auto diagonals = [&](int i) {
         const int rs = (i + 1) & 1;              // slot written at row i-1
-        if (SEG) {                               // segment boundary: row i-1 published?
-            gpoll(gwL ? gf(seg - 1, 0) : &gzero, gwL ? i : 0);
-            gpoll(gwR ? gf(seg, 1) : &gzero, gwR ? i : 0);
-            if (gwL || gwR) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-        }
         uint32_t Pp[NR], Mp;
         // path "L": predecessor column x-1 (down-right / up-right)
 #pragma unroll
         for (int k = 0; k < NR; ++k) Pp[k] = __shfl_up_sync(FULL, Ll[k], T);
         Mp = __shfl_up_sync(FULL, Ml, T);
-        if (gwL && col == 0) {                   // from the previous segment, row i-1
-            if (i > 0) {
-                const uint32_t* h = gh(seg - 1, 0) + (rs * T + chunk) * HS;
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) {
-                    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(h) + q);
-                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
-                }
-                Mp = __ldcg(gh(seg - 1, 0) + (rs * T) * HS + NR);
-            } else {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) Pp[k] = 0u;
-                Mp = 0u;
-            }
-        } else if (col == 0) {
-            const uint4* h = reinterpret_cast<const uint4*>(hL + ((rs * nw + warp) * T + chunk) * HS);
+        if (col == 0) {
+            const uint32_t* hs = hL + ((rs * nw + warp) * T + chunk) * HS;
+            const uint4* h = reinterpret_cast<const uint4*>(hs);
 #pragma unroll
             for (int q = 0; q < NR / 4; ++q) {
                 const uint4 v = h[q];
                 Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
             }
-            Mp = hLM[rs * nw + warp];
+            Mp = (SEG && gwL) ? hs[NR] : hLM[rs * nw + warp];
         }
         path_update<NR, T>(p, chunk, Pp, Mp, C, Ll, Ml);
         // path "R": predecessor column x+1 (down-left / up-left)
 #pragma unroll
         for (int k = 0; k < NR; ++k) Pp[k] = __shfl_down_sync(FULL, Lr[k], T);
         Mp = __shfl_down_sync(FULL, Mr, T);
-        if (gwR && col == CPW - 1) {             // from the next segment, row i-1
-            if (i > 0) {
-                const uint32_t* h = gh(seg, 1) + (rs * T + chunk) * HS;
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q) {
-                    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(h) + q);
-                    Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
-                }
-                Mp = __ldcg(gh(seg, 1) + (rs * T) * HS + NR);
-            } else {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) Pp[k] = 0u;
-                Mp = 0u;
-            }
-        } else if (col == CPW - 1) {
-            const uint4* h = reinterpret_cast<const uint4*>(hR + ((rs * nw + warp) * T + chunk) * HS);
+        if (col == CPW - 1) {
+            const uint32_t* hs = hR + ((rs * nw + warp) * T + chunk) * HS;
+            const uint4* h = reinterpret_cast<const uint4*>(hs);
 #pragma unroll
             for (int q = 0; q < NR / 4; ++q) {
                 const uint4 v = h[q];
                 Pp[4 * q] = v.x; Pp[4 * q + 1] = v.y; Pp[4 * q + 2] = v.z; Pp[4 * q + 3] = v.w;
             }
-            Mp = hRM[rs * nw + warp];
+            Mp = (SEG && gwR) ? hs[NR] : hRM[rs * nw + warp];
         }
         path_update<NR, T>(p, chunk, Pp, Mp, C, Lr, Mr);
         // columns beyond the image act as "outside" predecessors: zero state
@@ -638,30 +866,9 @@ vsweep_kernel(VArgs a)
             for (int q = 0; q < NR / 4; ++q) d4[q] = make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]);
             if (chunk == 0) wRm[ws * nw] = Mr;
         }
-        if (SEG && nseg > 1 && (warp == 0 || warp == nw - 1)) {
-            // segment boundary: halo to global memory, fence, then the row
-            // counter (one lane per direction, after the warp's stores)
-            if (gsendL) {
-                uint32_t* h = gh(seg, 0) + (ws * T + chunk) * HS;
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q)
-                    __stcg(reinterpret_cast<uint4*>(h) + q, make_uint4(Ll[4 * q], Ll[4 * q + 1], Ll[4 * q + 2], Ll[4 * q + 3]));
-                if (chunk == 0) __stcg(h + NR, Ml);
-            }
-            if (gsendR) {
-                uint32_t* h = gh(seg - 1, 1) + (ws * T + chunk) * HS;
-#pragma unroll
-                for (int q = 0; q < NR / 4; ++q)
-                    __stcg(reinterpret_cast<uint4*>(h) + q, make_uint4(Lr[4 * q], Lr[4 * q + 1], Lr[4 * q + 2], Lr[4 * q + 3]));
-                if (chunk == 0) __stcg(h + NR, Mr);
-            }
-            if (gsendL || gsendR) __threadfence();
-            __syncwarp();
-            if (chunk == 0 && gsendL)
-                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" :: "l"(gf(seg, 0)), "r"((unsigned)(i + 1)) : "memory");
-            if (chunk == 0 && gsendR)
-                asm volatile("st.release.gpu.global.u32 [%0], %1;\n" :: "l"(gf(seg - 1, 1)), "r"((unsigned)(i + 1)) : "memory");
-        }
+        // segment boundary: the edge column's state as tagged words
+        if (gsendL) gsend(gh(seg, 0) + (ws * T + chunk) * GQ, Ll, Ml, i);
+        if (gsendR) gsend(gh(seg - 1, 1) + (ws * T + chunk) * GQ, Lr, Mr, i);
     };
     // vertical path: predecessor = own column
     auto vertical = [&]() {
@@ -796,6 +1003,7 @@ vsweep_kernel(VArgs a)
             if (RING) load_pin(i + 1, PA, C);
             else { cen_ready(i + 1); cost(row_of(i + 1), (i + 1) % NSLOT, C); }
         }
+        if (SEG) grecv(i + 1);
     }
     wait();                                          // pairs with the last arrive
     if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
@@ -2065,16 +2273,12 @@ bool v2_plan(const DevParams& p, int device, V2Plan& pl)
     return true;
 }
 
-// Segment-boundary exchange buffers (nseg > 1) for nframes frames in flight.
-size_t v2_gflag_bytes(const V2Plan& pl, int nframes)
-{
-    const int nb = pl.ncta / (pl.cs > 0 ? pl.cs : 1) - 1;
-    return nb > 0 ? (size_t)nframes * nb * 2 * 8 * sizeof(uint32_t) : 0;
-}
+// Segment-boundary exchange buffer (nseg > 1) for nframes frames in flight:
+// [frames][nseg-1][2 dirs][2 slots][T][NR + 2] tagged u64 words.
 size_t v2_ghalo_bytes(const V2Plan& pl, int nframes)
 {
     const int nb = pl.ncta / (pl.cs > 0 ? pl.cs : 1) - 1;
-    return nb > 0 ? (size_t)nframes * nb * 2 * 2 * pl.T * (pl.DC / 2 + 4) * sizeof(uint32_t) : 0;
+    return nb > 0 ? (size_t)nframes * nb * 2 * 2 * pl.T * (pl.DC / 2 + 2) * sizeof(unsigned long long) : 0;
 }
 
 // The WTA kernel's window: rows [256t, 256t + 255 + min + D - 1] of stage t.
@@ -2143,10 +2347,10 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     if (stage == 0 || stage == 1) {
         VArgs a{};
         a.p = p; a.w = pl.w; a.cs = pl.cs; a.ncta = pl.ncta;
-        a.gflag = pl.gflag; a.ghalo = pl.ghalo;
+        a.ghalo = pl.ghalo;
         a.tma_cen = stage == 0 && pl.tma_cen;
-        if (pl.ncta > pl.cs && pl.NP == 3)       // segment-boundary row counters start at 0 each launch
-            cudaMemsetAsync(pl.gflag, 0, v2_gflag_bytes(pl, nframes), s);
+        if (pl.ncta > pl.cs && pl.NP == 3)       // segment-boundary tags start at 0 (no row) each launch
+            cudaMemsetAsync(pl.ghalo, 0, v2_ghalo_bytes(pl, nframes), s);
         a.cl = (const uint32_t*)cl; a.cr = (const uint32_t*)cr; a.sig_stride = sig_stride;
 #ifdef ASD_ABLATE
         static const int ablate = getenv("ASD_V2_ABLATE") ? atoi(getenv("ASD_V2_ABLATE")) : 0;
@@ -2156,8 +2360,18 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
         a.pa_stride = (long long)p.H * pl.ncta * pl.w * p.D;
         a.pout16 = pab; a.cell_stride = cell_stride;
         a.cbin = cbin;
-        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1, pl.blk,
-                                 pl.NP == 3 && pl.ncta > pl.cs);
+        bool segk = pl.NP == 3 && pl.ncta > pl.cs;
+#ifdef ASD_ABLATE
+        if (getenv("ASD_V2_FORCESEG") && pl.NP == 3) segk = true;   // experiment: SEG instance on one segment
+#endif
+        VKernel k = pick_vkernel(pl.DC, pl.T, pl.DPL, pl.NP, stage == 1, stage == 0 && variant == 1, pl.blk, segk);
+#ifdef ASD_ABLATE
+        if (getenv("ASD_V2_FORCESEG")) {
+            cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(stage == 1 ? pl.vsmem_up : pl.vsmem));
+            cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
+#endif
         return launch_vsweep(k, pl, nframes, a, stage == 1, s) == cudaSuccess ? 0 : -1;
     }
     (void)agg;

@@ -19,8 +19,14 @@ ap.add_argument("--timeline", action="store_true", help="print the per-launch ti
 ap.add_argument("--group", type=int, default=0, help="D3 pipeline group (frames); 0 = default")
 ap.add_argument("--block", type=int, default=1, help="SGBM block (P1/P2 scaled by its area)")
 ap.add_argument("--lr-mode", type=int, default=0)
+ap.add_argument("--width", type=int, default=0, help="override the configuration's width (synthetic scene rescaled)")
+ap.add_argument("--height", type=int, default=0)
 args = ap.parse_args()
 cfg = synth.CONFIGS[args.config]
+if args.width or args.height:
+    w, h = args.width or cfg.width, args.height or cfg.height
+    cfg = synth.StereoConfig(cfg.name + "'", w, h, cfg.num_disp, cfg.census_w, cfg.census_h, cfg.paths,
+                             cfg.focal_px * w / cfg.width, tag=cfg.tag)
 d = cfg.params_dict()
 if args.paths:
     d["paths"] = args.paths
