@@ -243,6 +243,9 @@ __device__ __forceinline__ int stg_swz(int pi)
 // a bank offset of k*(DC + 32/T) mod 32 so the T chunks of a column never hit
 // the same bank.  Three slots (rows i, i+1, i+2 in flight).
 // experiment switches (A/B builds, tools/ab_bench.sh); production uses the defaults
+#ifndef ASD_GSEG_PRE         // segment-boundary receive copies issued after the previous row's output
+#define ASD_GSEG_PRE 1
+#endif
 #ifndef ASD_HROWB_SG
 #define ASD_HROWB_SG 4            // SGBM row pass: pixels per register-buffered load group
 #endif
@@ -291,12 +294,13 @@ struct VGeom {
 // warp-uniform): the receiving lanes copy NQ pairs of tagged words from src
 // to a private shared stage with cp.async (all in flight at once, no
 // registers held), then move their low halves to dst; the warp retries until
-// every tag equals `tag` (and traps after 2^24 tries instead of hanging).  The loop lives in one asm block (uniform branches
+// every tag equals `tag` (and traps after 2^24 tries instead of hanging).
+// pre: the first copies were issued earlier (gseg_issue), only wait for them.  The loop lives in one asm block (uniform branches
 // only), so no data-dependent loop encloses the row's shuffles.
 template <int NQ> struct GsegRecv;
 template <> struct GsegRecv<5> {
     static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
-                                               unsigned tag, unsigned stage)
+                                               unsigned tag, unsigned stage, bool pre)
     {
         asm volatile("{\n"
                      " .reg .pred R, P, Q;\n"
@@ -306,6 +310,8 @@ template <> struct GsegRecv<5> {
                      " @Q bra.uni GD_%=;\n"
                      " setp.ne.u32 R, %1, 0;\n"
                      " mov.b32 N, 0;\n"
+                     " setp.ne.u32 P, %6, 0;\n"
+                     " @P bra.uni GW_%=;\n"
                      "GR_%=:\n"
                      " @R cp.async.cg.shared.global [%5+0], [%2+0], 16;\n"
                      " @R cp.async.cg.shared.global [%5+16], [%2+16], 16;\n"
@@ -313,6 +319,7 @@ template <> struct GsegRecv<5> {
                      " @R cp.async.cg.shared.global [%5+48], [%2+48], 16;\n"
                      " @R cp.async.cg.shared.global [%5+64], [%2+64], 16;\n"
                      " cp.async.commit_group;\n"
+                     "GW_%=:\n"
                      " cp.async.wait_group 0;\n"
                      " setp.ne.u32 P, %1, %1;\n"
                      " @R ld.shared.v2.b64 {A, B}, [%5+0];\n"
@@ -351,13 +358,13 @@ template <> struct GsegRecv<5> {
                      " @P trap;\n"
                      " @Q bra.uni GR_%=;\n"
                      "GD_%=:\n"
-                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage)
-                     : "memory");
+                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage),
+                     "r"((unsigned)pre) : "memory");
     }
 };
 template <> struct GsegRecv<7> {
     static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
-                                               unsigned tag, unsigned stage)
+                                               unsigned tag, unsigned stage, bool pre)
     {
         asm volatile("{\n"
                      " .reg .pred R, P, Q;\n"
@@ -367,6 +374,8 @@ template <> struct GsegRecv<7> {
                      " @Q bra.uni GD_%=;\n"
                      " setp.ne.u32 R, %1, 0;\n"
                      " mov.b32 N, 0;\n"
+                     " setp.ne.u32 P, %6, 0;\n"
+                     " @P bra.uni GW_%=;\n"
                      "GR_%=:\n"
                      " @R cp.async.cg.shared.global [%5+0], [%2+0], 16;\n"
                      " @R cp.async.cg.shared.global [%5+16], [%2+16], 16;\n"
@@ -376,6 +385,7 @@ template <> struct GsegRecv<7> {
                      " @R cp.async.cg.shared.global [%5+80], [%2+80], 16;\n"
                      " @R cp.async.cg.shared.global [%5+96], [%2+96], 16;\n"
                      " cp.async.commit_group;\n"
+                     "GW_%=:\n"
                      " cp.async.wait_group 0;\n"
                      " setp.ne.u32 P, %1, %1;\n"
                      " @R ld.shared.v2.b64 {A, B}, [%5+0];\n"
@@ -426,13 +436,13 @@ template <> struct GsegRecv<7> {
                      " @P trap;\n"
                      " @Q bra.uni GR_%=;\n"
                      "GD_%=:\n"
-                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage)
-                     : "memory");
+                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage),
+                     "r"((unsigned)pre) : "memory");
     }
 };
 template <> struct GsegRecv<9> {
     static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
-                                               unsigned tag, unsigned stage)
+                                               unsigned tag, unsigned stage, bool pre)
     {
         asm volatile("{\n"
                      " .reg .pred R, P, Q;\n"
@@ -442,6 +452,8 @@ template <> struct GsegRecv<9> {
                      " @Q bra.uni GD_%=;\n"
                      " setp.ne.u32 R, %1, 0;\n"
                      " mov.b32 N, 0;\n"
+                     " setp.ne.u32 P, %6, 0;\n"
+                     " @P bra.uni GW_%=;\n"
                      "GR_%=:\n"
                      " @R cp.async.cg.shared.global [%5+0], [%2+0], 16;\n"
                      " @R cp.async.cg.shared.global [%5+16], [%2+16], 16;\n"
@@ -453,6 +465,7 @@ template <> struct GsegRecv<9> {
                      " @R cp.async.cg.shared.global [%5+112], [%2+112], 16;\n"
                      " @R cp.async.cg.shared.global [%5+128], [%2+128], 16;\n"
                      " cp.async.commit_group;\n"
+                     "GW_%=:\n"
                      " cp.async.wait_group 0;\n"
                      " setp.ne.u32 P, %1, %1;\n"
                      " @R ld.shared.v2.b64 {A, B}, [%5+0];\n"
@@ -515,15 +528,15 @@ template <> struct GsegRecv<9> {
                      " @P trap;\n"
                      " @Q bra.uni GR_%=;\n"
                      "GD_%=:\n"
-                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage)
-                     : "memory");
+                     "}\n" :: "r"((unsigned)gw), "r"((unsigned)recv), "l"(src), "r"(dst), "r"(tag), "r"(stage),
+                     "r"((unsigned)pre) : "memory");
     }
 };
 template <int NQ>
 __device__ __forceinline__ void gseg_recv(bool gw, bool recv, const unsigned long long* src, unsigned dst,
-                                          unsigned tag, unsigned stage)
+                                          unsigned tag, unsigned stage, bool pre)
 {
-    GsegRecv<NQ>::run(gw, recv, src, dst, tag, stage);
+    GsegRecv<NQ>::run(gw, recv, src, dst, tag, stage, pre);
 }
 
 template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false, bool SEG = false>
@@ -786,8 +799,22 @@ vsweep_kernel(VArgs a)
         uint32_t* dst = (gwL ? hL : hR) + ((rs * nw + warp) * T + chunk) * HS;
         // stage: the warp's K_up output block (free between partial_out and
         // the next row's), GQ tagged words per chunk
-        gseg_recv<GQ / 2>(gw, rcv, src, smem_u32(dst), (unsigned)i, smem_u32(stg) + chunk * GQ * 8);
+        gseg_recv<GQ / 2>(gw, rcv, src, smem_u32(dst), (unsigned)i, smem_u32(stg) + chunk * GQ * 8, ASD_GSEG_PRE != 0);
         ASD_JITTER(9);
+    };
+    // the first copies of row i's receive, issued after the previous row's
+    // partial-sum output (the staging block is free from then on)
+    auto gissue = [&](int i) {
+        const bool gw = (gwL || gwR) && i > 0 && i < H;
+        if (gw && ((gwL && col == 0) || (gwR && col == CPW - 1))) {
+            const int rs = (i + 1) & 1;
+            const unsigned long long* src = (gwL ? gh(seg - 1, 0) : gh(seg, 1)) + (rs * T + chunk) * GQ;
+            const unsigned st = smem_u32(stg) + chunk * GQ * 8;
+#pragma unroll
+            for (int q = 0; q < GQ / 2; ++q)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(st + 16 * q), "l"(src + 2 * q) : "memory");
+        }
+        if (gw) cp_async_commit();
     };
     // tagged 8-byte stores of one chunk's state (row i, tag i + 1)
     auto gsend = [&](unsigned long long* h, const uint32_t (&Lx)[NR], uint32_t Mx, int i) {
@@ -998,6 +1025,7 @@ vsweep_kernel(VArgs a)
         issue_row(i + KR);                            // ring input: row i's slot is free now
         // ---- partial sum out (after the release so it does not wait on these stores)
         partial_out(y);
+        if (SEG && ASD_GSEG_PRE) gissue(i + 1);
         // ---- next row's cost while the barrier completes
         if (i + 1 < H) {
             if (RING) load_pin(i + 1, PA, C);
