@@ -145,15 +145,17 @@ def test_d3_envelope_p2(p2):
 
 @pytest.mark.parametrize("W,H,D,paths", [(320, 96, 96, 8), (320, 96, 96, 4), (512, 96, 256, 8),
                                          (600, 80, 256, 4), (1000, 40, 256, 8),
-                                         (1100, 48, 256, 8), (2100, 40, 128, 8)])
+                                         (1100, 48, 256, 8), (2100, 40, 128, 8),
+                                         (2300, 32, 256, 8), (4400, 24, 128, 8)])
 def test_d3_more_disparity_ranges(W, H, D, paths):
     """Engine D3 at D = 96 (DC = 24 disparities per thread, T = 4) and D = 256
     (T = 8 threads per column, 8 disparities per lane in the row kernel, the
     warp-per-pixel WTA): Table II's other disparity ranges and
     P:293's adjustable parameters.  An 8-path frame wider than one cluster
-    (16 CTAs of 64 columns at D = 256, of 128 at D = 128: the last two cases)
-    runs as two clusters joined through global memory at the boundary.
-    Every stage bit-exact."""
+    (16 CTAs of 64 columns at D = 256, of 128 at D = 128: the last four cases)
+    runs as two or four clusters joined through global memory at the
+    boundaries (tagged-word halos; a middle segment both receives from and
+    sends to each side).  Every stage bit-exact."""
     cfg = synth.StereoConfig("R", W, H, D, 9, 7, paths, 430.0 * W / 424 * D / 128, tag=12)
     left, right, _ = synth.speckle_pair(cfg, 0)
     _run(cfg.params_dict(), left, right, 3)
