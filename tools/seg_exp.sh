@@ -1,3 +1,7 @@
 #!/bin/bash
-# config D pipeline with forced cluster sizes (ablation build)
-for cs in 0 16 8 10 12; do echo "cs=$cs"; ASD_V2_CS=$cs tools/ab_line.sh "--config D --frames 32" 1 paper_2201_11924_b200/lib/variants/abl.so; done
+# sweep launch durations (ncu, serialised) at config C: with and without the per-row cluster barrier (timing only)
+L=$PWD/paper_2201_11924_b200/lib/variants/abl.so
+for ab in 0 1024; do
+  ASD_LIB=$L ASD_V2_ABLATE=$ab timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:vsweep --csv \
+    --log-file gpurun_out/cb_$ab.csv python tools/stage_times.py --frames 11 --max-batch 11 --reps 1 > /dev/null 2>&1; echo "ab=$ab rc=$?"
+done
