@@ -734,12 +734,12 @@ vsweep_kernel(VArgs a)
     auto arrive = [&]() {
         ASD_JITTER(1);
         __syncthreads();
-        if (clustered && !ABL(a, 1024)) {
+        if (clustered) {
             if (warp == 0 || warp == nw - 1) fence_cluster();
             cluster_arrive_relaxed();
         }
     };
-    auto wait = [&]() { if (clustered && !ABL(a, 1024)) cluster_wait(); ASD_JITTER(2); };
+    auto wait = [&]() { if (clustered) cluster_wait(); ASD_JITTER(2); };
 
     // halo write targets of this thread, slot 0 (slot 1 = + hslot / + nw), fixed for the kernel
     const int hslot = nw * T * HS;
@@ -1034,9 +1034,6 @@ vsweep_kernel(VArgs a)
         if (SEG) grecv(i + 1);
     }
     wait();                                          // pairs with the last arrive
-#ifdef ASD_ABLATE
-    if (clustered && ABL(a, 1024)) { cluster_arrive(); cluster_wait(); }   // timing experiment: no per-row cluster barrier
-#endif
     if (NP == 3 && a.cs > 1 && ABL(a, 1)) { cluster_arrive(); cluster_wait(); }
 }
 
