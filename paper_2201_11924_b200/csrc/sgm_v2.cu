@@ -286,17 +286,14 @@ struct VGeom {
 // staging; K_up: a CB ring beside the P_A ring), and the handoffs carry the
 // wider partials without the cost bits: K_down writes P_A (u16), K_up P_AB.
 
-// SEG: the frame spans several clusters (segments) joined through global memory
-// at their boundaries -- a separate instance, so frames in one cluster carry no
-// trace of it (a data-dependent wait loop in the row loop makes the compiler
-// guard every shuffle with WARPSYNC)
 // Segment-boundary receive (SEG instances, every warp calls it; gw is
 // warp-uniform): the receiving lanes copy NQ pairs of tagged words from src
 // to a private shared stage with cp.async (all in flight at once, no
 // registers held), then move their low halves to dst; the warp retries until
 // every tag equals `tag` (and traps after 2^24 tries instead of hanging).
-// pre: the first copies were issued earlier (gseg_issue), only wait for them.  The loop lives in one asm block (uniform branches
-// only), so no data-dependent loop encloses the row's shuffles.
+// pre: the first copies were issued earlier (gissue in the kernel), so the
+// first pass only waits for them.  The loop lives in one asm block (uniform
+// branches only), so no data-dependent loop encloses the row's shuffles.
 template <int NQ> struct GsegRecv;
 template <> struct GsegRecv<5> {
     static __device__ __forceinline__ void run(bool gw, bool recv, const unsigned long long* src, unsigned dst,
@@ -539,6 +536,10 @@ __device__ __forceinline__ void gseg_recv(bool gw, bool recv, const unsigned lon
     GsegRecv<NQ>::run(gw, recv, src, dst, tag, stage, pre);
 }
 
+// SEG: the frame spans several clusters (segments) joined through global memory
+// at their boundaries -- a separate instance, so frames in one cluster carry no
+// trace of it (a data-dependent wait loop in the row loop makes the compiler
+// guard every shuffle with WARPSYNC)
 template <int DC, int T, int NP, bool UP, int DPL_ROW, bool RR = false, bool BLK = false, bool SEG = false>
 __global__ void __launch_bounds__(DC >= 24 ? 512 : 1024, 1)
 vsweep_kernel(VArgs a)
