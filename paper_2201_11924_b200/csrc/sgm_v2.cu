@@ -255,9 +255,6 @@ __device__ __forceinline__ int stg_swz(int pi)
 #ifndef ASD_WTA_HALVES
 #define ASD_WTA_HALVES 1          // D = 256 (R1): the three-pass half-width-window WTA kernel
 #endif
-#ifndef ASD_HROW_SG
-#define ASD_HROW_SG 8             // pixels per register-buffered load group in the row kernel
-#endif
 #ifndef ASD_NSLOT
 #define ASD_NSLOT 4               // 6 and 8 measured no faster (tools/runs/d3ab.sh)
 #endif
@@ -1405,7 +1402,11 @@ constexpr int HROW_WARPS = 4;
 
 // CFROMP (R2's right-referenced pass, reading c24): the left->right path takes
 // its cost from the P_AB | C << 9 words instead of the census images.
-template <int D, bool CFROMP = false>
+// SG: pixels per register-buffered load group.  8 in general; 4 for the
+// 8-path D = 128 pipeline (config C 1966 vs 1952 frames/s), where 8 is better
+// for 4 paths (Table II D = 128: 4271 vs 4173), at D = 256 (config D 343 vs
+// 320) and for R2's cost-from-P_AB pass (1057 vs 1047).
+template <int D, bool CFROMP = false, int SG = 8>
 #ifndef ASD_HROW_MINB
 #define ASD_HROW_MINB 1               // 6 (<= 80 registers, spills) measured slower
 #endif
@@ -1417,7 +1418,6 @@ hrow_kernel(RArgs a)
 {
     using G = RowGeom<D>;
     constexpr int DPL = G::DPL, NRR = G::NRR, ACT = G::ACT;
-    constexpr int SG = ASD_HROW_SG;
     const DevParams& p = a.p;
     const int W = p.W, H = p.H;
     const int frame = blockIdx.y;
@@ -2097,8 +2097,9 @@ static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = f
     return nullptr;
 }
 
-static RKernel pick_rkernel(int D, bool cfromp = false)
+static RKernel pick_rkernel(int D, bool cfromp = false, bool eight_paths = false)
 {
+    if (D == 128 && !cfromp && eight_paths) return v2::hrow_kernel<128, false, 4>;
     if (D == 16) return cfromp ? v2::hrow_kernel<16, true> : v2::hrow_kernel<16, false>;
     if (D == 32) return cfromp ? v2::hrow_kernel<32, true> : v2::hrow_kernel<32, false>;
     if (D == 64) return cfromp ? v2::hrow_kernel<64, true> : v2::hrow_kernel<64, false>;
@@ -2412,7 +2413,7 @@ int launch_v2_stage(int stage, const DevParams& p, const V2Plan& pl, int nframes
     r.p2x2 = (uint32_t)p.p2 * 0x10001u;
     r.cb = cbin; r.cb_stride = (long long)p.H * pl.ncta * pl.w * p.D; r.wpad = pl.ncta * pl.w;
     if (stage == 2) {
-        RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1 || ASD_HROW_CFROMP);
+        RKernel k = pl.blk ? v2::hrow_blk_kernel<128> : pick_rkernel(p.D, variant == 1 || ASD_HROW_CFROMP, pl.NP == 3);
         const int hsm = pl.blk ? 0 : ASD_HROW_SMEM;
         if (hsm > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
         k<<<dim3((p.H + v2::HROW_WARPS - 1) / v2::HROW_WARPS, nframes), 32 * v2::HROW_WARPS, hsm, s>>>(r);
