@@ -1402,10 +1402,9 @@ constexpr int HROW_WARPS = 4;
 
 // CFROMP (R2's right-referenced pass, reading c24): the left->right path takes
 // its cost from the P_AB | C << 9 words instead of the census images.
-// SG: pixels per register-buffered load group.  8 in general; 4 for the
-// 8-path D = 128 pipeline (config C 1966 vs 1952 frames/s), where 8 is better
-// for 4 paths (Table II D = 128: 4271 vs 4173), at D = 256 (config D 343 vs
-// 320) and for R2's cost-from-P_AB pass (1057 vs 1047).
+// SG: pixels per register-buffered load group (4 instead of 8 gains
+// 0.3-0.5 % at config C but slows the sweeps it shares the SMs with, and loses
+// at 4 paths, D = 256 and in R2's pass)
 template <int D, bool CFROMP = false, int SG = 8>
 #ifndef ASD_HROW_MINB
 #define ASD_HROW_MINB 1               // 6 (<= 80 registers, spills) measured slower
@@ -2099,7 +2098,7 @@ static VKernel pick_vkernel(int DC, int T, int DPL, int np, bool up, bool rr = f
 
 static RKernel pick_rkernel(int D, bool cfromp = false, bool eight_paths = false)
 {
-    if (D == 128 && !cfromp && eight_paths) return v2::hrow_kernel<128, false, 4>;
+    (void)eight_paths;
     if (D == 16) return cfromp ? v2::hrow_kernel<16, true> : v2::hrow_kernel<16, false>;
     if (D == 32) return cfromp ? v2::hrow_kernel<32, true> : v2::hrow_kernel<32, false>;
     if (D == 64) return cfromp ? v2::hrow_kernel<64, true> : v2::hrow_kernel<64, false>;
