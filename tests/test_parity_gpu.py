@@ -172,3 +172,14 @@ def test_d3_two_segment_variants(variant):
     d.update({"sgbm3": dict(block_w=3, block_h=3, p1=72, p2=288), "r2": dict(lr_mode=1),
               "p2_100": dict(p2=100), "median5": dict(median_ksize=5)}[variant])
     _run(d, left, right, 3)
+
+
+@pytest.mark.parametrize("W,D,min_disp", [(2102, 128, 0), (2100, 128, 3), (1102, 256, 6)])
+def test_d3_segments_cp_async_census(W, D, min_disp):
+    """Frames spanning two clusters whose census rows are staged with 4-byte
+    cp.async instead of TMA (width not a multiple of 4, or min_disp not), so
+    the segment receive's cp.async groups interleave with the census groups
+    of the down sweep.  Every stage bit-exact."""
+    cfg = synth.StereoConfig("SC", W, 32, D, 9, 7, 8, 430.0 * W / 424 * D / 128, min_disp=min_disp, tag=14)
+    left, right, _ = synth.speckle_pair(cfg, 0)
+    _run(cfg.params_dict(), left, right, 3)

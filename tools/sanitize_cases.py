@@ -74,6 +74,9 @@ def cases():
                        "engine": 3}, 4, 4, None),
         "seg256_d3": ({**_cfg("C"), "width": 1100, "height": 48, "num_disp": 256,
                        "focal_px": 430.0 * 1100 / 424 * 2, "engine": 3}, 4, 4, None),
+        # two clusters, census staged by cp.async (width not a multiple of 4)
+        "seg128_cpa_d3": ({**_cfg("C"), "width": 2102, "height": 32, "focal_px": 430.0 * 2102 / 424,
+                           "engine": 3}, 3, 3, None),
         # four clusters per frame (middle segments receive from both sides)
         "seg4_256_d3": ({**_cfg("C"), "width": 2300, "height": 32, "num_disp": 256,
                          "focal_px": 430.0 * 2300 / 424 * 2, "engine": 3}, 3, 3, None),
